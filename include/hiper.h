@@ -1,0 +1,189 @@
+/*
+ * hiper.h -- C ABI of the B200-native ColTrast late-interaction (MaxSim) hot path.
+ *
+ * The method (HiPerRAG, arXiv 2505.04846, /root/reference/PAPER.md):
+ *   S(q, d) = sum_{i < len_q} max_{j < len_d} < q_i , d_j >                      (§2.2,
+ *   over L2-normalised token embeddings ("cosine per token pair")    PAPER.md:228 Fig.3B,
+ *                                                                                  PAPER.md:241 §3.2.1)
+ * used (i) for exact top-k retrieval over a chunk index ("semantic search in the vector database to
+ * identify the nearest neighbors", §2.3) and (ii) for the in-batch B x B score matrix of
+ * the ColTrast late-interaction loss L_LI ("L_LI is maxsim loss", §3.2.1).
+ * Readings of every gap (length masking, normalisation recipe, ties, padding) are DESIGN.md R1-R17.
+ *
+ * Conventions (all entry points):
+ *  - Never throws; every call returns hiper_status.  hiper_last_error() gives a thread-local detail
+ *    string for the last failing call on this thread.
+ *  - "device" pointers are CUDA device memory on the current device; "HOST" pointers are ordinary host
+ *    memory (read synchronously during the call, never retained).  Length arrays and pos_idx are small
+ *    HOST arrays so validation is eager; all device work is enqueued asynchronously on `stream`.
+ *  - Errors detectable on the host are returned before any launch, with outputs untouched.  A CUDA or
+ *    NCCL failure returns HIPER_ERR_CUDA / HIPER_ERR_NCCL and leaves outputs undefined.
+ *  - Token tensors are row-major [n][max_len][dim] (dim contiguous), float32 or bfloat16.  Rows
+ *    j >= len of an item are ignored (never read as zero vectors into a max, reading R2/R3).
+ *  - Scores are computed with bf16 operands and fp32 accumulation (tcgen05 tensor cores, sm_100a).
+ *  - Supported shapes (round 1): dim in {64, 128}; q_max_len <= 32; chunk max_len <= 256;
+ *    1 <= k <= 128; global ids < 2^32 - 1; n * roundup(max_len,16) < 2^31 per index.
+ *    Anything else returns HIPER_ERR_UNSUPPORTED.
+ *  - No CPU fallback exists: without an sm_100 device every compute call returns HIPER_ERR_UNSUPPORTED
+ *    or HIPER_ERR_CUDA.
+ */
+#ifndef HIPER_H_
+#define HIPER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(HIPER_BUILD)
+#define HIPER_API __attribute__((visibility("default")))
+#else
+#define HIPER_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* hiper_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  HIPER_OK = 0,
+  HIPER_ERR_INVALID_ARG = 1,     /* null pointer, k < 1, n < 0, bad flags, ... */
+  HIPER_ERR_DIM_MISMATCH = 2,    /* SPEC DimensionMismatch: query dim != index dim */
+  HIPER_ERR_EMPTY_TOKENS = 3,    /* SPEC EmptyTokenList: some len == 0 */
+  HIPER_ERR_EMPTY_BATCH = 4,     /* SPEC EmptyBatch: n_q == 0 for the loss */
+  HIPER_ERR_BAD_TEMPERATURE = 5, /* SPEC NonPositiveTemperature: tau <= 0 or not finite */
+  HIPER_ERR_BAD_POSITIVE = 6,    /* SPEC InvalidPositiveIndex */
+  HIPER_ERR_NONFINITE = 7,       /* SPEC "all entries finite" */
+  HIPER_ERR_ZERO_VECTOR = 8,     /* SPEC ZeroVector: a real row of norm 0 under NORM */
+  HIPER_ERR_OUT_OF_MEMORY = 9,
+  HIPER_ERR_CUDA = 10,
+  HIPER_ERR_NCCL = 11,
+  HIPER_ERR_UNSUPPORTED = 12,    /* shape/device outside the supported set above */
+  HIPER_ERR_WORKSPACE = 13       /* workspace NULL / too small / misaligned (needs 1024-B alignment) */
+} hiper_status;
+
+typedef enum { HIPER_F32 = 0, HIPER_BF16 = 1 } hiper_dtype;
+
+enum {
+  /* Rows are already unit-norm: skip NORM, store RNE_bf16(x) (reading R12). */
+  HIPER_ASSUME_NORMALIZED = 1u,
+  /* Reject non-finite entries (always on for hiper_index_build; opt-in for queries). */
+  HIPER_CHECK_FINITE = 2u,
+  /* hiper_index_build only: zero-copy.  The index references the caller's bf16 token buffer, which must
+   * have max_len % 16 == 0, 16-byte alignment, outlive the index and not be modified.  NORM (unless
+   * ASSUME_NORMALIZED) is applied IN PLACE and rows j >= len are zeroed in place. */
+  HIPER_BORROW_TOKENS = 4u,
+  /* Query-side calls: synchronise `stream` after query preparation and return HIPER_ERR_ZERO_VECTOR /
+   * HIPER_ERR_NONFINITE if a real query row is zero / non-finite.  Without it the same condition is
+   * recorded in the workspace status word (hiper_workspace_status) and scores are undefined. */
+  HIPER_VALIDATE_SYNC = 8u
+};
+
+typedef struct hiper_index_s hiper_index; /* opaque; immutable after build; shareable by readers */
+typedef struct hiper_comm_s hiper_comm;   /* opaque; owns one ncclComm_t */
+
+HIPER_API const char* hiper_status_string(hiper_status s);
+HIPER_API const char* hiper_last_error(void);
+HIPER_API int32_t hiper_version(void); /* major*10000 + minor*100 + patch */
+
+/* ------------------------------------------------------------------ multi-GPU (corpus sharding)
+ * One process per GPU.  Rank 0 calls hiper_comm_unique_id and broadcasts the 128 bytes (the Python
+ * binding uses torch.distributed); every rank then calls hiper_comm_create.  The communicator carries
+ * exactly one collective per query batch: an ncclAllGather of each shard's local top-k keys
+ * (BASELINE.json north_star: "merged with one NCCL all-gather over NVLink"). */
+HIPER_API hiper_status hiper_comm_unique_id(uint8_t id[128]);
+HIPER_API hiper_status hiper_comm_create(const uint8_t id[128], int32_t world, int32_t rank, int32_t device,
+                               hiper_comm** out);
+HIPER_API hiper_status hiper_comm_destroy(hiper_comm* comm);
+HIPER_API hiper_status hiper_comm_info(const hiper_comm* comm, int32_t* world, int32_t* rank);
+
+/* ------------------------------------------------------------------ step a1: corpus layout
+ * hiper_index_build: lay out a chunk corpus for scoring ("chunk embeddings are stored in a vector
+ * database ... each linked to a unique ID"; SPEC.md:184-192 build_index).
+ *   tokens  device [n][max_len][dim] (dtype), finite.
+ *   lens    HOST [n], 1 <= lens[c] <= max_len (EmptyTokenList otherwise).
+ *   id_base global id of chunk 0 of this shard; chunk c gets id id_base + c.
+ * Result layout (owned by the index unless BORROW): bf16 [n][ld_pad][dim], ld_pad = roundup(max_len,16),
+ * row j < lens[c] = NORM(tokens[c][j]) (R1), rows j >= lens[c] = 0; lens kept on device.
+ * Synchronises `stream` once at the end (build-time validation of NONFINITE / ZERO_VECTOR).
+ * n == 0 gives a valid empty index (searches return all padding). */
+HIPER_API hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype, const int32_t* lens, int64_t n,
+                               int32_t max_len, int32_t dim, int64_t id_base, uint32_t flags,
+                               hiper_stream_t stream, hiper_index** out);
+HIPER_API hiper_status hiper_index_destroy(hiper_index* idx);
+/* Any output pointer may be NULL.  layout: device bf16 [n][ld_pad][dim]; lens_dev: device int32 [n]. */
+HIPER_API hiper_status hiper_index_info(const hiper_index* idx, int64_t* n, int32_t* max_len, int32_t* dim,
+                              int32_t* ld_pad, int64_t* id_base, const void** layout,
+                              const int32_t** lens_dev);
+
+/* ------------------------------------------------------------------ step a2: query preparation
+ * NORM every real query row into the kernel's query layout: out device bf16 [n_q_pad][32][dim] with
+ * n_q_pad = roundup(n_q, 4); rows i >= q_lens[q] and queries q >= n_q are zero.  status: device
+ * uint32 (bit 0: zero row, bit 1: non-finite row), OR-ed, may be NULL.  Exposed so the layout can be
+ * checked bitwise against the oracle's NORM; the search/loss entry points call it internally. */
+HIPER_API hiper_status hiper_prepare_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
+                                   int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags,
+                                   void* out_layout, uint32_t* status, hiper_stream_t stream);
+
+/* ------------------------------------------------------------------ steps a2-a9: exact top-k
+ * hiper_maxsim_topk: for every query, the k chunks of highest S(q, c) over this shard (comm == NULL)
+ * or over all shards of `comm` (every rank passes the same queries and receives the identical global
+ * result).  Ordering: score descending, then global id ascending (R6).  When
+ * k > number of chunks the tail is (score -inf, id -1) (R7).
+ *   q_tokens device [n_q][q_max_len][dim]; q_lens HOST [n_q] in 1..q_max_len.
+ *   workspace device, >= hiper_maxsim_topk_workspace_size(idx, n_q, k, comm) bytes, 1024-B aligned,
+ *             caller-owned (e.g. torch allocator), not used concurrently by another call.
+ *   out_scores device float [n_q][k]; out_ids device int64 [n_q][k].
+ * Launches: query prep, the fused TMA/tcgen05 MaxSim + per-CTA top-k kernel, the top-k merge kernel
+ * (+ ncclAllGather and a second merge when comm != NULL). */
+HIPER_API size_t hiper_maxsim_topk_workspace_size(const hiper_index* idx, int32_t n_q, int32_t k,
+                                        const hiper_comm* comm);
+HIPER_API hiper_status hiper_maxsim_topk(const hiper_index* idx, const void* q_tokens, hiper_dtype dtype,
+                               const int32_t* q_lens, int32_t n_q, int32_t q_max_len, int32_t dim,
+                               int32_t k, uint32_t flags, const hiper_comm* comm, void* workspace,
+                               size_t workspace_bytes, float* out_scores, int64_t* out_ids,
+                               hiper_stream_t stream);
+
+/* ------------------------------------------------------------------ dense scores (test support + a10)
+ * out_scores device float [n_q][n] = S(q, c) for every query and every chunk of the index. */
+HIPER_API size_t hiper_maxsim_scores_workspace_size(const hiper_index* idx, int32_t n_q);
+HIPER_API hiper_status hiper_maxsim_scores(const hiper_index* idx, const void* q_tokens, hiper_dtype dtype,
+                                 const int32_t* q_lens, int32_t n_q, int32_t q_max_len, int32_t dim,
+                                 uint32_t flags, void* workspace, size_t workspace_bytes,
+                                 float* out_scores, hiper_stream_t stream);
+
+/* ------------------------------------------------------------------ steps a10-a11: ColTrast L_LI
+ * In-batch MaxSim scores S[i][j] = S(Q_i, D_j) (i < n_q, j < n_d) and the InfoNCE loss over them
+ * ("We apply LI loss to the local rank only"; SPEC.md:339-347 li_loss):
+ *   z_ij = S_ij / temperature;  l_i = logsumexp_j z_ij - z_{i,pos_i};  L = (1/n_q) sum_i l_i
+ * computed in fp32 with a max shift and the log1p form of DESIGN.md R13; fixed-order (deterministic)
+ * reductions.  temperature == 1 reproduces SPEC li_loss exactly (R9).
+ *   q_tokens device [n_q][q_max_len][dim], d_tokens device [n_d][d_max_len][dim] (same dtype);
+ *   q_lens / d_lens HOST; pos_idx HOST [n_q] or NULL (= diagonal, needs n_d >= n_q).
+ *   out_scores device float [n_q][n_d] or NULL; out_loss device float scalar (not NULL).
+ *   workspace >= hiper_coltrast_workspace_size(...) bytes, 1024-B aligned. */
+HIPER_API size_t hiper_coltrast_workspace_size(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim);
+HIPER_API hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const int32_t* q_lens, int32_t n_q,
+                                        int32_t q_max_len, const void* d_tokens,
+                                        const int32_t* d_lens, int32_t n_d, int32_t d_max_len,
+                                        int32_t dim, hiper_dtype dtype, uint32_t flags,
+                                        const int32_t* pos_idx, float temperature,
+                                        void* workspace, size_t workspace_bytes,
+                                        float* out_scores, float* out_loss, hiper_stream_t stream);
+
+/* Loss kernel alone over a given device score matrix S [n_q][n_d] (test support: isolates a11). */
+HIPER_API hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,
+                                const int32_t* pos_idx, float temperature, void* workspace,
+                                size_t workspace_bytes, float* out_loss, hiper_stream_t stream);
+
+/* Synchronise `stream` and report the device-side status word of a query-side workspace:
+ * HIPER_OK, HIPER_ERR_ZERO_VECTOR or HIPER_ERR_NONFINITE. */
+HIPER_API hiper_status hiper_workspace_status(const void* workspace, hiper_stream_t stream);
+
+/* Number of kernels the last successful compute call on this thread enqueued (bench evidence). */
+HIPER_API int32_t hiper_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIPER_H_ */

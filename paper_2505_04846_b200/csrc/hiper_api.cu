@@ -1,0 +1,853 @@
+// hiper_api.cu -- host side of the C ABI declared in include/hiper.h.
+//
+// Validation (eager, on host arrays), workspace carving, TMA tensor-map encoding, launches and the
+// NCCL all-gather.  No computation of the method happens on the host: every step runs in the kernels
+// under kernels/.  There is no CPU fallback: without an sm_100 device every compute entry point fails.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+
+#include "../../include/hiper.h"
+#include "kernels/infonce.cuh"
+#include "kernels/maxsim_sm100.cuh"
+#include "kernels/norm_layout.cuh"
+#include "kernels/topk_merge.cuh"
+
+using namespace hiper;
+
+// ============================================================================ errors
+static thread_local std::string g_last_error;
+static thread_local int32_t g_launches = 0;
+
+static hiper_status fail(hiper_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(_e == cudaErrorMemoryAllocation ? HIPER_ERR_OUT_OF_MEMORY : HIPER_ERR_CUDA, \
+                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__);       \
+  } while (0)
+
+#define TRY(expr)                        \
+  do {                                   \
+    hiper_status _s = (expr);            \
+    if (_s != HIPER_OK) return _s;       \
+  } while (0)
+
+extern "C" const char* hiper_status_string(hiper_status s) {
+  switch (s) {
+    case HIPER_OK: return "HIPER_OK";
+    case HIPER_ERR_INVALID_ARG: return "HIPER_ERR_INVALID_ARG";
+    case HIPER_ERR_DIM_MISMATCH: return "HIPER_ERR_DIM_MISMATCH";
+    case HIPER_ERR_EMPTY_TOKENS: return "HIPER_ERR_EMPTY_TOKENS";
+    case HIPER_ERR_EMPTY_BATCH: return "HIPER_ERR_EMPTY_BATCH";
+    case HIPER_ERR_BAD_TEMPERATURE: return "HIPER_ERR_BAD_TEMPERATURE";
+    case HIPER_ERR_BAD_POSITIVE: return "HIPER_ERR_BAD_POSITIVE";
+    case HIPER_ERR_NONFINITE: return "HIPER_ERR_NONFINITE";
+    case HIPER_ERR_ZERO_VECTOR: return "HIPER_ERR_ZERO_VECTOR";
+    case HIPER_ERR_OUT_OF_MEMORY: return "HIPER_ERR_OUT_OF_MEMORY";
+    case HIPER_ERR_CUDA: return "HIPER_ERR_CUDA";
+    case HIPER_ERR_NCCL: return "HIPER_ERR_NCCL";
+    case HIPER_ERR_UNSUPPORTED: return "HIPER_ERR_UNSUPPORTED";
+    case HIPER_ERR_WORKSPACE: return "HIPER_ERR_WORKSPACE";
+  }
+  return "HIPER_ERR_UNKNOWN";
+}
+extern "C" const char* hiper_last_error(void) { return g_last_error.c_str(); }
+extern "C" int32_t hiper_version(void) { return 100; }
+extern "C" int32_t hiper_last_launch_count(void) { return g_launches; }
+
+// ============================================================================ device helpers
+struct DevInfo {
+  int device = -1;
+  int num_sms = 0;
+  int max_smem = 0;
+};
+
+static hiper_status device_info(DevInfo& di) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  int major = 0, minor = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (major != 10 || minor != 0)
+    return fail(HIPER_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a only", dev,
+                major, minor);
+  di.device = dev;
+  CUDA_TRY(cudaDeviceGetAttribute(&di.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&di.max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  return HIPER_OK;
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static hiper_status get_encode_fn(PFN_encodeTiled* fn) {
+  static PFN_encodeTiled cached = nullptr;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (err == cudaSuccess && q == cudaDriverEntryPointSuccess) cached = (PFN_encodeTiled)p;
+  });
+  if (!cached) return fail(HIPER_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(err));
+  *fn = cached;
+  return HIPER_OK;
+}
+
+// 2-D bf16 tensor map over rows of `dim` elements, box = 64 elements x box_rows rows, 128B swizzle.
+static hiper_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int32_t dim,
+                              int32_t box_rows) {
+  PFN_encodeTiled enc;
+  TRY(get_encode_fn(&enc));
+  cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)dim * 2};
+  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(HIPER_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld dim=%d box_rows=%d",
+                (int)r, (long long)rows, dim, box_rows);
+  return HIPER_OK;
+}
+
+// ---------------------------------------------------------------------------- pinned staging ring
+// Small HOST arrays (lengths, positives) go to the device through pinned slots so the copy is truly
+// asynchronous; a slot is reused only after the event of its previous copy completed.
+namespace {
+struct StageSlot {
+  void* pinned = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool used = false;
+};
+struct StageRing {
+  std::mutex mu;
+  StageSlot slot[16];
+  int next = 0;
+};
+StageRing g_rings[64];
+}  // namespace
+
+static hiper_status stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return HIPER_OK;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  StageRing& ring = g_rings[dev & 63];
+  std::lock_guard<std::mutex> lock(ring.mu);
+  StageSlot& s = ring.slot[ring.next];
+  ring.next = (ring.next + 1) % 16;
+  if (s.ev == nullptr) CUDA_TRY(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  if (s.used) CUDA_TRY(cudaEventSynchronize(s.ev));
+  if (s.cap < bytes) {
+    if (s.pinned) CUDA_TRY(cudaFreeHost(s.pinned));
+    s.pinned = nullptr;
+    size_t cap = std::max<size_t>(bytes, 65536);
+    CUDA_TRY(cudaHostAlloc(&s.pinned, cap, cudaHostAllocDefault));
+    s.cap = cap;
+  }
+  memcpy(s.pinned, src, bytes);
+  CUDA_TRY(cudaMemcpyAsync(dst, s.pinned, bytes, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaEventRecord(s.ev, stream));
+  s.used = true;
+  return HIPER_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ============================================================================ the index
+struct hiper_index_s {
+  int64_t n = 0;
+  int32_t max_len = 0, ld_pad = 0, dim = 0;
+  int64_t id_base = 0;
+  int device = -1;
+  __nv_bfloat16* tok = nullptr;  // [n][ld_pad][dim]
+  bool owns_tok = false;
+  int32_t* lens = nullptr;  // device [n]
+  alignas(64) CUtensorMap tmap;
+};
+
+static hiper_status check_dims(int32_t dim) {
+  if (dim <= 0) return fail(HIPER_ERR_INVALID_ARG, "dim must be positive (got %d)", dim);
+  if (dim != 64 && dim != 128)
+    return fail(HIPER_ERR_UNSUPPORTED, "dim %d unsupported (round 1 supports 64 and 128)", dim);
+  return HIPER_OK;
+}
+
+static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src, int32_t in_rows,
+                                const int32_t* lens_dev, int64_t n_items, int32_t out_rows,
+                                int32_t dim, uint32_t flags, __nv_bfloat16* out, uint32_t* status,
+                                cudaStream_t stream) {
+  const int64_t rows = n_items * (int64_t)out_rows;
+  if (rows == 0) return HIPER_OK;
+  const int threads = 256;
+  const int64_t blocks = (rows + threads - 1) / threads;
+  if (blocks > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
+  const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
+  const uint32_t cf = (flags & HIPER_CHECK_FINITE) ? 1u : 0u;
+  if (dtype == HIPER_F32)
+    norm_layout_kernel<float><<<(unsigned)blocks, threads, 0, stream>>>(
+        (const float*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out, status);
+  else
+    norm_layout_kernel<__nv_bfloat16><<<(unsigned)blocks, threads, 0, stream>>>(
+        (const __nv_bfloat16*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out,
+        status);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return HIPER_OK;
+}
+
+static hiper_status check_lens(const int32_t* lens, int64_t n, int32_t max_len, const char* what) {
+  if (n > 0 && lens == nullptr) return fail(HIPER_ERR_INVALID_ARG, "%s lens is NULL", what);
+  for (int64_t i = 0; i < n; ++i) {
+    if (lens[i] == 0) return fail(HIPER_ERR_EMPTY_TOKENS, "%s %lld has 0 tokens", what, (long long)i);
+    if (lens[i] < 0 || lens[i] > max_len)
+      return fail(HIPER_ERR_INVALID_ARG, "%s %lld length %d outside 1..%d", what, (long long)i,
+                  lens[i], max_len);
+  }
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype, const int32_t* lens,
+                                          int64_t n, int32_t max_len, int32_t dim, int64_t id_base,
+                                          uint32_t flags, hiper_stream_t stream_, hiper_index** out) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!out) return fail(HIPER_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 0) return fail(HIPER_ERR_INVALID_ARG, "n < 0");
+  if (dtype != HIPER_F32 && dtype != HIPER_BF16) return fail(HIPER_ERR_INVALID_ARG, "bad dtype");
+  if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_BORROW_TOKENS))
+    return fail(HIPER_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  TRY(check_dims(dim));
+  if (max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "max_len must be >= 1");
+  if (max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "max_len %d > 256", max_len);
+  if (id_base < 0 || id_base + n >= 0xFFFFFFFFll)
+    return fail(HIPER_ERR_UNSUPPORTED, "global ids must be < 2^32-1");
+  const int32_t ld_pad = (int32_t)round_up(max_len, 16);
+  if (n * ld_pad >= 0x7FFFFFFFll)
+    return fail(HIPER_ERR_UNSUPPORTED, "n * ld_pad >= 2^31 rows for one index; shard the corpus");
+  TRY(check_lens(lens, n, max_len, "chunk"));
+  const bool borrow = (flags & HIPER_BORROW_TOKENS) != 0;
+  if (borrow && (dtype != HIPER_BF16 || max_len != ld_pad))
+    return fail(HIPER_ERR_INVALID_ARG, "HIPER_BORROW_TOKENS needs bf16 tokens and max_len %% 16 == 0");
+  if (n > 0) {
+    if (!tokens) return fail(HIPER_ERR_INVALID_ARG, "tokens is NULL");
+    if (((uintptr_t)tokens & 15) != 0) return fail(HIPER_ERR_INVALID_ARG, "tokens must be 16-B aligned");
+    if (!is_device_ptr(tokens)) return fail(HIPER_ERR_INVALID_ARG, "tokens must be device memory");
+  }
+  DevInfo di;
+  TRY(device_info(di));
+
+  hiper_index_s* ix = new hiper_index_s();
+  ix->n = n;
+  ix->max_len = max_len;
+  ix->ld_pad = ld_pad;
+  ix->dim = dim;
+  ix->id_base = id_base;
+  ix->device = di.device;
+  auto cleanup = [&](hiper_status s) {
+    if (ix->owns_tok && ix->tok) cudaFree(ix->tok);
+    if (ix->lens) cudaFree(ix->lens);
+    delete ix;
+    return s;
+  };
+  const int64_t n_alloc = std::max<int64_t>(n, 1);
+  if (cudaMalloc(&ix->lens, n_alloc * sizeof(int32_t)) != cudaSuccess)
+    return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "lens alloc"));
+  if (borrow) {
+    ix->tok = (__nv_bfloat16*)const_cast<void*>(tokens);
+  } else {
+    if (cudaMalloc(&ix->tok, (size_t)n_alloc * ld_pad * dim * 2) != cudaSuccess)
+      return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "layout alloc %lld bytes",
+                          (long long)n_alloc * ld_pad * dim * 2));
+    ix->owns_tok = true;
+  }
+  uint32_t* status = nullptr;
+  if (cudaMalloc(&status, sizeof(uint32_t)) != cudaSuccess)
+    return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "status alloc"));
+  hiper_status st = HIPER_OK;
+  uint32_t hstat = 0;
+  do {
+    if (cudaMemsetAsync(status, 0, sizeof(uint32_t), stream) != cudaSuccess) { st = fail(HIPER_ERR_CUDA, "memset"); break; }
+    if (n > 0 && cudaMemcpyAsync(ix->lens, lens, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream) != cudaSuccess) {
+      st = fail(HIPER_ERR_CUDA, "lens copy"); break;
+    }
+    st = launch_norm(tokens, dtype, n, max_len, ix->lens, n, ld_pad, dim,
+                     flags | HIPER_CHECK_FINITE, ix->tok, status, stream);
+    if (st != HIPER_OK) break;
+    if (cudaMemcpyAsync(&hstat, status, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess) {
+      st = fail(HIPER_ERR_CUDA, "build sync: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    if (hstat & kStatusNonFinite) { st = fail(HIPER_ERR_NONFINITE, "chunk tokens contain non-finite values"); break; }
+    if (hstat & kStatusZeroRow) { st = fail(HIPER_ERR_ZERO_VECTOR, "a chunk token row has norm 0"); break; }
+    if (n > 0) st = make_tmap(&ix->tmap, ix->tok, n * (int64_t)ld_pad, dim, ld_pad);
+  } while (0);
+  cudaFree(status);
+  if (st != HIPER_OK) return cleanup(st);
+  *out = ix;
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_index_destroy(hiper_index* ix) {
+  if (!ix) return HIPER_OK;
+  if (ix->owns_tok && ix->tok) cudaFree(ix->tok);
+  if (ix->lens) cudaFree(ix->lens);
+  delete ix;
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_index_info(const hiper_index* ix, int64_t* n, int32_t* max_len,
+                                         int32_t* dim, int32_t* ld_pad, int64_t* id_base,
+                                         const void** layout, const int32_t** lens_dev) {
+  if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
+  if (n) *n = ix->n;
+  if (max_len) *max_len = ix->max_len;
+  if (dim) *dim = ix->dim;
+  if (ld_pad) *ld_pad = ix->ld_pad;
+  if (id_base) *id_base = ix->id_base;
+  if (layout) *layout = ix->tok;
+  if (lens_dev) *lens_dev = ix->lens;
+  return HIPER_OK;
+}
+
+// ============================================================================ query preparation
+static constexpr int32_t kQSlot = 32;  // padded query-token rows per query (one warp of TMEM lanes)
+
+static int32_t n_q_pad_of(int32_t n_q) { return (int32_t)round_up(std::max(n_q, 1), 4); }
+
+static hiper_status validate_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
+                                     int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags) {
+  if (dtype != HIPER_F32 && dtype != HIPER_BF16) return fail(HIPER_ERR_INVALID_ARG, "bad dtype");
+  if (n_q < 0) return fail(HIPER_ERR_INVALID_ARG, "n_q < 0");
+  if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_VALIDATE_SYNC))
+    return fail(HIPER_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  TRY(check_dims(dim));
+  if (q_max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "q_max_len must be >= 1");
+  if (q_max_len > kQSlot) return fail(HIPER_ERR_UNSUPPORTED, "q_max_len %d > 32", q_max_len);
+  TRY(check_lens(q_lens, n_q, q_max_len, "query"));
+  if (n_q > 0) {
+    if (!q_tokens) return fail(HIPER_ERR_INVALID_ARG, "q_tokens is NULL");
+    if (((uintptr_t)q_tokens & 15) != 0) return fail(HIPER_ERR_INVALID_ARG, "q_tokens must be 16-B aligned");
+    if (!is_device_ptr(q_tokens)) return fail(HIPER_ERR_INVALID_ARG, "q_tokens must be device memory");
+  }
+  return HIPER_OK;
+}
+
+// Device-side query prep: q_lens HOST -> lens_dev (staged), NORM into layout [n_q_pad][32][dim].
+static hiper_status prep_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
+                                 int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags,
+                                 int32_t* lens_dev, __nv_bfloat16* layout, uint32_t* status,
+                                 cudaStream_t stream) {
+  TRY(stage_h2d(lens_dev, q_lens, (size_t)n_q * sizeof(int32_t), stream));
+  return launch_norm(q_tokens, dtype, n_q, q_max_len, lens_dev, n_q_pad_of(n_q), kQSlot, dim, flags,
+                     layout, status, stream);
+}
+
+static hiper_status sync_status(const uint32_t* status, cudaStream_t stream) {
+  uint32_t h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  if (h & kStatusNonFinite) return fail(HIPER_ERR_NONFINITE, "a query row is non-finite");
+  if (h & kStatusZeroRow) return fail(HIPER_ERR_ZERO_VECTOR, "a real query row has norm 0");
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_prepare_queries(const void* q_tokens, hiper_dtype dtype,
+                                              const int32_t* q_lens, int32_t n_q, int32_t q_max_len,
+                                              int32_t dim, uint32_t flags, void* out_layout,
+                                              uint32_t* status, hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
+  if (!out_layout || !is_device_ptr(out_layout)) return fail(HIPER_ERR_INVALID_ARG, "out_layout must be device memory");
+  DevInfo di;
+  TRY(device_info(di));
+  int32_t* lens_dev = nullptr;
+  CUDA_TRY(cudaMallocAsync(&lens_dev, std::max(n_q, 1) * sizeof(int32_t), stream));
+  hiper_status st = prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, lens_dev,
+                                 (__nv_bfloat16*)out_layout, status, stream);
+  cudaFreeAsync(lens_dev, stream);
+  return st;
+}
+
+// ============================================================================ the MaxSim kernel launch
+static int32_t choose_parts(int32_t n_groups, int64_t n_chunks, int num_sms) {
+  if (n_chunks <= 0) return 0;
+  const int64_t p0 = num_sms / std::gcd(n_groups, num_sms);
+  return (int32_t)std::max<int64_t>(1, std::min<int64_t>(p0, n_chunks));
+}
+
+struct KernelPlan {
+  int32_t n_groups = 0, n_parts = 0, n_stages = 0;
+  uint32_t a_bytes = 0, stage_bytes = 0, smem_bytes = 0;
+  int grid = 0;
+};
+
+static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int64_t n_chunks, int32_t ld_pad,
+                                int32_t dim, KernelPlan& kp) {
+  kp.n_groups = n_q_pad_of(n_q) / 4;
+  kp.n_parts = choose_parts(kp.n_groups, n_chunks, di.num_sms);
+  kp.a_bytes = (uint32_t)(dim / 64) * 16384u;
+  kp.stage_bytes = (uint32_t)ld_pad * 128u;
+  const uint32_t fixed = 1024u /*align slack*/ + 2u * kp.a_bytes + 512u /*barriers*/;
+  const uint32_t avail = (uint32_t)di.max_smem > fixed ? (uint32_t)di.max_smem - fixed : 0u;
+  kp.n_stages = (int32_t)std::min<uint32_t>(8u, avail / kp.stage_bytes);
+  if (kp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory for 2 stages");
+  kp.smem_bytes = fixed + kp.n_stages * kp.stage_bytes;
+  const int64_t units = (int64_t)kp.n_groups * kp.n_parts;
+  kp.grid = (int)std::min<int64_t>(units, di.num_sms);
+  return HIPER_OK;
+}
+
+template <int MODE, int KR>
+static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
+                                    const MaxsimArgs& a, cudaStream_t stream) {
+  auto kern = maxsim_sm100_kernel<MODE, KR>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
+  kern<<<kp.grid, kMaxsimThreads, kp.smem_bytes, stream>>>(tq, td, a);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return HIPER_OK;
+}
+
+static hiper_status launch_maxsim(int mode, int k, const KernelPlan& kp, const CUtensorMap& tq,
+                                  const CUtensorMap& td, const MaxsimArgs& a, cudaStream_t stream) {
+  if (kp.grid == 0) return HIPER_OK;
+  if (mode == 0) return launch_maxsim_t<0, 1>(kp, tq, td, a, stream);
+  if (k <= 32) return launch_maxsim_t<1, 1>(kp, tq, td, a, stream);
+  if (k <= 64) return launch_maxsim_t<1, 2>(kp, tq, td, a, stream);
+  return launch_maxsim_t<1, 4>(kp, tq, td, a, stream);
+}
+
+static hiper_status launch_merge(const uint64_t* lists, int32_t n_lists, int64_t list_stride,
+                                 int32_t n_q, int64_t q_stride, int32_t k, uint64_t* out_keys,
+                                 float* out_scores, int64_t* out_ids, cudaStream_t stream) {
+  if (n_q == 0) return HIPER_OK;
+  const int threads = 256, qpb = threads / 32;
+  const int blocks = (n_q + qpb - 1) / qpb;
+  if (k <= 32)
+    topk_merge_kernel<1><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids);
+  else if (k <= 64)
+    topk_merge_kernel<2><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids);
+  else
+    topk_merge_kernel<4><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return HIPER_OK;
+}
+
+// ============================================================================ communicator
+struct hiper_comm_s {
+  ncclComm_t comm = nullptr;
+  int32_t world = 1, rank = 0, device = 0;
+};
+
+#define NCCL_TRY(expr)                                                                          \
+  do {                                                                                          \
+    ncclResult_t _r = (expr);                                                                   \
+    if (_r != ncclSuccess)                                                                      \
+      return fail(HIPER_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(_r), __FILE__, __LINE__); \
+  } while (0)
+
+extern "C" hiper_status hiper_comm_unique_id(uint8_t id[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  if (!id) return fail(HIPER_ERR_INVALID_ARG, "id is NULL");
+  ncclUniqueId u;
+  NCCL_TRY(ncclGetUniqueId(&u));
+  memcpy(id, &u, 128);
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_comm_create(const uint8_t id[128], int32_t world, int32_t rank,
+                                          int32_t device, hiper_comm** out) {
+  if (!id || !out) return fail(HIPER_ERR_INVALID_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(HIPER_ERR_INVALID_ARG, "bad world/rank");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  hiper_comm_s* c = new hiper_comm_s();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(HIPER_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_comm_destroy(hiper_comm* c) {
+  if (!c) return HIPER_OK;
+  ncclResult_t r = c->comm ? ncclCommDestroy(c->comm) : ncclSuccess;
+  delete c;
+  if (r != ncclSuccess) return fail(HIPER_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_comm_info(const hiper_comm* c, int32_t* world, int32_t* rank) {
+  if (!c) return fail(HIPER_ERR_INVALID_ARG, "comm is NULL");
+  if (world) *world = c->world;
+  if (rank) *rank = c->rank;
+  return HIPER_OK;
+}
+
+// ============================================================================ workspace layouts
+struct TopkWs {
+  size_t status = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0, total = 0;
+};
+
+static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_groups, int32_t n_parts, int32_t k,
+                           int32_t world, bool with_comm, TopkWs& w) {
+  size_t off = 0;
+  w.status = off;
+  off += 256;
+  w.qlens = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
+  w.qlayout = off;
+  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
+  w.partial = off;
+  off = align_up(off + (size_t)n_parts * n_groups * 4 * k * 8, 256);
+  w.local = off;
+  if (with_comm) off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
+  w.gathered = off;
+  if (with_comm) off = align_up(off + (size_t)world * std::max(n_q, 1) * k * 8, 256);
+  w.total = off;
+}
+
+static hiper_status check_ws(const void* ws, size_t have, size_t need) {
+  if (!ws) return fail(HIPER_ERR_WORKSPACE, "workspace is NULL (need %zu bytes)", need);
+  if (((uintptr_t)ws & 1023) != 0) return fail(HIPER_ERR_WORKSPACE, "workspace must be 1024-B aligned");
+  if (have < need) return fail(HIPER_ERR_WORKSPACE, "workspace too small: %zu < %zu", have, need);
+  return HIPER_OK;
+}
+
+extern "C" size_t hiper_maxsim_topk_workspace_size(const hiper_index* ix, int32_t n_q, int32_t k,
+                                                   const hiper_comm* comm) {
+  if (!ix || n_q < 0 || k < 1) return 0;
+  int num_sms = 148;
+  if (cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ix->device) != cudaSuccess) {
+    cudaGetLastError();
+    num_sms = 148;
+  }
+  const int32_t G = n_q_pad_of(n_q) / 4;
+  TopkWs w;
+  topk_ws_layout(n_q, ix->dim, G, choose_parts(G, ix->n, num_sms), k, comm ? comm->world : 1,
+                 comm != nullptr, w);
+  return w.total;
+}
+
+extern "C" hiper_status hiper_workspace_status(const void* workspace, hiper_stream_t stream) {
+  if (!workspace) return fail(HIPER_ERR_WORKSPACE, "workspace is NULL");
+  return sync_status((const uint32_t*)workspace, (cudaStream_t)stream);
+}
+
+// ============================================================================ top-k search
+extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_tokens,
+                                          hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
+                                          int32_t q_max_len, int32_t dim, int32_t k, uint32_t flags,
+                                          const hiper_comm* comm, void* workspace,
+                                          size_t workspace_bytes, float* out_scores,
+                                          int64_t* out_ids, hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
+  if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
+  if (k < 1) return fail(HIPER_ERR_INVALID_ARG, "k must be >= 1");
+  if (k > 128) return fail(HIPER_ERR_UNSUPPORTED, "k %d > 128", k);
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
+  if (n_q == 0) return HIPER_OK;
+  if (!out_scores || !out_ids) return fail(HIPER_ERR_INVALID_ARG, "outputs are NULL");
+  DevInfo di;
+  TRY(device_info(di));
+  if (di.device != ix->device) return fail(HIPER_ERR_INVALID_ARG, "index lives on device %d, current is %d", ix->device, di.device);
+  KernelPlan kp;
+  TRY(plan_kernel(di, n_q, ix->n, ix->ld_pad, dim, kp));
+  const int32_t world = comm ? comm->world : 1;
+  TopkWs w;
+  topk_ws_layout(n_q, dim, kp.n_groups, kp.n_parts, k, world, comm != nullptr, w);
+  TRY(check_ws(workspace, workspace_bytes, w.total));
+  uint8_t* ws = (uint8_t*)workspace;
+  uint32_t* status = (uint32_t*)(ws + w.status);
+  int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
+  __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
+  uint64_t* partial = (uint64_t*)(ws + w.partial);
+
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
+  if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
+
+  if (kp.grid > 0) {
+    alignas(64) CUtensorMap tq;
+    TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
+    MaxsimArgs a{};
+    a.n_q = n_q;
+    a.n_groups = kp.n_groups;
+    a.n_parts = kp.n_parts;
+    a.ld_pad = ix->ld_pad;
+    a.num_kb = dim / 64;
+    a.k = k;
+    a.n_stages = kp.n_stages;
+    a.a_bytes = kp.a_bytes;
+    a.stage_bytes = kp.stage_bytes;
+    a.n_chunks = ix->n;
+    a.id_base = ix->id_base;
+    a.q_lens = qlens_dev;
+    a.d_lens = ix->lens;
+    a.partial = partial;
+    TRY(launch_maxsim(1, k, kp, tq, ix->tmap, a, stream));
+  }
+  const int64_t q_stride = k, list_stride = (int64_t)kp.n_groups * 4 * k;
+  if (!comm || comm->world == 1) {
+    TRY(launch_merge(partial, kp.n_parts, list_stride, n_q, q_stride, k, nullptr, out_scores, out_ids, stream));
+    return HIPER_OK;
+  }
+  uint64_t* local = (uint64_t*)(ws + w.local);
+  uint64_t* gathered = (uint64_t*)(ws + w.gathered);
+  TRY(launch_merge(partial, kp.n_parts, list_stride, n_q, q_stride, k, local, nullptr, nullptr, stream));
+  NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, comm->comm, stream));
+  TRY(launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream));
+  return HIPER_OK;
+}
+
+// ============================================================================ dense scores
+struct ScoresWs {
+  size_t status = 0, qlens = 0, qlayout = 0, total = 0;
+};
+static void scores_ws_layout(int32_t n_q, int32_t dim, ScoresWs& w) {
+  size_t off = 0;
+  w.status = off;
+  off += 256;
+  w.qlens = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
+  w.qlayout = off;
+  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
+  w.total = off;
+}
+
+extern "C" size_t hiper_maxsim_scores_workspace_size(const hiper_index* ix, int32_t n_q) {
+  if (!ix || n_q < 0) return 0;
+  ScoresWs w;
+  scores_ws_layout(n_q, ix->dim, w);
+  return w.total;
+}
+
+extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q_tokens,
+                                            hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
+                                            int32_t q_max_len, int32_t dim, uint32_t flags,
+                                            void* workspace, size_t workspace_bytes,
+                                            float* out_scores, hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
+  if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
+  if (n_q == 0 || ix->n == 0) return HIPER_OK;
+  if (!out_scores) return fail(HIPER_ERR_INVALID_ARG, "out_scores is NULL");
+  DevInfo di;
+  TRY(device_info(di));
+  KernelPlan kp;
+  TRY(plan_kernel(di, n_q, ix->n, ix->ld_pad, dim, kp));
+  ScoresWs w;
+  scores_ws_layout(n_q, dim, w);
+  TRY(check_ws(workspace, workspace_bytes, w.total));
+  uint8_t* ws = (uint8_t*)workspace;
+  uint32_t* status = (uint32_t*)(ws + w.status);
+  int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
+  __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
+  if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
+  alignas(64) CUtensorMap tq;
+  TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
+  MaxsimArgs a{};
+  a.n_q = n_q;
+  a.n_groups = kp.n_groups;
+  a.n_parts = kp.n_parts;
+  a.ld_pad = ix->ld_pad;
+  a.num_kb = dim / 64;
+  a.k = 1;
+  a.n_stages = kp.n_stages;
+  a.a_bytes = kp.a_bytes;
+  a.stage_bytes = kp.stage_bytes;
+  a.n_chunks = ix->n;
+  a.id_base = ix->id_base;
+  a.q_lens = qlens_dev;
+  a.d_lens = ix->lens;
+  a.scores = out_scores;
+  a.score_ld = ix->n;
+  return launch_maxsim(0, 1, kp, tq, ix->tmap, a, stream);
+}
+
+// ============================================================================ ColTrast scores + loss
+struct ColtrastWs {
+  size_t status = 0, qlens = 0, dlens = 0, pos = 0, qlayout = 0, dlayout = 0, scores = 0, total = 0;
+};
+static void coltrast_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim, ColtrastWs& w) {
+  const int32_t ld_pad = (int32_t)round_up(std::max(d_max_len, 1), 16);
+  size_t off = 0;
+  w.status = off;
+  off += 256;
+  w.qlens = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 256);
+  w.dlens = off;
+  off = align_up(off + (size_t)std::max(n_d, 1) * 4, 256);
+  w.pos = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
+  w.qlayout = off;
+  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
+  w.dlayout = off;
+  off = align_up(off + (size_t)std::max(n_d, 1) * ld_pad * dim * 2, 1024);
+  w.scores = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * std::max(n_d, 1) * 4, 1024);
+  w.total = off;
+}
+
+extern "C" size_t hiper_coltrast_workspace_size(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim) {
+  if (n_q < 0 || n_d < 0 || dim <= 0) return 0;
+  ColtrastWs w;
+  coltrast_ws_layout(n_q, n_d, d_max_len, dim, w);
+  return w.total;
+}
+
+static hiper_status launch_loss(const float* S, int32_t n_q, int32_t n_d, int64_t ld,
+                                const int32_t* pos_dev, float tau, float* out_loss,
+                                cudaStream_t stream) {
+  infonce_loss_kernel<<<1, 1024, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, out_loss);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return HIPER_OK;
+}
+
+static hiper_status validate_loss_args(int32_t n_q, int32_t n_d, const int32_t* pos_idx, float tau) {
+  if (n_q == 0) return fail(HIPER_ERR_EMPTY_BATCH, "empty batch");
+  if (n_q < 0 || n_d < 0) return fail(HIPER_ERR_INVALID_ARG, "negative batch size");
+  if (!(tau > 0.0f) || !std::isfinite(tau)) return fail(HIPER_ERR_BAD_TEMPERATURE, "temperature must be > 0 and finite");
+  if (n_d == 0) return fail(HIPER_ERR_BAD_POSITIVE, "no candidates");
+  if (pos_idx) {
+    for (int32_t i = 0; i < n_q; ++i)
+      if (pos_idx[i] < 0 || pos_idx[i] >= n_d)
+        return fail(HIPER_ERR_BAD_POSITIVE, "pos_idx[%d] = %d outside 0..%d", i, pos_idx[i], n_d - 1);
+  } else if (n_d < n_q) {
+    return fail(HIPER_ERR_BAD_POSITIVE, "diagonal positives need n_d >= n_q");
+  }
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const int32_t* q_lens, int32_t n_q,
+                                                   int32_t q_max_len, const void* d_tokens,
+                                                   const int32_t* d_lens, int32_t n_d, int32_t d_max_len,
+                                                   int32_t dim, hiper_dtype dtype, uint32_t flags,
+                                                   const int32_t* pos_idx, float temperature,
+                                                   void* workspace, size_t workspace_bytes,
+                                                   float* out_scores, float* out_loss, hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
+  if (d_max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "d_max_len must be >= 1");
+  if (d_max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "d_max_len %d > 256", d_max_len);
+  TRY(check_lens(d_lens, n_d, d_max_len, "doc"));
+  if (!d_tokens || !is_device_ptr(d_tokens) || ((uintptr_t)d_tokens & 15))
+    return fail(HIPER_ERR_INVALID_ARG, "d_tokens must be 16-B aligned device memory");
+  if (!out_loss) return fail(HIPER_ERR_INVALID_ARG, "out_loss is NULL");
+  DevInfo di;
+  TRY(device_info(di));
+  const int32_t ld_pad = (int32_t)round_up(d_max_len, 16);
+  KernelPlan kp;
+  TRY(plan_kernel(di, n_q, n_d, ld_pad, dim, kp));
+  ColtrastWs w;
+  coltrast_ws_layout(n_q, n_d, d_max_len, dim, w);
+  TRY(check_ws(workspace, workspace_bytes, w.total));
+  uint8_t* ws = (uint8_t*)workspace;
+  uint32_t* status = (uint32_t*)(ws + w.status);
+  int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
+  int32_t* dlens_dev = (int32_t*)(ws + w.dlens);
+  int32_t* pos_dev = (int32_t*)(ws + w.pos);
+  __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
+  __nv_bfloat16* dlayout = (__nv_bfloat16*)(ws + w.dlayout);
+  float* S = out_scores ? out_scores : (float*)(ws + w.scores);
+
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
+  TRY(stage_h2d(dlens_dev, d_lens, (size_t)n_d * 4, stream));
+  TRY(launch_norm(d_tokens, dtype, n_d, d_max_len, dlens_dev, n_d, ld_pad, dim, flags, dlayout, status, stream));
+  if (pos_idx) TRY(stage_h2d(pos_dev, pos_idx, (size_t)n_q * 4, stream));
+  if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
+
+  alignas(64) CUtensorMap tq, td;
+  TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
+  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, ld_pad));
+  MaxsimArgs a{};
+  a.n_q = n_q;
+  a.n_groups = kp.n_groups;
+  a.n_parts = kp.n_parts;
+  a.ld_pad = ld_pad;
+  a.num_kb = dim / 64;
+  a.k = 1;
+  a.n_stages = kp.n_stages;
+  a.a_bytes = kp.a_bytes;
+  a.stage_bytes = kp.stage_bytes;
+  a.n_chunks = n_d;
+  a.id_base = 0;
+  a.q_lens = qlens_dev;
+  a.d_lens = dlens_dev;
+  a.scores = S;
+  a.score_ld = n_d;
+  TRY(launch_maxsim(0, 1, kp, tq, td, a, stream));
+  return launch_loss(S, n_q, n_d, n_d, pos_idx ? pos_dev : nullptr, temperature, out_loss, stream);
+}
+
+extern "C" hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,
+                                           const int32_t* pos_idx, float temperature, void* workspace,
+                                           size_t workspace_bytes, float* out_loss, hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
+  if (!scores || !out_loss) return fail(HIPER_ERR_INVALID_ARG, "NULL pointer");
+  const size_t need = align_up((size_t)n_q * 4, 1024);
+  if (pos_idx) TRY(check_ws(workspace, workspace_bytes, need));
+  if (pos_idx) TRY(stage_h2d(workspace, pos_idx, (size_t)n_q * 4, stream));
+  return launch_loss(scores, n_q, n_d, n_d, pos_idx ? (const int32_t*)workspace : nullptr, temperature,
+                     out_loss, stream);
+}

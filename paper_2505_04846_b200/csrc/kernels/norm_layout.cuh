@@ -1,0 +1,110 @@
+// norm_layout.cuh -- steps a1 (corpus layout) and a2 (query preparation).
+//
+// One thread per OUTPUT row.  Row j < len of item i: NORM (R1, "rows normalized on entry",
+// SPEC.md:285):
+//   acc = 0; for k ascending: acc = fma_rn(x_k, x_k, acc);  inv = 1 / sqrt(acc) (both RN);
+//   y_k = RNE_bf16(x_k * inv)
+// Rows j >= len (and items >= n_items) are written as zero rows.  The layout step is HBM-bound
+// (read d*in_bytes, write d*2 bytes per row); the per-thread sequential fma chain keeps the
+// summation order fixed so the result is bit-identical to the oracle's independent NORM.
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace hiper {
+
+constexpr uint32_t kStatusZeroRow = 1u;
+constexpr uint32_t kStatusNonFinite = 2u;
+
+__device__ __forceinline__ float load_elem(const float* p) { return *p; }
+__device__ __forceinline__ float load_elem(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+template <typename Tin>
+__device__ __forceinline__ void load8(const Tin* p, float (&x)[8]);
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float (&x)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *reinterpret_cast<const float4*>(p + 4);
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+  x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&x)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[2 * i] = __uint_as_float(w[i] << 16);
+    x[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+// in:  [n_src][in_rows][d] (element strides), only items < n_src / rows < lens[item] are read
+// out: [n_items][out_rows][d] bf16
+// lens: device [n_src] (items >= n_src are empty)
+// d % 8 == 0 and 16-B aligned rows.  In-place (in == out) is allowed when Tin == bf16 and
+// in_rows == out_rows: every thread reads and writes only its own row.
+template <typename Tin>
+__global__ void __launch_bounds__(256) norm_layout_kernel(const Tin* in, int64_t n_src, int32_t in_rows,
+                                                          const int32_t* __restrict__ lens,
+                                                          int64_t n_items, int32_t out_rows, int32_t d,
+                                                          uint32_t assume_normalized,
+                                                          uint32_t check_finite,
+                                                          __nv_bfloat16* out, uint32_t* status) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n_items * (int64_t)out_rows) return;
+  const int64_t item = row / out_rows;
+  const int32_t j = (int32_t)(row - item * out_rows);
+  uint4* dst = reinterpret_cast<uint4*>(out + row * d);
+  const int32_t len = item < n_src ? lens[item] : 0;
+  if (j >= len) {
+    for (int32_t k = 0; k < d; k += 8) dst[k / 8] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const Tin* src = in + (item * in_rows + j) * (int64_t)d;
+  float inv = 1.0f;
+  if (!assume_normalized) {
+    float acc = 0.0f;
+    bool finite = true;
+    for (int32_t k = 0; k < d; k += 8) {
+      float x[8];
+      load8<Tin>(src + k, x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        finite &= isfinite(x[i]);
+        acc = __fmaf_rn(x[i], x[i], acc);
+      }
+    }
+    if (!finite) {
+      if (status) atomicOr(status, kStatusNonFinite);
+    } else if (acc == 0.0f) {
+      if (status) atomicOr(status, kStatusZeroRow);
+    }
+    inv = __fdiv_rn(1.0f, __fsqrt_rn(acc));
+  } else if (check_finite) {
+    bool finite = true;
+    for (int32_t k = 0; k < d; k += 8) {
+      float x[8];
+      load8<Tin>(src + k, x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) finite &= isfinite(x[i]);
+    }
+    if (!finite && status) atomicOr(status, kStatusNonFinite);
+  }
+  for (int32_t k = 0; k < d; k += 8) {
+    float x[8];
+    load8<Tin>(src + k, x);
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float a = assume_normalized ? x[2 * i] : __fmul_rn(x[2 * i], inv);
+      const float b = assume_normalized ? x[2 * i + 1] : __fmul_rn(x[2 * i + 1], inv);
+      const __nv_bfloat16 ha = __float2bfloat16_rn(a);
+      const __nv_bfloat16 hb = __float2bfloat16_rn(b);
+      w[i] = (uint32_t)__bfloat16_as_ushort(ha) | ((uint32_t)__bfloat16_as_ushort(hb) << 16);
+    }
+    dst[k / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+}  // namespace hiper

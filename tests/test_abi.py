@@ -1,0 +1,83 @@
+"""The C-ABI library loads and exports every symbol include/hiper.h declares; host-side validation
+runs before any device work (CPU only: no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "hiper.h")).read()
+    return sorted(set(re.findall(r"HIPER_API\s+[\w\s\*]+?\b(hiper_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    import paper_2505_04846_b200 as H
+    L = H.lib()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    assert sorted(H.EXPORTS) == syms
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    import paper_2505_04846_b200 as H
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", H.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out and "sm_90" not in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", H.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM"):   # tcgen05.mma, TMA, tcgen05.ld
+        assert mnem in sass, mnem
+    assert "HMMA" not in sass.replace("UTCHMMA", "")
+
+
+def test_status_strings():
+    import paper_2505_04846_b200 as H
+    L = H.lib()
+    for code, name in H.STATUS.items():
+        assert L.hiper_status_string(code).decode() == name
+
+
+def test_host_validation_before_device():
+    """Argument errors are reported without touching a device (works on a GPU-less host)."""
+    import paper_2505_04846_b200 as H
+    L = H.lib()
+    out = ctypes.c_void_p()
+    lens = np.ones(4, np.int32)
+    P = lens.ctypes.data_as(ctypes.c_void_p)
+    assert L.hiper_index_build(None, 0, P, -1, 8, 128, 0, 0, None, ctypes.byref(out)) == 1
+    assert L.hiper_index_build(None, 0, P, 4, 8, 96, 0, 0, None, ctypes.byref(out)) == 12
+    assert L.hiper_index_build(None, 0, P, 4, 300, 128, 0, 0, None, ctypes.byref(out)) == 12
+    assert L.hiper_index_build(None, 0, P, 4, 8, 128, 0, 1 << 7, None, ctypes.byref(out)) == 1
+    zero = np.array([1, 0, 1, 1], np.int32)
+    assert L.hiper_index_build(None, 0, zero.ctypes.data_as(ctypes.c_void_p), 4, 8, 128, 0, 0,
+                               None, ctypes.byref(out)) == 3
+    assert "0 tokens" in L.hiper_last_error().decode()
+    assert L.hiper_coltrast_scores_loss(None, P, 0, 8, None, P, 4, 8, 128, 1, 0, None,
+                                        ctypes.c_float(1.0), None, 0, None, None, None) == 4
+    assert L.hiper_coltrast_scores_loss(None, P, 4, 8, None, P, 4, 8, 128, 1, 0, None,
+                                        ctypes.c_float(-1.0), None, 0, None, None, None) == 5
+    bad = np.array([0, 1, 2, 9], np.int32)
+    assert L.hiper_coltrast_scores_loss(None, P, 4, 8, None, P, 4, 8, 128, 1, 0,
+                                        bad.ctypes.data_as(ctypes.c_void_p), ctypes.c_float(1.0),
+                                        None, 0, None, None, None) == 6
+    assert L.hiper_maxsim_topk(None, None, 1, P, 4, 8, 128, 10, 0, None, None, 0, None, None,
+                               None) == 1
+
+
+def test_product_path_does_not_import_oracle():
+    """The product package never imports or links the oracle (only tests/bench/smoke may)."""
+    pkg = os.path.join(ROOT, "paper_2505_04846_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower() or f == "__init__.py" \
+                    and "import oracle" not in txt, f
