@@ -183,6 +183,13 @@ HIPER_API hiper_status hiper_workspace_status(const void* workspace, hiper_strea
 /* Number of kernels the last successful compute call on this thread enqueued (bench evidence). */
 HIPER_API int32_t hiper_last_launch_count(void);
 
+/* Live per-kernel timing for the roofline report: while enabled, every launch of the fused MaxSim
+ * kernel is bracketed by CUDA events on its own stream.  hiper_profile_read synchronises on the
+ * recorded events, returns the summed kernel milliseconds and the number of launches since the last
+ * read, and resets the record. */
+HIPER_API void hiper_profile_enable(int32_t on);
+HIPER_API hiper_status hiper_profile_read(double* maxsim_ms, int32_t* n_launches);
+
 #ifdef __cplusplus
 }
 #endif

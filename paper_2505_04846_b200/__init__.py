@@ -45,6 +45,7 @@ EXPORTS = [
     "hiper_maxsim_topk_workspace_size", "hiper_maxsim_topk", "hiper_maxsim_scores_workspace_size",
     "hiper_maxsim_scores", "hiper_coltrast_workspace_size", "hiper_coltrast_scores_loss",
     "hiper_infonce_loss", "hiper_workspace_status", "hiper_last_launch_count",
+    "hiper_profile_enable", "hiper_profile_read",
 ]
 
 
@@ -90,6 +91,8 @@ def lib():
                                         ctypes.c_float, P, sz, P, P, P], i32),
         "hiper_infonce_loss": ([P, i32, i32, P, ctypes.c_float, P, sz, P, P], i32),
         "hiper_workspace_status": ([P, P], i32),
+        "hiper_profile_enable": ([i32], None),
+        "hiper_profile_read": ([P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -229,7 +232,7 @@ def _raw_u8_view(ptr: int, nbytes: int):
     torch = _torch()
 
     class _Arr:
-        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, True),
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
                                     "version": 3}
 
     return torch.as_tensor(_Arr(), device="cuda")
@@ -364,3 +367,14 @@ def hiper_workspace_status(workspace, stream=None) -> str:
 
 def last_launch_count() -> int:
     return int(lib().hiper_last_launch_count())
+
+
+def hiper_profile_enable(on: bool = True):
+    lib().hiper_profile_enable(int(bool(on)))
+
+
+def hiper_profile_read():
+    """(summed fused-MaxSim-kernel milliseconds, launches) since the last read (synchronises)."""
+    ms, n = ctypes.c_double(), ctypes.c_int32()
+    _check(lib().hiper_profile_read(ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value

@@ -16,6 +16,8 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/hiper.h"
 #include "kernels/infonce.cuh"
@@ -437,13 +439,72 @@ static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int64_t n_chunks
   return HIPER_OK;
 }
 
+// ---------------------------------------------------------------------------- live kernel timing
+namespace {
+struct ProfileRec {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> live, pool;
+};
+ProfileRec g_prof;
+}  // namespace
+
+extern "C" void hiper_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lock(g_prof.mu);
+  g_prof.on = on != 0;
+}
+
+extern "C" hiper_status hiper_profile_read(double* maxsim_ms, int32_t* n_launches) {
+  std::lock_guard<std::mutex> lock(g_prof.mu);
+  double total = 0.0;
+  for (auto& e : g_prof.live) {
+    CUDA_TRY(cudaEventSynchronize(e.second));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+    total += ms;
+    g_prof.pool.push_back(e);
+  }
+  if (maxsim_ms) *maxsim_ms = total;
+  if (n_launches) *n_launches = (int32_t)g_prof.live.size();
+  g_prof.live.clear();
+  return HIPER_OK;
+}
+
+static hiper_status profile_begin(cudaStream_t stream, std::pair<cudaEvent_t, cudaEvent_t>* ev, bool* rec) {
+  std::lock_guard<std::mutex> lock(g_prof.mu);
+  *rec = g_prof.on;
+  if (!g_prof.on) return HIPER_OK;
+  if (g_prof.pool.empty()) {
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    g_prof.pool.push_back({a, b});
+  }
+  *ev = g_prof.pool.back();
+  g_prof.pool.pop_back();
+  CUDA_TRY(cudaEventRecord(ev->first, stream));
+  return HIPER_OK;
+}
+
+static hiper_status profile_end(cudaStream_t stream, const std::pair<cudaEvent_t, cudaEvent_t>& ev, bool rec) {
+  if (!rec) return HIPER_OK;
+  CUDA_TRY(cudaEventRecord(ev.second, stream));
+  std::lock_guard<std::mutex> lock(g_prof.mu);
+  g_prof.live.push_back(ev);
+  return HIPER_OK;
+}
+
 template <int MODE, int KR>
 static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
                                     const MaxsimArgs& a, cudaStream_t stream) {
   auto kern = maxsim_sm100_kernel<MODE, KR>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  bool rec = false;
+  TRY(profile_begin(stream, &ev, &rec));
   kern<<<kp.grid, kMaxsimThreads, kp.smem_bytes, stream>>>(tq, td, a);
   CUDA_TRY(cudaGetLastError());
+  TRY(profile_end(stream, ev, rec));
   ++g_launches;
   return HIPER_OK;
 }

@@ -97,7 +97,7 @@ int grid_for(uint64_t total) {
 
 }  // namespace
 
-extern "C" int synth_corpus(void* out, int out_bf16, int64_t chunk_start, int64_t n, int32_t L,
+extern "C" __attribute__((visibility("default"))) int synth_corpus(void* out, int out_bf16, int64_t chunk_start, int64_t n, int32_t L,
                             int32_t d, uint64_t seed, int planted, float sigma, void* stream) {
   if (n <= 0) return 0;
   const uint64_t total = (uint64_t)n * L * d;
@@ -107,7 +107,7 @@ extern "C" int synth_corpus(void* out, int out_bf16, int64_t chunk_start, int64_
   return (int)cudaGetLastError();
 }
 
-extern "C" int synth_queries(void* out, int out_bf16, int64_t q_start, int64_t n_q, int32_t Lq,
+extern "C" __attribute__((visibility("default"))) int synth_queries(void* out, int out_bf16, int64_t q_start, int64_t n_q, int32_t Lq,
                              int32_t d, uint64_t qseed, int diagonal, int query_planted,
                              int64_t n_chunks, int32_t L, const int32_t* chunk_lens_dev,
                              uint64_t corpus_seed, int corpus_planted, float sigma, float sigma_q,
