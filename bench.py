@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py -- exact MaxSim top-k retrieval throughput (BASELINE.json metric) on B200.
+
+One step = one pass of the whole hot path (query prep a2, fused TMA/tcgen05 MaxSim
++ masked max/sum + per-CTA top-k a3-a6, merge a7, [all-gather + merge a8], decode a9) for a batch of
+Q queries against the full corpus, which is resident in HBM (built once, before timing).
+
+Default workload (N=1): BASELINE.json configs[2] -- 1M chunks x 256 tokens x dim 128 bf16, query batch
+1024 x 32 tokens, top-10.  The metric's 3.6M-chunk corpus (236 GB) does not fit one GPU, so N=1 uses the
+largest single-GPU config; --gpus N > 1 shards the SAME 1M corpus over N ranks (strong scaling: total
+work fixed) and merges the per-rank top-k with one ncclAllGather.  --chunks 3600000 runs the paper-scale
+corpus when N >= 2.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "queries/s (exact MaxSim top-10, 3.6M chunks) at 1/2/4/8 B200; % bf16 TC peak"
+UNIT = "queries/s"
+FALLBACK_PEAK_SUSTAINED = 1400.0  # B200_PROFILING.md fallback (sustained under the power cap)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--chunks", type=int, default=1_000_000)
+    ap.add_argument("--queries", type=int, default=1024)
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--chunk-len", type=int, default=256)
+    ap.add_argument("--query-len", type=int, default=32)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--qseed", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU work for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def workload_config(a, world):
+    return {
+        "workload": (f"{'config3' if a.chunks == 1_000_000 else 'config4' if a.chunks == 3_600_000 else 'custom'}: "
+                     f"{a.chunks} chunks x {a.chunk_len} tokens, dim {a.dim}, bf16, query batch "
+                     f"{a.queries} x {a.query_len} tokens, top-{a.k}"),
+        "chunks": a.chunks, "chunk_len": a.chunk_len, "dim": a.dim, "query_batch": a.queries,
+        "query_len": a.query_len, "k": a.k, "corpus_per_gpu": a.chunks // world,
+        "parallelism": f"corpus-sharded x{world}, one ncclAllGather of top-k keys" if world > 1
+        else "single GPU",
+        "l2": "inputs larger than L2: the corpus (%.1f GB) is streamed every step, no flush needed"
+              % (a.chunks * a.chunk_len * a.dim * 2 / 1e9),
+        "generator": f"synth planted-topic corpus seed {a.seed}, planted queries seed {a.qseed}",
+    }
+
+
+def flops_per_pair(a):
+    return 2.0 * a.query_len * a.chunk_len * a.dim
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if "bf16_tflops_sustained" in d:
+            return float(d["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained (measured)"
+    return FALLBACK_PEAK_SUSTAINED, "B200_PROFILING.md fallback, sustained"
+
+
+def ncu_traffic(a, world):
+    """DRAM bytes (read + write) per launch of the fused kernel, from the committed `ncu --set full`
+    capture of this same workload (profiles/ncu_traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    ent = json.load(open(p)).get("maxsim_sm100_kernel", {})
+    if ent.get("chunks_per_gpu") == a.chunks // world and ent.get("queries") == a.queries:
+        return float(ent["dram_bytes_per_launch"])
+    return None
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = [l.strip().split(",") for l in open(self.f.name) if l.count(",") >= 8]
+        os.unlink(self.f.name)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons, power = [], [], set(), []
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+                power.append(float(r[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_median": statistics.median(power)}
+
+
+# ------------------------------------------------------------------------------------------ oracle leg
+def oracle_sample(a, n_chunks_sample, n_queries_sample=4):
+    """Time the CPU oracle (as it stands) on a bounded sample of the same workload.
+
+    Timed: NORM of the sample queries + MaxSim of every (query, chunk) pair + exact top-k.
+    (The corpus NORM is build-time on both sides and excluded.)"""
+    import numpy as np
+
+    import oracle
+    from synth import gen
+    cores = len(os.sched_getaffinity(0))
+    C_s = int(n_chunks_sample)
+    corp = gen.corpus(a.seed, 0, C_s, a.chunk_len, a.dim)
+    cn = oracle.norm_rows(corp)
+    q = gen.queries(a.qseed, n_queries_sample, a.query_len, a.dim, corpus_seed=a.seed,
+                    n_chunks=a.chunks, L=a.chunk_len)
+    ids = np.arange(C_s, dtype=np.int64)
+    t0 = time.perf_counter()
+    qn = oracle.norm_rows(q)
+    S = oracle.maxsim_matrix(qn, np.full(n_queries_sample, a.query_len, np.int32), cn,
+                             np.full(C_s, a.chunk_len, np.int32), n_threads=cores)
+    for r in range(n_queries_sample):
+        oracle.topk(S[r], ids, a.k)
+    dt = time.perf_counter() - t0
+    # queries/s over the full corpus, extrapolated linearly in the corpus size
+    qps = n_queries_sample / (dt * a.chunks / C_s)
+    return qps, dt, cores, C_s, n_queries_sample
+
+
+def calibrated_oracle(a, seconds):
+    # a short calibration run, then one run sized to ~`seconds` of CPU work
+    _, dt0, cores, c0, nq = oracle_sample(a, 64)
+    C_s = int(max(64, min(200_000, 64 * seconds / max(dt0, 1e-3))))
+    return oracle_sample(a, C_s, nq)
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    per_step = max(1.0, min(6.0, 150.0 / max(1, a.steps + a.warmup)))
+    _, dt0, cores, _, nq = oracle_sample(a, 64)
+    C_s = int(max(64, min(200_000, 64 * per_step / max(dt0, 1e-3))))
+    times = []
+    for i in range(a.warmup + a.steps):
+        qps, dt, cores, C_s, nq = oracle_sample(a, C_s, nq)
+        if i >= a.warmup:
+            times.append(dt)
+    dt = sum(times) / len(times)
+    value = nq / (dt * a.chunks / C_s)
+    sample = (f"{nq} queries x {C_s} chunks per step (of {a.chunks}); queries/s extrapolated "
+              f"linearly to the full corpus; float64 C oracle, OpenMP over pairs")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(a, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ our arm
+def run_ours(a, rank, local_rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2505_04846_b200 as H
+    from synth import device, gen
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    H.lib()
+    c0 = rank * a.chunks // world
+    c1 = (rank + 1) * a.chunks // world
+    n_local = c1 - c0
+    corpus = torch.empty((n_local, a.chunk_len, a.dim), dtype=torch.bfloat16, device="cuda")
+    device.corpus_(corpus, a.seed, c0)
+    lens = np.full(n_local, a.chunk_len, np.int32)
+    idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_BORROW_TOKENS)
+    comm = H.Comm() if world > 1 else None
+    q = torch.empty((a.queries, a.query_len, a.dim), dtype=torch.bfloat16, device="cuda")
+    device.queries_(q, a.qseed, corpus_seed=a.seed, n_chunks=a.chunks, L=a.chunk_len)
+    qlen = np.full(a.queries, a.query_len, np.int32)
+    ws = H.TopkWorkspace(idx, a.queries, a.k, comm)
+    out = (torch.empty((a.queries, a.k), dtype=torch.float32, device="cuda"),
+           torch.empty((a.queries, a.k), dtype=torch.int64, device="cuda"))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        H.hiper_maxsim_topk(idx, q, qlen, a.k, comm=comm, workspace=ws, out=out, stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(a.warmup, 0)):
+        step()
+    launches_per_step = H.last_launch_count()
+    barrier()
+    clocks = ClockSampler(list(range(world))) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    H.hiper_profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    H.hiper_profile_enable(False)
+    kern_ms, kern_n = H.hiper_profile_read()
+    clk = clocks.stop() if clocks else None
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    kern_avg_ms = max_over_ranks(kern_ms / max(kern_n, 1))
+    value = a.queries * a.steps / (ms / 1e3)
+
+    # planted-target sanity (the planted target chunk must be the top-1 hit)
+    tgt = torch.from_numpy(gen.query_targets(a.qseed, a.queries, a.chunks, False)).cuda()
+    top1 = float((out[1][:, 0] == tgt).float().mean().item())
+
+    # ---- e2e: host (pinned) queries in, host results out, through the public API, every step
+    e2e = None
+    if not a.no_e2e:
+        q_host = q.cpu().pin_memory()
+        s_host = torch.empty_like(out[0], device="cpu").pin_memory()
+        i_host = torch.empty_like(out[1], device="cpu").pin_memory()
+        q_dev = torch.empty_like(q)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.steps):
+            q_dev.copy_(q_host, non_blocking=True)
+            H.hiper_maxsim_topk(idx, q_dev, qlen, a.k, comm=comm, workspace=ws, out=out, stream=stream)
+            s_host.copy_(out[0], non_blocking=True)
+            i_host.copy_(out[1], non_blocking=True)
+        f1.record(stream)
+        barrier()
+        ms_e2e = max_over_ranks(f0.elapsed_time(f1))
+        h2d = q_host.numel() * q_host.element_size() * world
+        d2h = (s_host.numel() * 4 + i_host.numel() * 8) * world
+        e2e = {"value": a.queries * a.steps / (ms_e2e / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ms_e2e / a.steps}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = load_peaks()
+    flops_launch = flops_per_pair(a) * a.queries * n_local
+    achieved = flops_launch / (kern_avg_ms / 1e3) / 1e12
+    traffic = ncu_traffic(a, world)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload_config(a, world),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "maxsim_sm100_kernel (fused TMA + tcgen05.mma + masked max/sum + top-k)",
+                     "kernel_ms_per_launch": kern_avg_ms, "kernel_launches": kern_n,
+                     "algorithmic_flops_per_launch": flops_launch,
+                     "flops_per_pair": flops_per_pair(a), "peak_source": peak_src,
+                     "kernel_share_of_step": kern_avg_ms / (ms / a.steps)},
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * a.steps,
+        "clocks": clk,
+        "extra": {"chunk_pairs_per_s": value * a.chunks,
+                  "tflops_step": flops_per_pair(a) * a.queries * a.chunks * a.steps / (ms / 1e3) / 1e12,
+                  "top1_is_planted_target": top1, "launches_per_step": launches_per_step},
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        qps, dt, cores, C_s, nq = calibrated_oracle(a, a.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": qps, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"{nq} queries x {C_s} chunks ({dt:.1f} s: query NORM + MaxSim + top-k), "
+                       f"extrapolated linearly to {a.chunks} chunks; float64 C oracle, OpenMP"),
+        }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    run_ours(a, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

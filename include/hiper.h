@@ -118,7 +118,7 @@ HIPER_API hiper_status hiper_index_info(const hiper_index* idx, int64_t* n, int3
 
 /* ------------------------------------------------------------------ step a2: query preparation
  * NORM every real query row into the kernel's query layout: out device bf16 [n_q_pad][32][dim] with
- * n_q_pad = roundup(n_q, 4); rows i >= q_lens[q] and queries q >= n_q are zero.  status: device
+ * n_q_pad = roundup(n_q, 8); rows i >= q_lens[q] and queries q >= n_q are zero.  status: device
  * uint32 (bit 0: zero row, bit 1: non-finite row), OR-ed, may be NULL.  Exposed so the layout can be
  * checked bitwise against the oracle's NORM; the search/loss entry points call it internally. */
 HIPER_API hiper_status hiper_prepare_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,

@@ -257,7 +257,7 @@ def hiper_prepare_queries(q_tokens, q_lens, *, flags: int = 0, stream=None):
     torch = _torch()
     n_q, q_max_len, dim = q_tokens.shape
     ql = _host_i32(q_lens)
-    n_pad = max(4, (n_q + 3) // 4 * 4)
+    n_pad = max(8, (n_q + 7) // 8 * 8)
     out = torch.empty((n_pad, 32, dim), dtype=torch.bfloat16, device=q_tokens.device)
     status = torch.zeros(1, dtype=torch.int32, device=q_tokens.device)
     _check(lib().hiper_prepare_queries(_dev_ptr(q_tokens), _dtype_code(q_tokens), _ptr(ql), n_q,

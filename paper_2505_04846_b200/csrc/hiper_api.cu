@@ -22,6 +22,7 @@
 #include "../../include/hiper.h"
 #include "kernels/infonce.cuh"
 #include "kernels/maxsim_sm100.cuh"
+#include "kernels/maxsim_sm100_pair.cuh"
 #include "kernels/norm_layout.cuh"
 #include "kernels/topk_merge.cuh"
 
@@ -201,7 +202,8 @@ struct hiper_index_s {
   __nv_bfloat16* tok = nullptr;  // [n][ld_pad][dim]
   bool owns_tok = false;
   int32_t* lens = nullptr;  // device [n]
-  alignas(64) CUtensorMap tmap;
+  alignas(64) CUtensorMap tmap;       // box = 64 dims x ld_pad rows   (single-CTA kernel)
+  alignas(64) CUtensorMap tmap_half;  // box = 64 dims x ld_pad/2 rows (CTA-pair kernel)
 };
 
 static hiper_status check_dims(int32_t dim) {
@@ -321,6 +323,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     if (hstat & kStatusNonFinite) { st = fail(HIPER_ERR_NONFINITE, "chunk tokens contain non-finite values"); break; }
     if (hstat & kStatusZeroRow) { st = fail(HIPER_ERR_ZERO_VECTOR, "a chunk token row has norm 0"); break; }
     if (n > 0) st = make_tmap(&ix->tmap, ix->tok, n * (int64_t)ld_pad, dim, ld_pad);
+    if (n > 0 && st == HIPER_OK) st = make_tmap(&ix->tmap_half, ix->tok, n * (int64_t)ld_pad, dim, ld_pad / 2);
   } while (0);
   cudaFree(status);
   if (st != HIPER_OK) return cleanup(st);
@@ -353,7 +356,8 @@ extern "C" hiper_status hiper_index_info(const hiper_index* ix, int64_t* n, int3
 // ============================================================================ query preparation
 static constexpr int32_t kQSlot = 32;  // padded query-token rows per query (one warp of TMEM lanes)
 
-static int32_t n_q_pad_of(int32_t n_q) { return (int32_t)round_up(std::max(n_q, 1), 4); }
+// Queries are padded to a multiple of 8: one CTA pair's M = 256 rows = 8 queries x 32 token rows.
+static int32_t n_q_pad_of(int32_t n_q) { return (int32_t)round_up(std::max(n_q, 1), 8); }
 
 static hiper_status validate_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
                                      int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags) {
@@ -417,7 +421,19 @@ static int32_t choose_parts(int32_t n_groups, int64_t n_chunks, int num_sms) {
   return (int32_t)std::max<int64_t>(1, std::min<int64_t>(p0, n_chunks));
 }
 
+// Kernel shape: the CTA-pair kernel (cta_group::2, M = 256) is the production path; the
+// single-CTA kernel (M = 128) is kept for ablation only (HIPER_MAXSIM_CTA=1).
+static bool use_pair_kernel() {
+  static const bool pair = [] {
+    const char* e = getenv("HIPER_MAXSIM_CTA");
+    return !(e && e[0] == '1');
+  }();
+  return pair;
+}
+
 struct KernelPlan {
+  bool pair = true;
+  int32_t qpg = 8;  // queries per row group (8 for a CTA pair, 4 for one CTA)
   int32_t n_groups = 0, n_parts = 0, n_stages = 0;
   uint32_t a_bytes = 0, stage_bytes = 0, smem_bytes = 0;
   int grid = 0;
@@ -425,17 +441,20 @@ struct KernelPlan {
 
 static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int64_t n_chunks, int32_t ld_pad,
                                 int32_t dim, KernelPlan& kp) {
-  kp.n_groups = n_q_pad_of(n_q) / 4;
-  kp.n_parts = choose_parts(kp.n_groups, n_chunks, di.num_sms);
+  kp.pair = use_pair_kernel();
+  kp.qpg = kp.pair ? 8 : 4;
+  const int slots = kp.pair ? di.num_sms / 2 : di.num_sms;  // CTA pairs or CTAs
+  kp.n_groups = n_q_pad_of(n_q) / kp.qpg;
+  kp.n_parts = choose_parts(kp.n_groups, n_chunks, slots);
   kp.a_bytes = (uint32_t)(dim / 64) * 16384u;
-  kp.stage_bytes = (uint32_t)ld_pad * 128u;
+  kp.stage_bytes = (uint32_t)(kp.pair ? ld_pad / 2 : ld_pad) * 128u;
   const uint32_t fixed = 1024u /*align slack*/ + 2u * kp.a_bytes + 512u /*barriers*/;
   const uint32_t avail = (uint32_t)di.max_smem > fixed ? (uint32_t)di.max_smem - fixed : 0u;
-  kp.n_stages = (int32_t)std::min<uint32_t>(8u, avail / kp.stage_bytes);
+  kp.n_stages = (int32_t)std::min<uint32_t>(kp.pair ? 12u : 8u, avail / kp.stage_bytes);
   if (kp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory for 2 stages");
   kp.smem_bytes = fixed + kp.n_stages * kp.stage_bytes;
   const int64_t units = (int64_t)kp.n_groups * kp.n_parts;
-  kp.grid = (int)std::min<int64_t>(units, di.num_sms);
+  kp.grid = (int)std::min<int64_t>(units, slots) * (kp.pair ? 2 : 1);
   return HIPER_OK;
 }
 
@@ -497,12 +516,31 @@ static hiper_status profile_end(cudaStream_t stream, const std::pair<cudaEvent_t
 template <int MODE, int KR>
 static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
                                     const MaxsimArgs& a, cudaStream_t stream) {
-  auto kern = maxsim_sm100_kernel<MODE, KR>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   bool rec = false;
-  TRY(profile_begin(stream, &ev, &rec));
-  kern<<<kp.grid, kMaxsimThreads, kp.smem_bytes, stream>>>(tq, td, a);
+  if (kp.pair) {
+    auto kern = maxsim_sm100_pair_kernel<MODE, KR>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)kp.grid);
+    cfg.blockDim = dim3(kMaxsimThreads);
+    cfg.dynamicSmemBytes = kp.smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TRY(profile_begin(stream, &ev, &rec));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, td, a));
+  } else {
+    auto kern = maxsim_sm100_kernel<MODE, KR>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
+    TRY(profile_begin(stream, &ev, &rec));
+    kern<<<kp.grid, kMaxsimThreads, kp.smem_bytes, stream>>>(tq, td, a);
+  }
   CUDA_TRY(cudaGetLastError());
   TRY(profile_end(stream, ev, rec));
   ++g_launches;
@@ -598,7 +636,7 @@ struct TopkWs {
   size_t status = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0, total = 0;
 };
 
-static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_groups, int32_t n_parts, int32_t k,
+static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t k,
                            int32_t world, bool with_comm, TopkWs& w) {
   size_t off = 0;
   w.status = off;
@@ -608,7 +646,7 @@ static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_groups, int32_t n
   w.qlayout = off;
   off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
   w.partial = off;
-  off = align_up(off + (size_t)n_parts * n_groups * 4 * k * 8, 256);
+  off = align_up(off + (size_t)n_parts * kEpiGroups * n_q_pad_of(n_q) * k * 8, 256);
   w.local = off;
   if (with_comm) off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
   w.gathered = off;
@@ -631,10 +669,11 @@ extern "C" size_t hiper_maxsim_topk_workspace_size(const hiper_index* ix, int32_
     cudaGetLastError();
     num_sms = 148;
   }
-  const int32_t G = n_q_pad_of(n_q) / 4;
+  const bool pair = use_pair_kernel();
+  const int32_t G = n_q_pad_of(n_q) / (pair ? 8 : 4);
   TopkWs w;
-  topk_ws_layout(n_q, ix->dim, G, choose_parts(G, ix->n, num_sms), k, comm ? comm->world : 1,
-                 comm != nullptr, w);
+  topk_ws_layout(n_q, ix->dim, choose_parts(G, ix->n, pair ? num_sms / 2 : num_sms), k,
+                 comm ? comm->world : 1, comm != nullptr, w);
   return w.total;
 }
 
@@ -666,7 +705,7 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
   TRY(plan_kernel(di, n_q, ix->n, ix->ld_pad, dim, kp));
   const int32_t world = comm ? comm->world : 1;
   TopkWs w;
-  topk_ws_layout(n_q, dim, kp.n_groups, kp.n_parts, k, world, comm != nullptr, w);
+  topk_ws_layout(n_q, dim, kp.n_parts, k, world, comm != nullptr, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
   uint8_t* ws = (uint8_t*)workspace;
   uint32_t* status = (uint32_t*)(ws + w.status);
@@ -696,16 +735,18 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
     a.q_lens = qlens_dev;
     a.d_lens = ix->lens;
     a.partial = partial;
-    TRY(launch_maxsim(1, k, kp, tq, ix->tmap, a, stream));
+    TRY(launch_maxsim(1, k, kp, tq, kp.pair ? ix->tmap_half : ix->tmap, a, stream));
   }
-  const int64_t q_stride = k, list_stride = (int64_t)kp.n_groups * 4 * k;
+  // partial lists [P][kEpiGroups][n_q_pad][k]: n_lists = P * kEpiGroups, each [n_q_pad][k]
+  const int64_t q_stride = k, list_stride = (int64_t)n_q_pad_of(n_q) * k;
+  const int32_t n_lists = kp.n_parts * kEpiGroups;
   if (!comm || comm->world == 1) {
-    TRY(launch_merge(partial, kp.n_parts, list_stride, n_q, q_stride, k, nullptr, out_scores, out_ids, stream));
+    TRY(launch_merge(partial, n_lists, list_stride, n_q, q_stride, k, nullptr, out_scores, out_ids, stream));
     return HIPER_OK;
   }
   uint64_t* local = (uint64_t*)(ws + w.local);
   uint64_t* gathered = (uint64_t*)(ws + w.gathered);
-  TRY(launch_merge(partial, kp.n_parts, list_stride, n_q, q_stride, k, local, nullptr, nullptr, stream));
+  TRY(launch_merge(partial, n_lists, list_stride, n_q, q_stride, k, local, nullptr, nullptr, stream));
   NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, comm->comm, stream));
   TRY(launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream));
   return HIPER_OK;
@@ -777,7 +818,7 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
   a.d_lens = ix->lens;
   a.scores = out_scores;
   a.score_ld = ix->n;
-  return launch_maxsim(0, 1, kp, tq, ix->tmap, a, stream);
+  return launch_maxsim(0, 1, kp, tq, kp.pair ? ix->tmap_half : ix->tmap, a, stream);
 }
 
 // ============================================================================ ColTrast scores + loss
@@ -878,7 +919,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
 
   alignas(64) CUtensorMap tq, td;
   TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
-  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, ld_pad));
+  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, kp.pair ? ld_pad / 2 : ld_pad));
   MaxsimArgs a{};
   a.n_q = n_q;
   a.n_groups = kp.n_groups;

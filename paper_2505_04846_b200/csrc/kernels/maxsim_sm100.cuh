@@ -50,7 +50,10 @@ struct MaxsimArgs {
   uint64_t* partial;      // MODE 1: [P][4G][k]
 };
 
-constexpr int kMaxsimThreads = 256;  // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare, 4-7 epilogue
+// warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare; warps 4-7 = epilogue warpgroup 0 (accumulator 0, even
+// chunks), warps 8-11 = epilogue warpgroup 1 (accumulator 1, odd chunks).
+constexpr int kMaxsimThreads = 384;
+constexpr int kEpiGroups = 2;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccStride = 256;  // TMEM columns per accumulator buffer
 
@@ -105,15 +108,23 @@ __device__ __forceinline__ void unit_decode(const MaxsimArgs& a, int32_t u, int3
   c1 = (int64_t)(p + 1) * a.n_chunks / a.n_parts;
 }
 
-__device__ __forceinline__ float max32(const uint32_t (&v)[32], float m) {
+// Running max over 64 TMEM columns with 4 independent FMNMX3 chains (ILP 4: the reduction is
+// issue-bound, not latency-bound).
+__device__ __forceinline__ void max64(const uint32_t (&v)[64], float (&m)[4]) {
 #pragma unroll
-  for (int i = 0; i < 32; i += 2) m = fmaxf(fmaxf(m, __uint_as_float(v[i])), __uint_as_float(v[i + 1]));
-  return m;
+  for (int i = 0; i < 64; i += 8) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      m[c] = fmaxf(fmaxf(m[c], __uint_as_float(v[i + 2 * c])), __uint_as_float(v[i + 2 * c + 1]));
+  }
 }
-__device__ __forceinline__ float max32_masked(const uint32_t (&v)[32], float m, int rem) {
+// Same, for a ragged tail: columns >= rem are excluded from the max (reading R2).
+__device__ __forceinline__ void max64_masked(const uint32_t (&v)[64], float (&m)[4], int rem) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) m = (i < rem) ? fmaxf(m, __uint_as_float(v[i])) : m;
-  return m;
+  for (int i = 0; i < 64; ++i) {
+    const float x = (i < rem) ? __uint_as_float(v[i]) : -INFINITY;
+    m[i & 3] = fmaxf(m[i & 3], x);
+  }
 }
 
 template <int MODE, int KR>
@@ -150,7 +161,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       mbar_init(bar_afull(b), 1);
       mbar_init(bar_aempty(b), 1);
       mbar_init(bar_tfull(b), 1);
-      mbar_init(bar_tempty(b), 4);
+      mbar_init(bar_tempty(b), 4);  // the 4 warps of the epilogue group that owns buffer b
     }
     fence_mbarrier_init();
   }
@@ -231,9 +242,12 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     }
   } else if (warp >= 4) {
     // ================= epilogue: masked max over doc tokens, masked sum over query tokens ====
+    // Group e owns TMEM accumulator e, i.e. the chunks with global chunk counter t % 2 == e, so each
+    // group has two MMA periods per chunk to drain its accumulator.
     const uint32_t qslot = warp & 3u;
-    const uint32_t lane_base = (qslot * 32u) << 16;
-    uint32_t t = 0;
+    const uint32_t grp = (warp - 4u) >> 2;
+    const uint32_t taddr_base = tmem_base + ((qslot * 32u) << 16) + grp * kAccStride;
+    uint32_t t = 0, mine = 0;
     for (int32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       int32_t g, p;
       int64_t c0, c1;
@@ -242,24 +256,27 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       const int32_t lq = q < args.n_q ? __ldg(args.q_lens + q) : 0;
       WarpTopK<KR> topk;
       topk.init();
-      int32_t ld_next = (c0 < c1) ? __ldg(args.d_lens + c0) : 0;
-      for (int64_t c = c0; c < c1; ++c, ++t) {
+      // first chunk of this unit owned by this group
+      const int64_t first = c0 + (int64_t)((grp - (t & 1u)) & 1u);
+      t += (uint32_t)(c1 - c0);
+      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + first) : 0;
+      for (int64_t c = first; c < c1; c += 2, ++mine) {
         const int32_t ld = ld_next;
-        if (c + 1 < c1) ld_next = __ldg(args.d_lens + c + 1);
-        const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
-        mbar_wait(bar_tfull(acc), tph);
+        if (c + 2 < c1) ld_next = __ldg(args.d_lens + c + 2);
+        mbar_wait(bar_tfull(grp), mine & 1u);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + lane_base + acc * kAccStride;
-        float m = -INFINITY;
-        for (int32_t col = 0; col < ld; col += 32) {
-          uint32_t v[32];
-          tmem_ld32_wait(taddr + (uint32_t)col, v);
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int32_t col = 0; col < ld; col += 64) {
+          uint32_t v[64];
+          tmem_ld64_wait(taddr_base + (uint32_t)col, v);
           const int rem = ld - col;
-          m = (rem >= 32) ? max32(v, m) : max32_masked(v, m, rem);
+          if (rem >= 64) max64(v, m4);
+          else max64_masked(v, m4, rem);
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_tempty(acc));
+        if (lane == 0) mbar_arrive(bar_tempty(grp));
+        const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         float sv = ((int32_t)lane < lq) ? m : 0.0f;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
@@ -272,7 +289,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         }
       }
       if constexpr (MODE == 1) {
-        uint64_t* dst = args.partial + ((int64_t)p * args.n_groups * 4 + q) * args.k;
+        // partial lists: [P][kEpiGroups][4G = n_q_pad][k]
+        uint64_t* dst = args.partial +
+                        (((int64_t)p * kEpiGroups + grp) * args.n_groups * 4 + q) * args.k;
 #pragma unroll
         for (int r = 0; r < KR; ++r) {
           const int i = r * 32 + (int)lane;

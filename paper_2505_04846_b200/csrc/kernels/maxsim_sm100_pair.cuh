@@ -1,0 +1,210 @@
+// maxsim_sm100_pair.cuh -- steps a3-a6 on a CTA pair (cta_group::2): the production MaxSim kernel.
+//
+//   S(q, c) = sum_{i < len_q} max_{j < len_c} < q_i , d_{c,j} >       (§2.2, Fig.3B
+//                                                                    PAPER.md:228)
+//
+// Same method and epilogue as maxsim_sm100.cuh, but two SMs of a TPC cooperate on every MMA:
+//  * a cluster of 2 CTAs owns a "row-group pair" of 8 queries (256 query-token rows): CTA r keeps
+//    the A tile of queries 8g+4r .. 8g+4r+3 (128 rows) resident in its shared memory;
+//  * per chunk, CTA r TMA-loads only token rows [r*ld_pad/2, (r+1)*ld_pad/2) of the chunk, so each SM
+//    fills half as many B bytes per MMA FLOP as the single-CTA kernel (L2->SMEM and SMEM-port
+//    traffic halved: the profiled limiter of the M = 128 kernel);
+//  * the leader CTA's single MMA thread issues tcgen05.mma.cta_group::2 with M = 256, N = ld_pad,
+//    K = 16: the hardware reads A and B halves from both CTAs' shared memory and writes each CTA's
+//    128 accumulator rows into that CTA's TMEM (128 lanes x ld_pad fp32 columns);
+//  * each CTA's two epilogue warpgroups drain their own TMEM exactly as in the single-CTA kernel and
+//    release the accumulator to the leader with a cluster-scope mbarrier arrive.
+// Barriers: full[s] / a_full[b] / t_empty[b] live in the leader (both CTAs' TMA complete_tx and both
+// CTAs' epilogue arrivals land there); empty[s] / a_empty[b] / t_full[b] exist in both CTAs and are
+// signalled by the leader's multicast tcgen05.commit.
+#pragma once
+#include "maxsim_sm100.cuh"
+
+namespace hiper {
+
+template <int MODE, int KR>
+__global__ void __launch_bounds__(kMaxsimThreads, 1)
+    maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                             const __grid_constant__ CUtensorMap tmap_d, const MaxsimArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  using namespace ptx;
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();  // 0 = leader
+  const uint32_t pair = cluster_id_x();
+  const uint32_t n_pairs = nclusters_x();
+
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sA = base;                   // 2 x a_bytes (this CTA's 128 query rows)
+  const uint32_t sB = sA + 2 * args.a_bytes;  // n_stages x stage_bytes (this CTA's half chunk)
+  const uint32_t sBar = sB + args.n_stages * args.stage_bytes;
+  const int S = args.n_stages;
+  auto bar_full = [&](int s) { return sBar + 8u * s; };
+  auto bar_empty = [&](int s) { return sBar + 8u * (S + s); };
+  auto bar_afull = [&](int b) { return sBar + 8u * (2 * S + b); };
+  auto bar_aempty = [&](int b) { return sBar + 8u * (2 * S + 2 + b); };
+  auto bar_tfull = [&](int b) { return sBar + 8u * (2 * S + 4 + b); };
+  auto bar_tempty = [&](int b) { return sBar + 8u * (2 * S + 6 + b); };
+  const uint32_t sTmemPtr = sBar + 8u * (2 * S + 8);
+  uint32_t* tmem_ptr_generic =
+      reinterpret_cast<uint32_t*>(smem_raw + (sTmemPtr - smem_u32(smem_raw)));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(bar_full(s), 1);   // leader's producer arrive (+ both CTAs' tx bytes)
+      mbar_init(bar_empty(s), 1);  // leader's multicast commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar_afull(b), 1);
+      mbar_init(bar_aempty(b), 1);
+      mbar_init(bar_tfull(b), 1);
+      mbar_init(bar_tempty(b), 8);  // 4 warps of the owning epilogue group in each of the 2 CTAs
+    }
+    fence_mbarrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(sTmemPtr, kTmemCols);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr_generic);
+
+  const int32_t n_units = args.n_groups * args.n_parts;  // n_groups = row-group pairs (8 queries)
+  const int32_t half_rows = args.ld_pad >> 1;
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs) =================
+    if (lane == 0) {
+      prefetch_tmap(&tmap_q);
+      prefetch_tmap(&tmap_d);
+      int s = 0;
+      uint32_t ph = 0, it = 0;
+      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
+        int32_t g, p;
+        int64_t c0, c1;
+        unit_decode(args, u, g, p, c0, c1);
+        const uint32_t ab = it & 1u, aph = (it >> 1) & 1u;
+        mbar_wait(bar_aempty(ab), aph ^ 1u);
+        if (rank == 0) mbar_arrive_expect_tx(bar_afull(ab), 2u * args.a_bytes);
+        const uint32_t afull_leader = mapa_shared(bar_afull(ab), 0);
+        for (int kb = 0; kb < args.num_kb; ++kb)
+          tma_load_2d_pair(sA + ab * args.a_bytes + kb * 16384u, &tmap_q, afull_leader, kb * 64,
+                           (int32_t)((2 * g + (int32_t)rank) * 128));
+        for (int64_t c = c0; c < c1; ++c) {
+          for (int kb = 0; kb < args.num_kb; ++kb) {
+            mbar_wait(bar_empty(s), ph ^ 1u);
+            if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
+            tma_load_2d_pair(sB + s * args.stage_bytes, &tmap_d, mapa_shared(bar_full(s), 0),
+                             kb * 64, (int32_t)(c * args.ld_pad + (int64_t)rank * half_rows));
+            if (++s == S) { s = 0; ph ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer: leader CTA, single thread =================
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(256, (uint32_t)args.ld_pad);
+      int s = 0;
+      uint32_t ph = 0, it = 0, t = 0;
+      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
+        int32_t g, p;
+        int64_t c0, c1;
+        unit_decode(args, u, g, p, c0, c1);
+        const uint32_t ab = it & 1u, aph = (it >> 1) & 1u;
+        mbar_wait(bar_afull(ab), aph);
+        tc_fence_after();
+        const uint32_t a_tile = sA + ab * args.a_bytes;
+        for (int64_t c = c0; c < c1; ++c, ++t) {
+          const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
+          mbar_wait(bar_tempty(acc), tph ^ 1u);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * kAccStride;
+          for (int kb = 0; kb < args.num_kb; ++kb) {
+            mbar_wait(bar_full(s), ph);
+            tc_fence_after();
+            const uint32_t a_kb = a_tile + kb * 16384u;
+            const uint32_t b_st = sB + s * args.stage_bytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_kb + kk * 32),
+                               umma_desc_sw128(b_st + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
+            mma_commit_pair_mc(bar_empty(s), 0x3);  // both CTAs' stage s free again
+            if (++s == S) { s = 0; ph ^= 1u; }
+          }
+          mma_commit_pair_mc(bar_tfull(acc), 0x3);  // both CTAs' accumulator rows ready
+        }
+        mma_commit_pair_mc(bar_aempty(ab), 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs, each on its own 128 TMEM lanes) =================
+    const uint32_t qslot = warp & 3u;
+    const uint32_t grp = (warp - 4u) >> 2;
+    const uint32_t taddr_base = tmem_base + ((qslot * 32u) << 16) + grp * kAccStride;
+    const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), 0);
+    uint32_t t = 0, mine = 0;
+    for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
+      int32_t g, p;
+      int64_t c0, c1;
+      unit_decode(args, u, g, p, c0, c1);
+      const int32_t q = g * 8 + (int32_t)rank * 4 + (int32_t)qslot;
+      const int32_t lq = q < args.n_q ? __ldg(args.q_lens + q) : 0;
+      WarpTopK<KR> topk;
+      topk.init();
+      const int64_t first = c0 + (int64_t)((grp - (t & 1u)) & 1u);
+      t += (uint32_t)(c1 - c0);
+      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + first) : 0;
+      for (int64_t c = first; c < c1; c += 2, ++mine) {
+        const int32_t ld = ld_next;
+        if (c + 2 < c1) ld_next = __ldg(args.d_lens + c + 2);
+        mbar_wait(bar_tfull(grp), mine & 1u);
+        tc_fence_after();
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int32_t col = 0; col < ld; col += 64) {
+          uint32_t v[64];
+          tmem_ld64_wait(taddr_base + (uint32_t)col, v);
+          const int rem = ld - col;
+          if (rem >= 64) max64(v, m4);
+          else max64_masked(v, m4, rem);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        float sv = ((int32_t)lane < lq) ? m : 0.0f;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        sv += 0.0f;  // canonical +0
+        if constexpr (MODE == 0) {
+          if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + c] = sv;
+        } else {
+          const uint64_t key = make_key(sv, args.id_base + c);
+          if (key > topk.thresh) topk.insert(key, args.k, lane);
+        }
+      }
+      if constexpr (MODE == 1) {
+        // partial lists: [P][kEpiGroups][8G][k]
+        uint64_t* dst = args.partial +
+                        (((int64_t)p * kEpiGroups + grp) * args.n_groups * 8 + q) * args.k;
+#pragma unroll
+        for (int r = 0; r < KR; ++r) {
+          const int i = r * 32 + (int)lane;
+          if (i < args.k) dst[i] = topk.v[r];
+        }
+      }
+    }
+  }
+
+  // teardown: every multicast commit / remote arrive has landed before either CTA exits
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kTmemCols);
+  }
+}
+
+}  // namespace hiper

@@ -101,7 +101,7 @@ def test_layout_bitwise(H, dtype, var_len, L):
     assert lay.shape == (37, ld_pad, 128)
     assert np.array_equal(lay, expected_layout(corp, clen, ld_pad))
     ql = query_layout(H, q, qlen)
-    exp_q = np.zeros((12, 32, 128), dtype=np.uint16)
+    exp_q = np.zeros((16, 32, 128), dtype=np.uint16)
     exp_q[:9] = expected_layout(q, qlen, 32)
     assert np.array_equal(ql, exp_q)
 
