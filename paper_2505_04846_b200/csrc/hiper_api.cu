@@ -513,13 +513,23 @@ static hiper_status profile_end(cudaStream_t stream, const std::pair<cudaEvent_t
   return HIPER_OK;
 }
 
+static int debug_mode() {
+  static const int m = [] {
+    const char* e = getenv("HIPER_DEBUG_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
+}
+
 template <int MODE, int KR>
 static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
                                     const MaxsimArgs& a, cudaStream_t stream) {
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   bool rec = false;
   if (kp.pair) {
-    auto kern = maxsim_sm100_pair_kernel<MODE, KR>;
+    auto kern = maxsim_sm100_pair_kernel<MODE, KR, 0>;
+    if (MODE == 1 && KR == 1 && debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1>;
+    if (MODE == 1 && KR == 1 && debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)kp.grid);

@@ -22,7 +22,10 @@
 
 namespace hiper {
 
-template <int MODE, int KR>
+// DBG (ablation builds only, selected by HIPER_DEBUG_MODE): 0 = production; 1 = epilogue skips the
+// TMEM reads and reductions (measures the TMA + MMA pipeline alone); 2 = additionally no chunk TMA
+// after the first stage fill (measures MMA issue alone).  DBG != 0 results are meaningless.
+template <int MODE, int KR, int DBG = 0>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_d, const MaxsimArgs args) {
@@ -95,9 +98,13 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         for (int64_t c = c0; c < c1; ++c) {
           for (int kb = 0; kb < args.num_kb; ++kb) {
             mbar_wait(bar_empty(s), ph ^ 1u);
-            if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
-            tma_load_2d_pair(sB + s * args.stage_bytes, &tmap_d, mapa_shared(bar_full(s), 0),
-                             kb * 64, (int32_t)(c * args.ld_pad + (int64_t)rank * half_rows));
+            if (DBG == 2 && (c > c0 || it > 0)) {
+              if (rank == 0) mbar_arrive(bar_full(s));
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
+              tma_load_2d_pair(sB + s * args.stage_bytes, &tmap_d, mapa_shared(bar_full(s), 0),
+                               kb * 64, (int32_t)(c * args.ld_pad + (int64_t)rank * half_rows));
+            }
             if (++s == S) { s = 0; ph ^= 1u; }
           }
         }
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         mbar_wait(bar_tfull(grp), mine & 1u);
         tc_fence_after();
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        for (int32_t col = 0; col < ld; col += 64) {
+        for (int32_t col = 0; col < (DBG ? 0 : ld); col += 64) {
           uint32_t v[64];
           tmem_ld64_wait(taddr_base + (uint32_t)col, v);
           const int rem = ld - col;
