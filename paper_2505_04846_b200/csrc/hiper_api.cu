@@ -447,7 +447,10 @@ static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int64_t n_chunks
   kp.n_groups = n_q_pad_of(n_q) / kp.qpg;
   kp.n_parts = choose_parts(kp.n_groups, n_chunks, slots);
   kp.a_bytes = (uint32_t)(dim / 64) * 16384u;
-  kp.stage_bytes = (uint32_t)(kp.pair ? ld_pad / 2 : ld_pad) * 128u;
+  // pair kernel: one stage = this CTA's half of a whole chunk (all K-blocks); single-CTA kernel:
+  // one stage = one 64-dim K-block of a whole chunk
+  kp.stage_bytes = kp.pair ? (uint32_t)(ld_pad / 2) * 128u * (uint32_t)(dim / 64)
+                           : (uint32_t)ld_pad * 128u;
   const uint32_t fixed = 1024u /*align slack*/ + 2u * kp.a_bytes + 512u /*barriers*/;
   const uint32_t avail = (uint32_t)di.max_smem > fixed ? (uint32_t)di.max_smem - fixed : 0u;
   kp.n_stages = (int32_t)std::min<uint32_t>(kp.pair ? 12u : 8u, avail / kp.stage_bytes);

@@ -25,6 +25,9 @@ namespace hiper {
 // DBG (ablation builds only, selected by HIPER_DEBUG_MODE): 0 = production; 1 = epilogue skips the
 // TMEM reads and reductions (measures the TMA + MMA pipeline alone); 2 = additionally no chunk TMA
 // after the first stage fill (measures MMA issue alone).  DBG != 0 results are meaningless.
+// warps 0-7: epilogue groups 0/1; 8: TMEM allocator; 9: spare; 10: TMA producer; 11: MMA issuer
+constexpr uint32_t kPairAllocWarp = 8, kPairProducerWarp = 10, kPairMmaWarp = 11;
+
 template <int MODE, int KR, int DBG = 0>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     }
     fence_mbarrier_init();
   }
-  if (warp == 2) {
+  if (warp == kPairAllocWarp) {
     tmem_alloc_pair(sTmemPtr, kTmemCols);
     tmem_relinquish_pair();
   }
@@ -76,8 +79,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
 
   const int32_t n_units = args.n_groups * args.n_parts;  // n_groups = row-group pairs (8 queries)
   const int32_t half_rows = args.ld_pad >> 1;
+  const uint32_t half_tile = (uint32_t)half_rows * 128u;  // one 64-dim K-block of this CTA's half chunk
 
-  if (warp == 0) {
+  if (warp == kPairProducerWarp) {
     // ================= TMA producer (both CTAs) =================
     if (lane == 0) {
       prefetch_tmap(&tmap_q);
@@ -96,22 +100,24 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           tma_load_2d_pair(sA + ab * args.a_bytes + kb * 16384u, &tmap_q, afull_leader, kb * 64,
                            (int32_t)((2 * g + (int32_t)rank) * 128));
         for (int64_t c = c0; c < c1; ++c) {
-          for (int kb = 0; kb < args.num_kb; ++kb) {
-            mbar_wait(bar_empty(s), ph ^ 1u);
-            if (DBG == 2 && (c > c0 || it > 0)) {
-              if (rank == 0) mbar_arrive(bar_full(s));
-            } else {
-              if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
-              tma_load_2d_pair(sB + s * args.stage_bytes, &tmap_d, mapa_shared(bar_full(s), 0),
+          // one stage = this CTA's half of one whole chunk (all dim/64 K-blocks)
+          mbar_wait(bar_empty(s), ph ^ 1u);
+          if (DBG == 2 && (c > c0 || it > 0)) {
+            if (rank == 0) mbar_arrive(bar_full(s));
+          } else {
+            if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
+            const uint32_t full_leader = mapa_shared(bar_full(s), 0);
+            for (int kb = 0; kb < args.num_kb; ++kb)
+              tma_load_2d_pair(sB + s * args.stage_bytes + kb * half_tile, &tmap_d, full_leader,
                                kb * 64, (int32_t)(c * args.ld_pad + (int64_t)rank * half_rows));
-            }
-            if (++s == S) { s = 0; ph ^= 1u; }
           }
+          if (++s == S) { s = 0; ph ^= 1u; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kPairMmaWarp) {
     // ================= MMA issuer: leader CTA, single thread =================
+    // (highest warp id: the SMSP arbiter favours it over the epilogue warps sharing its SMSP)
     if (rank == 0 && lane == 0) {
       const uint32_t idesc = idesc_bf16_f32(256, (uint32_t)args.ld_pad);
       int s = 0;
@@ -129,27 +135,29 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           mbar_wait(bar_tempty(acc), tph ^ 1u);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
+          mbar_wait(bar_full(s), ph);
+          tc_fence_after();
+          const uint32_t b_st = sB + s * args.stage_bytes;
           for (int kb = 0; kb < args.num_kb; ++kb) {
-            mbar_wait(bar_full(s), ph);
-            tc_fence_after();
             const uint32_t a_kb = a_tile + kb * 16384u;
-            const uint32_t b_st = sB + s * args.stage_bytes;
+            const uint32_t b_kb = b_st + kb * half_tile;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               mma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_kb + kk * 32),
-                               umma_desc_sw128(b_st + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
-            mma_commit_pair_mc(bar_empty(s), 0x3);  // both CTAs' stage s free again
-            if (++s == S) { s = 0; ph ^= 1u; }
+                               umma_desc_sw128(b_kb + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
           }
+          mma_commit_pair_mc(bar_empty(s), 0x3);  // both CTAs' stage s free again
+          if (++s == S) { s = 0; ph ^= 1u; }
           mma_commit_pair_mc(bar_tfull(acc), 0x3);  // both CTAs' accumulator rows ready
         }
         mma_commit_pair_mc(bar_aempty(ab), 0x3);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ================= epilogue (both CTAs, each on its own 128 TMEM lanes) =================
+    // warp w reads TMEM lanes 32*(w%4)..+31 (the hardware's lane-quarter rule).
     const uint32_t qslot = warp & 3u;
-    const uint32_t grp = (warp - 4u) >> 2;
+    const uint32_t grp = warp >> 2;
     const uint32_t taddr_base = tmem_base + ((qslot * 32u) << 16) + grp * kAccStride;
     const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), 0);
     uint32_t t = 0, mine = 0;
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   // teardown: every multicast commit / remote arrive has landed before either CTA exits
   tc_fence_before();
   cluster_sync();
-  if (warp == 2) {
+  if (warp == kPairAllocWarp) {
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, kTmemCols);
   }
