@@ -208,7 +208,7 @@ def run_reference(a, rank, world):
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------------------ our arm
@@ -260,11 +260,11 @@ def run_ours(a, rank, local_rank, world):
     for _ in range(max(a.warmup, 0)):
         step()
     launches_per_step = H.last_launch_count()
-    barrier()
     clocks = ClockSampler(list(range(world))) if rank == 0 else None
     if clocks:
         clocks.start()
         time.sleep(0.3)
+    barrier()  # after the sampler started: every rank enters the timed region together
     H.hiper_profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -345,21 +345,39 @@ def run_ours(a, rank, local_rank, world):
             "sample": (f"{nq} queries x {C_s} chunks ({dt:.1f} s: query NORM + MaxSim + top-k), "
                        f"extrapolated linearly to {a.chunks} chunks; float64 C oracle, OpenMP"),
         }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
+_RESULT_FD = None
+
+
+def emit(line: dict):
+    """Print the ONE JSON result line to the real stdout (library chatter goes to stderr)."""
+    os.write(_RESULT_FD if _RESULT_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _RESULT_FD
+    # NCCL / CUDA libraries may write to fd 1; keep the real stdout for the result line only.
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
     a = parse()
     rank = int(os.environ.get("RANK", 0))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    if a.impl == "reference":
-        run_reference(a, rank, world)
-        return
-    run_ours(a, rank, local_rank, world)
+    try:
+        if a.impl == "reference":
+            run_reference(a, rank, world)
+            return
+        run_ours(a, rank, local_rank, world)
+    except BaseException:
+        import traceback
+        sys.stderr.write(f"[bench rank {rank}] failed:\n{traceback.format_exc()}")
+        sys.stderr.flush()
+        raise
 
 
 if __name__ == "__main__":
