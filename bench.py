@@ -39,26 +39,41 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--chunks", type=int, default=1_000_000)
-    ap.add_argument("--queries", type=int, default=1024)
-    ap.add_argument("--k", type=int, default=10)
-    ap.add_argument("--chunk-len", type=int, default=256)
-    ap.add_argument("--query-len", type=int, default=32)
-    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--workload", choices=["config3", "config4", "config5", "config2"],
+                    default="config3",
+                    help="config3 (default, N=1 headline): 1M x 256-token chunks, Q=1024, top-10; "
+                         "config4: 3.6M chunks, top-100 (N>=2); config5: pooled 3.6M x 768, "
+                         "Q=4096, top-10; config2: ColTrast step B=256 scores + InfoNCE")
+    ap.add_argument("--chunks", type=int, default=None)
+    ap.add_argument("--queries", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--chunk-len", type=int, default=None)
+    ap.add_argument("--query-len", type=int, default=None)
+    ap.add_argument("--dim", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--qseed", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target CPU work for the cpu_baseline sample")
-    return ap.parse_args()
+    a = ap.parse_args()
+    defaults = {  # BASELINE.json configs
+        "config3": dict(chunks=1_000_000, queries=1024, k=10, chunk_len=256, query_len=32, dim=128),
+        "config4": dict(chunks=3_600_000, queries=1024, k=100, chunk_len=256, query_len=32, dim=128),
+        "config5": dict(chunks=3_600_000, queries=4096, k=10, chunk_len=1, query_len=1, dim=768),
+        "config2": dict(chunks=256, queries=256, k=1, chunk_len=256, query_len=32, dim=128),
+    }[a.workload]
+    for key, v in defaults.items():
+        if getattr(a, key) is None:
+            setattr(a, key, v)
+    return a
 
 
 def workload_config(a, world):
     return {
-        "workload": (f"{'config3' if a.chunks == 1_000_000 else 'config4' if a.chunks == 3_600_000 else 'custom'}: "
-                     f"{a.chunks} chunks x {a.chunk_len} tokens, dim {a.dim}, bf16, query batch "
-                     f"{a.queries} x {a.query_len} tokens, top-{a.k}"),
+        "workload": (f"{a.workload}: {a.chunks} chunks x {a.chunk_len} tokens, dim {a.dim}, bf16, "
+                     f"query batch {a.queries} x {a.query_len} tokens, top-{a.k}"
+                     + (" (pooled single-vector limit case)" if a.chunk_len == 1 else "")),
         "chunks": a.chunks, "chunk_len": a.chunk_len, "dim": a.dim, "query_batch": a.queries,
         "query_len": a.query_len, "k": a.k, "corpus_per_gpu": a.chunks // world,
         "parallelism": f"corpus-sharded x{world}, one ncclAllGather of top-k keys" if world > 1
@@ -146,7 +161,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ oracle leg
-def oracle_sample(a, n_chunks_sample, n_queries_sample=4):
+def oracle_sample(a, n_chunks_sample, n_queries_sample=None):
     """Time the CPU oracle (as it stands) on a bounded sample of the same workload.
 
     Timed: NORM of the sample queries + MaxSim of every (query, chunk) pair + exact top-k.
@@ -156,6 +171,8 @@ def oracle_sample(a, n_chunks_sample, n_queries_sample=4):
     import oracle
     from synth import gen
     cores = len(os.sched_getaffinity(0))
+    if n_queries_sample is None:
+        n_queries_sample = 256 if a.chunk_len == 1 else 4
     C_s = int(n_chunks_sample)
     corp = gen.corpus(a.seed, 0, C_s, a.chunk_len, a.dim)
     cn = oracle.norm_rows(corp)
@@ -177,7 +194,7 @@ def oracle_sample(a, n_chunks_sample, n_queries_sample=4):
 def calibrated_oracle(a, seconds):
     # a short calibration run, then one run sized to ~`seconds` of CPU work
     _, dt0, cores, c0, nq = oracle_sample(a, 64)
-    C_s = int(max(64, min(200_000, 64 * seconds / max(dt0, 1e-3))))
+    C_s = int(max(64, min(200_000, 64 * seconds / max(dt0, 1e-3), a.chunks)))
     return oracle_sample(a, C_s, nq)
 
 
@@ -189,7 +206,7 @@ def run_reference(a, rank, world):
     oracle.build()
     per_step = max(1.0, min(6.0, 150.0 / max(1, a.steps + a.warmup)))
     _, dt0, cores, _, nq = oracle_sample(a, 64)
-    C_s = int(max(64, min(200_000, 64 * per_step / max(dt0, 1e-3))))
+    C_s = int(max(64, min(200_000, 64 * per_step / max(dt0, 1e-3), a.chunks)))
     times = []
     for i in range(a.warmup + a.steps):
         qps, dt, cores, C_s, nq = oracle_sample(a, C_s, nq)
@@ -359,6 +376,117 @@ def emit(line: dict):
     os.write(_RESULT_FD if _RESULT_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
+def run_coltrast(a, rank, local_rank, world):
+    """--workload config2: the ColTrast training-step hot path (a10 + a11), B x B in-batch MaxSim
+    scores + row-logsumexp InfoNCE, one independent replica per GPU ("local rank only")."""
+    import numpy as np
+    import torch
+
+    import paper_2505_04846_b200 as H
+    from synth import gen
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    B, L, Lq, d = a.queries, a.chunk_len, a.query_len, a.dim
+    seed, qseed = 3 + 100 * rank, 4 + 100 * rank
+    to_dev = lambda x: torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16)
+    docs = to_dev(gen.corpus(seed, 0, B, L, d))
+    qs = to_dev(gen.queries(qseed, B, Lq, d, corpus_seed=seed, n_chunks=B, L=L, diagonal=True,
+                            sigma_q=gen.SIGMA_Q_HARD))
+    ql, dl = np.full(B, Lq, np.int32), np.full(B, L, np.int32)
+    ws = H.ColtrastWorkspace(B, B, L, d)
+    out = (torch.empty((B, B), dtype=torch.float32, device="cuda"),
+           torch.empty(1, dtype=torch.float32, device="cuda"))
+    stream = torch.cuda.current_stream()
+
+    def step(qd=qs, dd=docs):
+        H.hiper_coltrast_scores_loss(qd, ql, dd, dl, temperature=1.0, workspace=ws, out=out,
+                                     stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    launches = H.last_launch_count()
+    steps = max(a.steps, 50)  # a step is ~0.1 ms: time many
+    clocks = ClockSampler(list(range(world))) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    barrier()
+    H.hiper_profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    barrier()
+    H.hiper_profile_enable(False)
+    kern_ms, kern_n = H.hiper_profile_read()
+    clk = clocks.stop() if clocks else None
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    kern_avg = max_over_ranks(kern_ms / max(kern_n, 1))
+    # e2e: host inputs in, loss out, every step
+    qh, dh = qs.cpu().pin_memory(), docs.cpu().pin_memory()
+    qd, dd = torch.empty_like(qs), torch.empty_like(docs)
+    lh = torch.empty(1, dtype=torch.float32).pin_memory()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(steps):
+        qd.copy_(qh, non_blocking=True)
+        dd.copy_(dh, non_blocking=True)
+        step(qd, dd)
+        lh.copy_(out[1], non_blocking=True)
+    f1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(f0.elapsed_time(f1))
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    flops = 2.0 * B * B * Lq * L * d
+    peak, peak_src = load_peaks()
+    value = world * steps / (ms / 1e3)
+    line = {
+        "metric": "ColTrast in-batch MaxSim scores + InfoNCE steps/s (B=256, configs[1])",
+        "value": value, "unit": "steps/s", "n_gpus": world, "steps": steps, "warmup": a.warmup,
+        "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"config2: B={B} queries x {Lq} tokens vs {B} chunks x {L} tokens, "
+                               f"dim {d}, tau 1, replicas only", "parallelism": f"dp{world} replicas"},
+        "roofline": {"bound": "tensor", "achieved": flops / (kern_avg / 1e3) / 1e12, "peak": peak,
+                     "unit": "TFLOP/s", "frac": flops / (kern_avg / 1e3) / 1e12 / peak,
+                     "traffic": None, "kernel": "maxsim_sm100_pair_kernel MODE 0",
+                     "kernel_ms_per_launch": kern_avg, "peak_source": peak_src,
+                     "kernel_share_of_step": kern_avg / (ms / steps)},
+        "e2e": {"value": world * steps / (ms_e2e / 1e3), "unit": "steps/s",
+                "h2d_bytes_per_step": (qh.numel() + dh.numel()) * 2 * world,
+                "d2h_bytes_per_step": 4 * world},
+        "gpu_launches": launches * steps, "clocks": clk,
+        "extra": {"loss": float(out[1].item()), "tflops_step": flops * world * steps / (ms / 1e3) / 1e12},
+    }
+    emit(line)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     global _RESULT_FD
     # NCCL / CUDA libraries may write to fd 1; keep the real stdout for the result line only.
@@ -371,6 +499,9 @@ def main():
     try:
         if a.impl == "reference":
             run_reference(a, rank, world)
+            return
+        if a.workload == "config2":
+            run_coltrast(a, rank, local_rank, world)
             return
         run_ours(a, rank, local_rank, world)
     except BaseException:

@@ -23,6 +23,7 @@
 #include "kernels/infonce.cuh"
 #include "kernels/maxsim_sm100.cuh"
 #include "kernels/maxsim_sm100_pair.cuh"
+#include "kernels/pooled_sm100_pair.cuh"
 #include "kernels/norm_layout.cuh"
 #include "kernels/topk_merge.cuh"
 
@@ -206,10 +207,17 @@ struct hiper_index_s {
   alignas(64) CUtensorMap tmap_half;  // box = 64 dims x ld_pad/2 rows (CTA-pair kernel)
 };
 
-static hiper_status check_dims(int32_t dim) {
+// Token path (max_len > 1): dim in {64, 128}.  Pooled path (one row per item, a12): dim % 64 == 0,
+// 64 <= dim <= 4096.
+static hiper_status check_dims(int32_t dim, bool pooled = false) {
   if (dim <= 0) return fail(HIPER_ERR_INVALID_ARG, "dim must be positive (got %d)", dim);
+  if (pooled) {
+    if (dim % 64 != 0 || dim > 4096)
+      return fail(HIPER_ERR_UNSUPPORTED, "pooled dim %d unsupported (multiple of 64, <= 4096)", dim);
+    return HIPER_OK;
+  }
   if (dim != 64 && dim != 128)
-    return fail(HIPER_ERR_UNSUPPORTED, "dim %d unsupported (round 1 supports 64 and 128)", dim);
+    return fail(HIPER_ERR_UNSUPPORTED, "dim %d unsupported for token rows (64 or 128)", dim);
   return HIPER_OK;
 }
 
@@ -258,17 +266,18 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   if (dtype != HIPER_F32 && dtype != HIPER_BF16) return fail(HIPER_ERR_INVALID_ARG, "bad dtype");
   if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_BORROW_TOKENS))
     return fail(HIPER_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
-  TRY(check_dims(dim));
   if (max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "max_len must be >= 1");
   if (max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "max_len %d > 256", max_len);
+  const bool pooled = (max_len == 1);  // one vector per chunk: the pooled limit case (a12)
+  TRY(check_dims(dim, pooled));
   if (id_base < 0 || id_base + n >= 0xFFFFFFFFll)
     return fail(HIPER_ERR_UNSUPPORTED, "global ids must be < 2^32-1");
-  const int32_t ld_pad = (int32_t)round_up(max_len, 16);
+  const int32_t ld_pad = pooled ? 1 : (int32_t)round_up(max_len, 16);
   if (n * ld_pad >= 0x7FFFFFFFll)
     return fail(HIPER_ERR_UNSUPPORTED, "n * ld_pad >= 2^31 rows for one index; shard the corpus");
   TRY(check_lens(lens, n, max_len, "chunk"));
   const bool borrow = (flags & HIPER_BORROW_TOKENS) != 0;
-  if (borrow && (dtype != HIPER_BF16 || max_len != ld_pad))
+  if (borrow && (dtype != HIPER_BF16 || max_len != ld_pad || (dim % 8) != 0))
     return fail(HIPER_ERR_INVALID_ARG, "HIPER_BORROW_TOKENS needs bf16 tokens and max_len %% 16 == 0");
   if (n > 0) {
     if (!tokens) return fail(HIPER_ERR_INVALID_ARG, "tokens is NULL");
@@ -322,8 +331,12 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     }
     if (hstat & kStatusNonFinite) { st = fail(HIPER_ERR_NONFINITE, "chunk tokens contain non-finite values"); break; }
     if (hstat & kStatusZeroRow) { st = fail(HIPER_ERR_ZERO_VECTOR, "a chunk token row has norm 0"); break; }
-    if (n > 0) st = make_tmap(&ix->tmap, ix->tok, n * (int64_t)ld_pad, dim, ld_pad);
-    if (n > 0 && st == HIPER_OK) st = make_tmap(&ix->tmap_half, ix->tok, n * (int64_t)ld_pad, dim, ld_pad / 2);
+    if (n > 0 && pooled) {
+      st = make_tmap(&ix->tmap, ix->tok, n, dim, 128);  // pooled kernel: 128 chunk rows per CTA
+    } else if (n > 0) {
+      st = make_tmap(&ix->tmap, ix->tok, n * (int64_t)ld_pad, dim, ld_pad);
+      if (st == HIPER_OK) st = make_tmap(&ix->tmap_half, ix->tok, n * (int64_t)ld_pad, dim, ld_pad / 2);
+    }
   } while (0);
   cudaFree(status);
   if (st != HIPER_OK) return cleanup(st);
@@ -360,12 +373,15 @@ static constexpr int32_t kQSlot = 32;  // padded query-token rows per query (one
 static int32_t n_q_pad_of(int32_t n_q) { return (int32_t)round_up(std::max(n_q, 1), 8); }
 
 static hiper_status validate_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
-                                     int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags) {
+                                     int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags,
+                                     bool pooled = false) {
   if (dtype != HIPER_F32 && dtype != HIPER_BF16) return fail(HIPER_ERR_INVALID_ARG, "bad dtype");
   if (n_q < 0) return fail(HIPER_ERR_INVALID_ARG, "n_q < 0");
   if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_VALIDATE_SYNC))
     return fail(HIPER_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
-  TRY(check_dims(dim));
+  TRY(check_dims(dim, pooled));
+  if (pooled && q_max_len != 1)
+    return fail(HIPER_ERR_UNSUPPORTED, "a pooled index (max_len 1) takes pooled queries (q_max_len 1)");
   if (q_max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "q_max_len must be >= 1");
   if (q_max_len > kQSlot) return fail(HIPER_ERR_UNSUPPORTED, "q_max_len %d > 32", q_max_len);
   TRY(check_lens(q_lens, n_q, q_max_len, "query"));
@@ -646,14 +662,18 @@ extern "C" hiper_status hiper_comm_info(const hiper_comm* c, int32_t* world, int
 
 // ============================================================================ workspace layouts
 struct TopkWs {
-  size_t status = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0, total = 0;
+  size_t status = 0, progress = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0,
+         total = 0;
 };
+static constexpr int32_t kLockstepWindow = 192;  // chunks (12 MB of a 256 x 128 bf16 corpus)
 
 static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t k,
                            int32_t world, bool with_comm, TopkWs& w) {
   size_t off = 0;
   w.status = off;
   off += 256;
+  w.progress = off;
+  off += 1024;  // up to 256 pairs
   w.qlens = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
   w.qlayout = off;
@@ -674,9 +694,12 @@ static hiper_status check_ws(const void* ws, size_t have, size_t need) {
   return HIPER_OK;
 }
 
+static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, const hiper_comm* comm);
+
 extern "C" size_t hiper_maxsim_topk_workspace_size(const hiper_index* ix, int32_t n_q, int32_t k,
                                                    const hiper_comm* comm) {
   if (!ix || n_q < 0 || k < 1) return 0;
+  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, k, comm);
   int num_sms = 148;
   if (cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ix->device) != cudaSuccess) {
     cudaGetLastError();
@@ -696,6 +719,151 @@ extern "C" hiper_status hiper_workspace_status(const void* workspace, hiper_stre
 }
 
 // ============================================================================ top-k search
+// ============================================================================ pooled limit case (a12)
+// One vector per query and per chunk: S = <NORM(q), NORM(c)> via the K-pipelined pair GEMM with a
+// fused per-query register top-k (kernels/pooled_sm100_pair.cuh).
+constexpr int kPooledKP = 16;  // register top-k slots per query thread (k <= 16 on this path)
+
+struct PooledPlan {
+  int32_t n_qtiles = 0, n_ctiles = 0, n_parts = 0, n_stages = 0, q_pad = 0;
+  uint32_t stage_bytes = 32768u, smem_bytes = 0;
+  int grid = 0;
+};
+
+static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks, PooledPlan& pp) {
+  pp.n_qtiles = (int32_t)((std::max(n_q, 1) + 255) / 256);
+  pp.q_pad = pp.n_qtiles * 256;
+  const int64_t ct = (n_chunks + 255) / 256;
+  if (ct > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many chunks");
+  pp.n_ctiles = (int32_t)ct;
+  const int pairs = di.num_sms / 2;
+  pp.n_parts = choose_parts(pp.n_qtiles, pp.n_ctiles, pairs);
+  const uint32_t fixed = 1024u + 512u;
+  pp.n_stages = (int32_t)std::min<uint32_t>(8u, ((uint32_t)di.max_smem - fixed) / pp.stage_bytes);
+  if (pp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory");
+  pp.smem_bytes = fixed + pp.n_stages * pp.stage_bytes;
+  pp.grid = (int)std::min<int64_t>((int64_t)pp.n_qtiles * pp.n_parts, pairs) * 2;
+  return HIPER_OK;
+}
+
+template <int MODE>
+static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, const CUtensorMap& tc,
+                                  const PooledArgs& a, cudaStream_t stream) {
+  if (pp.grid == 0 || pp.n_parts == 0) return HIPER_OK;
+  auto kern = pooled_sm100_pair_kernel<MODE, kPooledKP>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem_bytes));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)pp.grid);
+  cfg.blockDim = dim3(kMaxsimThreads);
+  cfg.dynamicSmemBytes = pp.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  bool rec = false;
+  TRY(profile_begin(stream, &ev, &rec));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, tc, a));
+  TRY(profile_end(stream, ev, rec));
+  ++g_launches;
+  return HIPER_OK;
+}
+
+struct PooledWs {
+  size_t status = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0, total = 0;
+};
+static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t q_pad, int32_t k,
+                             int32_t world, bool with_comm, PooledWs& w) {
+  size_t off = 0;
+  w.status = off;
+  off += 256;
+  w.qlens = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
+  w.qlayout = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * dim * 2, 1024);
+  w.partial = off;
+  off = align_up(off + (size_t)n_parts * kEpiGroups * q_pad * k * 8, 256);
+  w.local = off;
+  if (with_comm) off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
+  w.gathered = off;
+  if (with_comm) off = align_up(off + (size_t)world * std::max(n_q, 1) * k * 8, 256);
+  w.total = off;
+}
+
+static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, hiper_dtype dtype,
+                                  const int32_t* q_lens, int32_t n_q, int32_t dim, int32_t k,
+                                  uint32_t flags, const hiper_comm* comm, void* workspace,
+                                  size_t workspace_bytes, float* out_scores, int64_t* out_ids,
+                                  float* dense_scores, cudaStream_t stream) {
+  if (!dense_scores && k > kPooledKP)
+    return fail(HIPER_ERR_UNSUPPORTED, "pooled top-k supports k <= %d (got %d)", kPooledKP, k);
+  DevInfo di;
+  TRY(device_info(di));
+  PooledPlan pp;
+  TRY(plan_pooled(di, n_q, ix->n, pp));
+  const int32_t world = comm ? comm->world : 1;
+  PooledWs w;
+  pooled_ws_layout(n_q, dim, pp.n_parts, pp.q_pad, dense_scores ? 1 : k, world, comm != nullptr, w);
+  TRY(check_ws(workspace, workspace_bytes, w.total));
+  uint8_t* ws = (uint8_t*)workspace;
+  uint32_t* status = (uint32_t*)(ws + w.status);
+  int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
+  __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
+  uint64_t* partial = (uint64_t*)(ws + w.partial);
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  TRY(stage_h2d(qlens_dev, q_lens, (size_t)n_q * 4, stream));
+  TRY(launch_norm(q_tokens, dtype, n_q, 1, qlens_dev, n_q, 1, dim, flags, qlayout, status, stream));
+  if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
+  PooledArgs a{};
+  a.n_q = n_q;
+  a.n_qtiles = pp.n_qtiles;
+  a.n_ctiles = pp.n_ctiles;
+  a.n_parts = pp.n_parts;
+  a.num_kb = dim / 64;
+  a.k = dense_scores ? 1 : k;
+  a.n_stages = pp.n_stages;
+  a.stage_bytes = pp.stage_bytes;
+  a.q_pad = pp.q_pad;
+  a.n_chunks = ix->n;
+  a.id_base = ix->id_base;
+  a.partial = partial;
+  a.scores = dense_scores;
+  a.score_ld = ix->n;
+  if (ix->n > 0) {
+    alignas(64) CUtensorMap tq;
+    TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
+    if (dense_scores) return launch_pooled<0>(pp, tq, ix->tmap, a, stream);
+    TRY(launch_pooled<1>(pp, tq, ix->tmap, a, stream));
+  }
+  const int32_t n_lists = ix->n > 0 ? pp.n_parts * kEpiGroups : 0;
+  const int64_t list_stride = (int64_t)pp.q_pad * k;
+  if (!comm || comm->world == 1)
+    return launch_merge(partial, n_lists, list_stride, n_q, k, k, nullptr, out_scores, out_ids, stream);
+  uint64_t* local = (uint64_t*)(ws + w.local);
+  uint64_t* gathered = (uint64_t*)(ws + w.gathered);
+  TRY(launch_merge(partial, n_lists, list_stride, n_q, k, k, local, nullptr, nullptr, stream));
+  NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, comm->comm, stream));
+  return launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream);
+}
+
+static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, const hiper_comm* comm) {
+  int num_sms = 148;
+  if (cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ix->device) != cudaSuccess) {
+    cudaGetLastError();
+    num_sms = 148;
+  }
+  const int32_t qt = (std::max(n_q, 1) + 255) / 256;
+  const int32_t ct = (int32_t)((ix->n + 255) / 256);
+  PooledWs w;
+  pooled_ws_layout(n_q, ix->dim, choose_parts(qt, ct, num_sms / 2), qt * 256, k,
+                   comm ? comm->world : 1, comm != nullptr, w);
+  return w.total;
+}
+
 extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_tokens,
                                           hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
                                           int32_t q_max_len, int32_t dim, int32_t k, uint32_t flags,
@@ -708,9 +876,13 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
   if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
   if (k < 1) return fail(HIPER_ERR_INVALID_ARG, "k must be >= 1");
   if (k > 128) return fail(HIPER_ERR_UNSUPPORTED, "k %d > 128", k);
-  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
+  const bool pooled = ix->ld_pad == 1;
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, pooled));
   if (n_q == 0) return HIPER_OK;
   if (!out_scores || !out_ids) return fail(HIPER_ERR_INVALID_ARG, "outputs are NULL");
+  if (pooled)
+    return pooled_search(ix, q_tokens, dtype, q_lens, n_q, dim, k, flags, comm, workspace,
+                         workspace_bytes, out_scores, out_ids, nullptr, stream);
   DevInfo di;
   TRY(device_info(di));
   if (di.device != ix->device) return fail(HIPER_ERR_INVALID_ARG, "index lives on device %d, current is %d", ix->device, di.device);
@@ -725,8 +897,9 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
   int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
   __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
   uint64_t* partial = (uint64_t*)(ws + w.partial);
+  uint32_t* progress = (uint32_t*)(ws + w.progress);
 
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  CUDA_TRY(cudaMemsetAsync(status, 0, w.qlens - w.status, stream));  // status + lockstep progress
   TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
 
@@ -748,6 +921,8 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
     a.q_lens = qlens_dev;
     a.d_lens = ix->lens;
     a.partial = partial;
+    a.progress = (kp.pair && getenv("HIPER_NO_LOCKSTEP") == nullptr) ? progress : nullptr;
+    a.window = kLockstepWindow;
     TRY(launch_maxsim(1, k, kp, tq, kp.pair ? ix->tmap_half : ix->tmap, a, stream));
   }
   // partial lists [P][kEpiGroups][n_q_pad][k]: n_lists = P * kEpiGroups, each [n_q_pad][k]
@@ -782,6 +957,7 @@ static void scores_ws_layout(int32_t n_q, int32_t dim, ScoresWs& w) {
 
 extern "C" size_t hiper_maxsim_scores_workspace_size(const hiper_index* ix, int32_t n_q) {
   if (!ix || n_q < 0) return 0;
+  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, 1, nullptr);
   ScoresWs w;
   scores_ws_layout(n_q, ix->dim, w);
   return w.total;
@@ -796,9 +972,13 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
   if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
-  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
+  const bool pooled = ix->ld_pad == 1;
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, pooled));
   if (n_q == 0 || ix->n == 0) return HIPER_OK;
   if (!out_scores) return fail(HIPER_ERR_INVALID_ARG, "out_scores is NULL");
+  if (pooled)
+    return pooled_search(ix, q_tokens, dtype, q_lens, n_q, dim, 1, flags, nullptr, workspace,
+                         workspace_bytes, nullptr, nullptr, out_scores, stream);
   DevInfo di;
   TRY(device_info(di));
   KernelPlan kp;

@@ -48,6 +48,8 @@ struct MaxsimArgs {
   float* scores;          // MODE 0: [n_q][score_ld]
   int64_t score_ld;
   uint64_t* partial;      // MODE 1: [P][4G][k]
+  uint32_t* progress;     // pair kernel: [n_pairs] progress words for L2 lockstep, or nullptr
+  int32_t window;         // chunks a pair may run ahead of the slowest pair (lockstep window)
 };
 
 // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare; warps 4-7 = epilogue warpgroup 0 (accumulator 0, even

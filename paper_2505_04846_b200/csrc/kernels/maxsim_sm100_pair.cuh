@@ -28,6 +28,30 @@ namespace hiper {
 // warps 0-7: epilogue groups 0/1; 8: TMEM allocator; 9: spare; 10: TMA producer; 11: MMA issuer
 constexpr uint32_t kPairAllocWarp = 8, kPairProducerWarp = 10, kPairMmaWarp = 11;
 
+// L2 lockstep.  All pairs of a wave stream the same corpus partition(s); left alone they drift
+// apart by more than the L2 can hold (measured: 5.6 TB of DRAM reads per launch for a 65.5 GB
+// corpus at Q = 1024).  Each leader publishes its position (unit iteration << 20 | chunk offset)
+// every 16 chunks and waits while it is more than `window` chunks ahead of the slowest pair, so the
+// chunks in flight across the GPU stay inside a few MB of L2.  Finished pairs publish ~0u.
+__device__ __forceinline__ void lockstep_publish(uint32_t* progress, uint32_t pair, uint32_t pos) {
+  *reinterpret_cast<volatile uint32_t*>(progress + pair) = pos;
+}
+__device__ __forceinline__ void lockstep_wait(const uint32_t* progress, uint32_t n_pairs, uint32_t pos,
+                                              uint32_t window) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t mn = 0xFFFFFFFFu;
+    for (uint32_t j = 0; j < n_pairs; ++j)
+      mn = min(mn, *reinterpret_cast<const volatile uint32_t*>(progress + j));
+    if ((uint64_t)pos <= (uint64_t)mn + window) return;
+    __nanosleep(200);
+    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) {
+      printf("hiper: lockstep watchdog pair %u pos 0x%x min 0x%x\n", 0u, pos, mn);
+      __trap();
+    }
+  }
+}
+
 template <int MODE, int KR, int DBG = 0>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
@@ -100,6 +124,12 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           tma_load_2d_pair(sA + ab * args.a_bytes + kb * 16384u, &tmap_q, afull_leader, kb * 64,
                            (int32_t)((2 * g + (int32_t)rank) * 128));
         for (int64_t c = c0; c < c1; ++c) {
+          if (args.progress != nullptr && rank == 0 && ((c - c0) & 15) == 0) {
+            const int64_t off = c - c0 < 0xFFFFF ? c - c0 : 0xFFFFF;
+            const uint32_t pos = (it << 20) | (uint32_t)off;
+            lockstep_publish(args.progress, pair, pos);
+            lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
+          }
           // one stage = this CTA's half of one whole chunk (all dim/64 K-blocks)
           mbar_wait(bar_empty(s), ph ^ 1u);
           if (DBG == 2 && (c > c0 || it > 0)) {
@@ -114,6 +144,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           if (++s == S) { s = 0; ph ^= 1u; }
         }
       }
+      if (args.progress != nullptr && rank == 0) lockstep_publish(args.progress, pair, 0xFFFFFFFFu);
     }
   } else if (warp == kPairMmaWarp) {
     // ================= MMA issuer: leader CTA, single thread =================

@@ -1,0 +1,221 @@
+// pooled_sm100_pair.cuh -- step a12: the pooled single-vector limit case (BASELINE.json configs[4]).
+//
+// With one token per query and per chunk (Lq = Ld = 1) MaxSim reduces to the dot of NORM'd vectors,
+// i.e. cosine similarity of pooled embeddings -- the paper's deployed retrieval ("cosine similarity
+// on the pooled embeddings"; "ranked according to the cosine similarity").
+// The work is then a plain dense GEMM S = Q C^T (K = dim, e.g. 768) with a fused per-query top-k:
+//  * a CTA pair (cta_group::2) computes 256 queries x 256 chunks per accumulator (M = 256, N = 256),
+//    K-pipelined: every stage holds one 64-dim K-block of this CTA's 128 query rows (A) and of its
+//    128 chunk rows (B), both TMA-loaded (OOB rows zero-filled: no padding in HBM);
+//  * two TMEM accumulators (2 x 256 columns) alternate between the two epilogue warpgroups;
+//  * epilogue thread = one query (its TMEM lane); it scans its 256 scores per tile with a float
+//    threshold test and keeps a register-resident sorted top-k (KP slots) of sortable keys, written
+//    to partial[p][group][q][k] at the end of the unit; topk_merge.cuh merges partitions / ranks.
+//  * MODE 0 writes the dense score matrix instead (test support).
+#pragma once
+#include "maxsim_sm100_pair.cuh"
+
+namespace hiper {
+
+struct PooledArgs {
+  int32_t n_q;        // real queries
+  int32_t n_qtiles;   // ceil(n_q / 256)
+  int32_t n_ctiles;   // ceil(n_chunks / 256)
+  int32_t n_parts;    // P (partitions of chunk tiles)
+  int32_t num_kb;     // dim / 64
+  int32_t k;          // top-k (MODE 1), k <= KP
+  int32_t n_stages;
+  uint32_t stage_bytes;  // per CTA: A 128x64 + B 128x64 bf16 = 32 KiB
+  int32_t q_pad;      // n_qtiles * 256 (partial row stride)
+  int64_t n_chunks;
+  int64_t id_base;
+  float* scores;      // MODE 0: [n_q][score_ld]
+  int64_t score_ld;
+  uint64_t* partial;  // MODE 1: [P][kEpiGroups][q_pad][k]
+};
+
+template <int MODE, int KP>
+__global__ void __launch_bounds__(kMaxsimThreads, 1)
+    pooled_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                             const __grid_constant__ CUtensorMap tmap_c, const PooledArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  using namespace ptx;
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pair = cluster_id_x();
+  const uint32_t n_pairs = nclusters_x();
+
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sStage = base;  // n_stages x {A 16 KiB | B 16 KiB}
+  const uint32_t sBar = sStage + args.n_stages * args.stage_bytes;
+  const int S = args.n_stages;
+  auto bar_full = [&](int s) { return sBar + 8u * s; };
+  auto bar_empty = [&](int s) { return sBar + 8u * (S + s); };
+  auto bar_tfull = [&](int b) { return sBar + 8u * (2 * S + b); };
+  auto bar_tempty = [&](int b) { return sBar + 8u * (2 * S + 2 + b); };
+  const uint32_t sTmemPtr = sBar + 8u * (2 * S + 4);
+  uint32_t* tmem_ptr_generic =
+      reinterpret_cast<uint32_t*>(smem_raw + (sTmemPtr - smem_u32(smem_raw)));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(bar_full(s), 1);
+      mbar_init(bar_empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar_tfull(b), 1);
+      mbar_init(bar_tempty(b), 8);
+    }
+    fence_mbarrier_init();
+  }
+  if (warp == kPairAllocWarp) {
+    tmem_alloc_pair(sTmemPtr, kTmemCols);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr_generic);
+
+  const int32_t n_units = args.n_qtiles * args.n_parts;
+  auto decode = [&](int32_t u, int32_t& qt, int32_t& p, int32_t& t0, int32_t& t1) {
+    p = u / args.n_qtiles;
+    qt = u - p * args.n_qtiles;
+    t0 = (int32_t)((int64_t)p * args.n_ctiles / args.n_parts);
+    t1 = (int32_t)((int64_t)(p + 1) * args.n_ctiles / args.n_parts);
+  };
+
+  if (warp == kPairProducerWarp) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap_q);
+      prefetch_tmap(&tmap_c);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
+        int32_t qt, p, t0, t1;
+        decode(u, qt, p, t0, t1);
+        for (int32_t ct = t0; ct < t1; ++ct) {
+          for (int kb = 0; kb < args.num_kb; ++kb) {
+            mbar_wait(bar_empty(s), ph ^ 1u);
+            if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
+            const uint32_t full_leader = mapa_shared(bar_full(s), 0);
+            const uint32_t st = sStage + s * args.stage_bytes;
+            tma_load_2d_pair(st, &tmap_q, full_leader, kb * 64, qt * 256 + (int32_t)rank * 128);
+            tma_load_2d_pair(st + 16384u, &tmap_c, full_leader, kb * 64, ct * 256 + (int32_t)rank * 128);
+            if (++s == S) { s = 0; ph ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == kPairMmaWarp) {
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(256, 256);
+      int s = 0;
+      uint32_t ph = 0, t = 0;
+      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
+        int32_t qt, p, t0, t1;
+        decode(u, qt, p, t0, t1);
+        for (int32_t ct = t0; ct < t1; ++ct, ++t) {
+          const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
+          mbar_wait(bar_tempty(acc), tph ^ 1u);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * kAccStride;
+          for (int kb = 0; kb < args.num_kb; ++kb) {
+            mbar_wait(bar_full(s), ph);
+            tc_fence_after();
+            const uint32_t st = sStage + s * args.stage_bytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss_pair(d_tmem, umma_desc_sw128(st + kk * 32),
+                               umma_desc_sw128(st + 16384u + kk * 32), idesc,
+                               (kb | kk) != 0 ? 1u : 0u);
+            mma_commit_pair_mc(bar_empty(s), 0x3);
+            if (++s == S) { s = 0; ph ^= 1u; }
+          }
+          mma_commit_pair_mc(bar_tfull(acc), 0x3);
+        }
+      }
+    }
+  } else if (warp < 8) {
+    const uint32_t qslot = warp & 3u;
+    const uint32_t grp = warp >> 2;
+    const uint32_t taddr_base = tmem_base + ((qslot * 32u) << 16) + grp * kAccStride;
+    const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), 0);
+    const int32_t k = args.k;
+    uint32_t t = 0, mine = 0;
+    for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
+      int32_t qt, p, t0, t1;
+      decode(u, qt, p, t0, t1);
+      const int32_t q = qt * 256 + (int32_t)rank * 128 + (int32_t)qslot * 32 + (int32_t)lane;
+      uint64_t v[KP];
+#pragma unroll
+      for (int j = 0; j < KP; ++j) v[j] = 0ull;
+      uint64_t thr = 0ull;  // key of rank k-1
+      const int32_t first = t0 + (int32_t)((grp - (t & 1u)) & 1u);
+      t += (uint32_t)(t1 - t0);
+      for (int32_t ct = first; ct < t1; ct += 2, ++mine) {
+        mbar_wait(bar_tfull(grp), mine & 1u);
+        tc_fence_after();
+        const int64_t cbase = (int64_t)ct * 256;
+        const int64_t left = args.n_chunks - cbase;
+        const int32_t ncols = left < 256 ? (int32_t)left : 256;
+        for (int32_t col = 0; col < ncols; col += 64) {
+          uint32_t r[64];
+          tmem_ld64_wait(taddr_base + (uint32_t)col, r);
+          if constexpr (MODE == 0) {
+            if (q < args.n_q) {
+              float* dst = args.scores + (int64_t)q * args.score_ld + cbase + col;
+#pragma unroll
+              for (int j = 0; j < 64; ++j)
+                if (col + j < ncols) dst[j] = __uint_as_float(r[j]) + 0.0f;
+            }
+          } else {
+            const uint32_t othr = (uint32_t)(thr >> 32);
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+              const float x = __uint_as_float(r[j]) + 0.0f;
+              const uint32_t ox = float_orderable(x);
+              if (ox >= othr && col + j < ncols) {
+                uint64_t key = ((uint64_t)ox << 32) | (uint64_t)(~(uint32_t)(args.id_base + cbase + col + j));
+                if (key > thr) {
+#pragma unroll
+                  for (int m = 0; m < KP; ++m) {
+                    const uint64_t hi = v[m] > key ? v[m] : key;
+                    key = v[m] > key ? key : v[m];
+                    v[m] = hi;
+                  }
+                  uint64_t nt = 0ull;
+#pragma unroll
+                  for (int m = 0; m < KP; ++m)
+                    if (m == k - 1) nt = v[m];
+                  thr = nt;
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader);
+      }
+      if constexpr (MODE == 1) {
+        if (q < args.n_q) {
+          uint64_t* dst = args.partial + (((int64_t)p * kEpiGroups + grp) * args.q_pad + q) * k;
+#pragma unroll
+          for (int m = 0; m < KP; ++m)
+            if (m < k) dst[m] = v[m];
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == kPairAllocWarp) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kTmemCols);
+  }
+}
+
+}  // namespace hiper
