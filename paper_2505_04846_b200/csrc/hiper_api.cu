@@ -738,7 +738,7 @@ static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks
   pp.n_ctiles = (int32_t)ct;
   const int pairs = di.num_sms / 2;
   pp.n_parts = choose_parts(pp.n_qtiles, pp.n_ctiles, pairs);
-  const uint32_t fixed = 1024u + 512u;
+  const uint32_t fixed = 1024u + 512u;  // align slack, barriers
   pp.n_stages = (int32_t)std::min<uint32_t>(8u, ((uint32_t)di.max_smem - fixed) / pp.stage_bytes);
   if (pp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory");
   pp.smem_bytes = fixed + pp.n_stages * pp.stage_bytes;
@@ -774,13 +774,16 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
 }
 
 struct PooledWs {
-  size_t status = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0, total = 0;
+  size_t status = 0, progress = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0,
+         total = 0;
 };
 static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t q_pad, int32_t k,
                              int32_t world, bool with_comm, PooledWs& w) {
   size_t off = 0;
   w.status = off;
   off += 256;
+  w.progress = off;
+  off += 1024;
   w.qlens = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
   w.qlayout = off;
@@ -814,7 +817,7 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
   __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
   uint64_t* partial = (uint64_t*)(ws + w.partial);
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  CUDA_TRY(cudaMemsetAsync(status, 0, w.qlens - w.status, stream));  // status + lockstep words
   TRY(stage_h2d(qlens_dev, q_lens, (size_t)n_q * 4, stream));
   TRY(launch_norm(q_tokens, dtype, n_q, 1, qlens_dev, n_q, 1, dim, flags, qlayout, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
@@ -833,6 +836,8 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   a.partial = partial;
   a.scores = dense_scores;
   a.score_ld = ix->n;
+  a.progress = getenv("HIPER_NO_LOCKSTEP") == nullptr ? (uint32_t*)(ws + w.progress) : nullptr;
+  a.window = 16;
   if (ix->n > 0) {
     alignas(64) CUtensorMap tq;
     TRY(make_tmap(&tq, qlayout, n_q, dim, 128));

@@ -32,7 +32,19 @@ struct PooledArgs {
   float* scores;      // MODE 0: [n_q][score_ld]
   int64_t score_ld;
   uint64_t* partial;  // MODE 1: [P][kEpiGroups][q_pad][k]
+  uint32_t* progress; // [n_pairs] L2 lockstep words (see maxsim_sm100_pair.cuh), or nullptr
+  int32_t window;     // chunk tiles a pair may run ahead of the slowest pair
 };
+
+// Per-thread register top-k: the epilogue thread of query q keeps KP sortable keys in registers.
+// Scanning a 64-column TMEM block is one float compare per column against the k-th score; the rare
+// hits are collected in a bit mask and inserted out of the unrolled loop (a local copy of the block
+// is made only then), so the insertion code exists once and the 64 scores stay in registers.
+__device__ __forceinline__ float pooled_thr_score(uint64_t thr) {
+  if (thr == 0ull) return -INFINITY;
+  const uint32_t o = (uint32_t)(thr >> 32);
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
 
 template <int MODE, int KP>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
@@ -91,11 +103,16 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       prefetch_tmap(&tmap_q);
       prefetch_tmap(&tmap_c);
       int s = 0;
-      uint32_t ph = 0;
-      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
+      uint32_t ph = 0, it = 0;
+      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
         int32_t qt, p, t0, t1;
         decode(u, qt, p, t0, t1);
         for (int32_t ct = t0; ct < t1; ++ct) {
+          if (args.progress != nullptr && rank == 0 && ((ct - t0) & 3) == 0) {
+            const uint32_t pos = (it << 20) | (uint32_t)(ct - t0);
+            lockstep_publish(args.progress, pair, pos);
+            lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
+          }
           for (int kb = 0; kb < args.num_kb; ++kb) {
             mbar_wait(bar_empty(s), ph ^ 1u);
             if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
@@ -107,6 +124,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           }
         }
       }
+      if (args.progress != nullptr && rank == 0) lockstep_publish(args.progress, pair, 0xFFFFFFFFu);
     }
   } else if (warp == kPairMmaWarp) {
     if (rank == 0 && lane == 0) {
@@ -150,8 +168,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       const int32_t q = qt * 256 + (int32_t)rank * 128 + (int32_t)qslot * 32 + (int32_t)lane;
       uint64_t v[KP];
 #pragma unroll
-      for (int j = 0; j < KP; ++j) v[j] = 0ull;
-      uint64_t thr = 0ull;  // key of rank k-1
+      for (int m = 0; m < KP; ++m) v[m] = 0ull;
+      uint64_t thr = 0ull;        // key of rank k-1 (0 while the list is not full)
+      float thr_f = -INFINITY;    // its score: candidates below it are rejected with one compare
       const int32_t first = t0 + (int32_t)((grp - (t & 1u)) & 1u);
       t += (uint32_t)(t1 - t0);
       for (int32_t ct = first; ct < t1; ct += 2, ++mine) {
@@ -171,13 +190,19 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                 if (col + j < ncols) dst[j] = __uint_as_float(r[j]) + 0.0f;
             }
           } else {
-            const uint32_t othr = (uint32_t)(thr >> 32);
+            const int32_t nj = ncols - col;  // >= 64 except in the corpus' last tile
+            uint64_t hits = 0ull;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-              const float x = __uint_as_float(r[j]) + 0.0f;
-              const uint32_t ox = float_orderable(x);
-              if (ox >= othr && col + j < ncols) {
-                uint64_t key = ((uint64_t)ox << 32) | (uint64_t)(~(uint32_t)(args.id_base + cbase + col + j));
+            for (int j = 0; j < 64; ++j)
+              hits |= (uint64_t)(__uint_as_float(r[j]) >= thr_f && j < nj) << j;
+            if (hits) {
+              float xs[64];  // rare path: a local copy so the hits can be indexed dynamically
+#pragma unroll
+              for (int j = 0; j < 64; ++j) xs[j] = __uint_as_float(r[j]) + 0.0f;
+              while (hits) {
+                const int j = __ffsll((long long)hits) - 1;
+                hits &= hits - 1;
+                uint64_t key = make_key(xs[j], args.id_base + cbase + col + j);
                 if (key > thr) {
 #pragma unroll
                   for (int m = 0; m < KP; ++m) {
@@ -190,6 +215,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                   for (int m = 0; m < KP; ++m)
                     if (m == k - 1) nt = v[m];
                   thr = nt;
+                  thr_f = pooled_thr_score(thr);
                 }
               }
             }
