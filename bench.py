@@ -341,7 +341,7 @@ def run_ours(a, rank, local_rank, world):
         "config": workload_config(a, world),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "maxsim_sm100_kernel (fused TMA + tcgen05.mma + masked max/sum + top-k)",
+                     "kernel": ("pooled_sm100_pair_kernel (fused TMA + tcgen05.mma cta_group::2 GEMM + per-query top-k)" if a.chunk_len == 1 else "maxsim_sm100_pair_kernel (fused TMA + tcgen05.mma cta_group::2 + masked max/sum + top-k)"),
                      "kernel_ms_per_launch": kern_avg_ms, "kernel_launches": kern_n,
                      "algorithmic_flops_per_launch": flops_launch,
                      "flops_per_pair": flops_per_pair(a), "peak_source": peak_src,

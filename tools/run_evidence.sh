@@ -1,13 +1,21 @@
-# Round evidence: plain bench, launch list, DRAM traffic of the bench's own fused-kernel launch,
-# and one ncu --set full capture (reduced corpus) of the fused kernel.
+# Round evidence: tests, plain benches, launch list, DRAM traffic of the bench's own fused-kernel launch,
+# and one ncu --set full capture of each fused kernel on a reduced corpus.
 set -x
 python __graft_entry__.py > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$? >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
-B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 python bench.py --workload config5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+timeout 900 python bench.py --workload config2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 600 $B > gpurun_out/plain_b.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1 && \
   timeout 1500 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum --replay-mode application --clock-control none -k regex:maxsim -s 1 -c 1 --csv --log-file gpurun_out/traffic.csv $B > gpurun_out/ncu_traffic.log 2>&1
 C="python bench.py --chunks 100000 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 300 $C > gpurun_out/plain_c.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:maxsim -s 1 -c 1 -o gpurun_out/prof_final $C > gpurun_out/ncu_full.log 2>&1
+P="python bench.py --workload config5 --chunks 360000 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 300 $P > gpurun_out/plain_p.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:pooled -s 1 -c 1 -o gpurun_out/prof_pooled $P > gpurun_out/ncu_pooled.log 2>&1
 echo done
