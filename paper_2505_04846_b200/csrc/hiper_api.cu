@@ -817,7 +817,8 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
   __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
   uint64_t* partial = (uint64_t*)(ws + w.partial);
-  CUDA_TRY(cudaMemsetAsync(status, 0, w.qlens - w.status, stream));  // status + lockstep words
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  CUDA_TRY(cudaMemsetAsync(ws + w.progress, 0xFF, w.qlens - w.progress, stream));  // "not started"
   TRY(stage_h2d(qlens_dev, q_lens, (size_t)n_q * 4, stream));
   TRY(launch_norm(q_tokens, dtype, n_q, 1, qlens_dev, n_q, 1, dim, flags, qlayout, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
@@ -904,7 +905,10 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
   uint64_t* partial = (uint64_t*)(ws + w.partial);
   uint32_t* progress = (uint32_t*)(ws + w.progress);
 
-  CUDA_TRY(cudaMemsetAsync(status, 0, w.qlens - w.status, stream));  // status + lockstep progress
+  // status = 0; lockstep words = ~0 ("not started": a pair that is not resident yet never holds the
+  // others back, so the lockstep cannot deadlock even if the grid is not fully co-resident)
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  CUDA_TRY(cudaMemsetAsync(progress, 0xFF, w.qlens - w.progress, stream));
   TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
 
