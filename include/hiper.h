@@ -171,6 +171,35 @@ HIPER_API hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const in
                                         void* workspace, size_t workspace_bytes,
                                         float* out_scores, float* out_loss, hiper_stream_t stream);
 
+/* ------------------------------------------------------------------ NEXT N2: the full ColTrast loss
+ * L = (L_LI + L_C) / 2 ("The total loss per iteration is L = (L_LI + L_C)/2").
+ *  L_LI: as hiper_coltrast_scores_loss over the local rank's b queries vs its b positives (token level,
+ *        diagonal positives, temperature tau_li; "We apply LI loss to the local rank only").
+ *  L_C:  InfoNCE over cos(pooled q_i, c_j) / tau_c (SimCSE form).  The candidates c_j
+ *        are the pooled positives of ALL ranks of `comm`, gathered with one ncclAllGather ("pooled
+ *        embeddings from all ranks are gathered, and loss is calculated with the local rank compared
+ *        to min(N, W) samples"): the local b positives first, then the other ranks in
+ *        (rank, position) order, truncated to m = min(n_max, W), W = world * b.
+ *        Query i's positive is candidate i.
+ *   q_tokens/d_tokens device [b][q_max_len|d_max_len][dim]; q_lens/d_lens HOST [b];
+ *   q_pooled/d_pooled device [b][dp] (any scale: NORM'd inside), dp % 64 == 0;
+ *   n_max >= b (else HIPER_ERR_INVALID_ARG, SPEC NTooSmall); comm may be NULL (W = b).
+ *   out_losses device float[3] = {L_LI, L_C, L}; out_scores_c device float [b][m] or NULL;
+ *   out_m HOST int32 (may be NULL) receives m.  Every rank of comm must call it (collective). */
+HIPER_API size_t hiper_coltrast_loss_workspace_size(int32_t b, int32_t d_max_len, int32_t dim,
+                                                    int32_t dp, int32_t n_max,
+                                                    const hiper_comm* comm);
+HIPER_API hiper_status hiper_coltrast_loss(const void* q_tokens, const int32_t* q_lens,
+                                           int32_t q_max_len, const void* d_tokens,
+                                           const int32_t* d_lens, int32_t d_max_len, int32_t dim,
+                                           const void* q_pooled, const void* d_pooled, int32_t dp,
+                                           int32_t b, hiper_dtype dtype, uint32_t flags,
+                                           int32_t n_max, float tau_li, float tau_c,
+                                           const hiper_comm* comm, void* workspace,
+                                           size_t workspace_bytes, float* out_losses,
+                                           float* out_scores_c, int32_t* out_m,
+                                           hiper_stream_t stream);
+
 /* Loss kernel alone over a given device score matrix S [n_q][n_d] (test support: isolates a11). */
 HIPER_API hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,
                                 const int32_t* pos_idx, float temperature, void* workspace,

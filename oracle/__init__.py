@@ -14,7 +14,10 @@ this module only marshals numpy arrays into it.  Each wrapper names the passage 
 * :func:`topk`           exact top-k, score desc then id asc, padded (-inf,-1) (§2.3,
                          SPEC.md:193-201)
 * :func:`infonce`        mean_i logsumexp_j(S_ij/tau) - S_{i,pos_i}/tau  ("L_LI is
-                         maxsim loss")
+                         maxsim loss"; also L_C's SimCSE form)
+* :func:`gather_candidates`  min(N, W) candidates, local positives first, then (rank, position)
+                         order -- plain list logic
+* :func:`coltrast_total` L = (L_LI + L_C) / 2 (PAPER.md:252)
 
 Parity status: every function above is pinned by ``tests/test_oracle_pins.py`` (no "parity
 unpinned" function).
@@ -149,6 +152,31 @@ def infonce(S: np.ndarray, pos=None, tau: float = 1.0) -> float:
     if (p < 0).any() or (p >= M).any():
         raise OracleError("positive", 0)
     return float(lib().oracle_infonce(_ptr(S), B, M, _ptr(p), float(tau)))
+
+
+def gather_candidates(batches, local_rank: int, N: int):
+    """PAPER.md:252 "loss is calculated with the local rank compared to min(N, W) samples, where N is
+    the maximum to consider and W is the total samples across all ranks"; SPEC.md:321-329 fill order:
+    the local rank's positives first, then the other ranks' rows in (rank, position) order."""
+    b = len(batches[local_rank])
+    W = sum(len(x) for x in batches)
+    if N < b:
+        raise OracleError("NTooSmall", N)
+    m = min(N, W)
+    out = list(batches[local_rank])
+    for r, batch in enumerate(batches):
+        if r == local_rank:
+            continue
+        for row in batch:
+            if len(out) == m:
+                return out
+            out.append(row)
+    return out[:m]
+
+
+def coltrast_total(l_li: float, l_c: float) -> float:
+    """PAPER.md:252: "The total loss per iteration is L = (L_LI + L_C) / 2"."""
+    return (l_li + l_c) / 2.0
 
 
 def max_threads() -> int:

@@ -45,7 +45,8 @@ EXPORTS = [
     "hiper_maxsim_topk_workspace_size", "hiper_maxsim_topk", "hiper_maxsim_scores_workspace_size",
     "hiper_maxsim_scores", "hiper_coltrast_workspace_size", "hiper_coltrast_scores_loss",
     "hiper_infonce_loss", "hiper_workspace_status", "hiper_last_launch_count",
-    "hiper_profile_enable", "hiper_profile_read",
+    "hiper_profile_enable", "hiper_profile_read", "hiper_coltrast_loss_workspace_size",
+    "hiper_coltrast_loss",
 ]
 
 
@@ -92,6 +93,9 @@ def lib():
         "hiper_infonce_loss": ([P, i32, i32, P, ctypes.c_float, P, sz, P, P], i32),
         "hiper_workspace_status": ([P, P], i32),
         "hiper_profile_enable": ([i32], None),
+        "hiper_coltrast_loss_workspace_size": ([i32, i32, i32, i32, i32, P], sz),
+        "hiper_coltrast_loss": ([P, P, i32, P, P, i32, i32, P, P, i32, i32, i32, u32, i32,
+                                 ctypes.c_float, ctypes.c_float, P, P, sz, P, P, P, P], i32),
         "hiper_profile_read": ([P, P], i32),
     }
     for name, (args, res) in sig.items():
@@ -378,3 +382,31 @@ def hiper_profile_read():
     ms, n = ctypes.c_double(), ctypes.c_int32()
     _check(lib().hiper_profile_read(ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+def hiper_coltrast_loss(q_tokens, q_lens, d_tokens, d_lens, q_pooled, d_pooled, *, n_max: int,
+                        tau_li: float = 1.0, tau_c: float = 0.05, comm: Comm | None = None,
+                        flags: int = 0, want_scores: bool = False, stream=None):
+    """NEXT N2: (losses float32[3] = [L_LI, L_C, L] on the device, S_C [b][m] or None, m).
+
+    Collective over `comm` (every rank calls it with its local batch)."""
+    torch = _torch()
+    b, q_max_len, dim = q_tokens.shape
+    _, d_max_len, _ = d_tokens.shape
+    dp = q_pooled.shape[-1]
+    ql, dl = _host_i32(q_lens), _host_i32(d_lens)
+    world = comm.world if comm else 1
+    m = min(n_max, world * b)
+    nb = lib().hiper_coltrast_loss_workspace_size(b, d_max_len, dim, dp, n_max,
+                                                  comm.handle if comm else None)
+    ws, wp, wn = _workspace(nb, q_tokens.device)
+    losses = torch.empty(3, dtype=torch.float32, device=q_tokens.device)
+    S = torch.empty((b, m), dtype=torch.float32, device=q_tokens.device) if want_scores else None
+    mo = ctypes.c_int32()
+    _check(lib().hiper_coltrast_loss(
+        _dev_ptr(q_tokens), _ptr(ql), q_max_len, _dev_ptr(d_tokens), _ptr(dl), d_max_len, dim,
+        _dev_ptr(q_pooled), _dev_ptr(d_pooled), dp, b, _dtype_code(q_tokens), flags, n_max,
+        float(tau_li), float(tau_c), comm.handle if comm else None, ctypes.c_void_p(wp), wn,
+        _dev_ptr(losses), _dev_ptr(S), ctypes.byref(mo), _stream_ptr(stream)))
+    losses._hiper_ws = ws
+    return losses, S, mo.value

@@ -1056,8 +1056,10 @@ extern "C" size_t hiper_coltrast_workspace_size(int32_t n_q, int32_t n_d, int32_
 
 static hiper_status launch_loss(const float* S, int32_t n_q, int32_t n_d, int64_t ld,
                                 const int32_t* pos_dev, float tau, float* out_loss,
-                                cudaStream_t stream) {
-  infonce_loss_kernel<<<1, 1024, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, out_loss);
+                                cudaStream_t stream, const float* combine_with = nullptr,
+                                float* out_combined = nullptr) {
+  infonce_loss_kernel<<<1, 1024, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, out_loss, combine_with,
+                                              out_combined);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return HIPER_OK;
@@ -1140,6 +1142,150 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
   a.score_ld = n_d;
   TRY(launch_maxsim(0, 1, kp, tq, td, a, stream));
   return launch_loss(S, n_q, n_d, n_d, pos_idx ? pos_dev : nullptr, temperature, out_loss, stream);
+}
+
+
+// ============================================================================ N2: full ColTrast loss
+// L = (L_LI + L_C) / 2:
+//   L_LI  in-batch MaxSim InfoNCE over the local rank's b x b token-level scores (a10-a11);
+//   L_C   InfoNCE (SimCSE form) over cos(pooled q_i, candidate_j) / tau_c, where the
+//         candidates are the pooled passages of ALL ranks gathered with one ncclAllGather, local
+//         positives first then the other ranks in (rank, position) order, truncated to
+//         m = min(N, W) ("compared to min(N, W) samples").
+// Pooled rows are NORM'd like token rows (cosine), scored by the pooled pair-GEMM kernel (MODE 0).
+static hiper_status pooled_dense_raw(const DevInfo& di, const __nv_bfloat16* qlayout, int32_t n_q,
+                                     const __nv_bfloat16* clayout, int64_t m, int32_t dim, float* S,
+                                     int64_t ld, cudaStream_t stream) {
+  PooledPlan pp;
+  TRY(plan_pooled(di, n_q, m, pp));
+  alignas(64) CUtensorMap tq, tc;
+  TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
+  TRY(make_tmap(&tc, clayout, m, dim, 128));
+  PooledArgs a{};
+  a.n_q = n_q;
+  a.n_qtiles = pp.n_qtiles;
+  a.n_ctiles = pp.n_ctiles;
+  a.n_parts = pp.n_parts;
+  a.num_kb = dim / 64;
+  a.k = 1;
+  a.n_stages = pp.n_stages;
+  a.stage_bytes = pp.stage_bytes;
+  a.q_pad = pp.q_pad;
+  a.n_chunks = m;
+  a.scores = S;
+  a.score_ld = ld;
+  return launch_pooled<0>(pp, tq, tc, a, stream);
+}
+
+struct FullLossWs {
+  size_t li = 0, ones = 0, qp = 0, dp = 0, gathered = 0, cand = 0, sc = 0, total = 0;
+  size_t li_bytes = 0;
+};
+static void full_loss_ws_layout(int32_t b, int32_t d_max_len, int32_t dim, int32_t dp, int32_t m,
+                                int32_t world, FullLossWs& w) {
+  ColtrastWs cw;
+  coltrast_ws_layout(b, b, d_max_len, dim, cw);
+  size_t off = 0;
+  w.li = off;
+  w.li_bytes = cw.total;
+  off = align_up(off + cw.total, 1024);
+  w.ones = off;
+  off = align_up(off + (size_t)std::max(b, 1) * 4, 1024);
+  w.qp = off;
+  off = align_up(off + (size_t)std::max(b, 1) * dp * 2, 1024);
+  w.dp = off;
+  off = align_up(off + (size_t)std::max(b, 1) * dp * 2, 1024);
+  w.gathered = off;
+  off = align_up(off + (size_t)world * std::max(b, 1) * dp * 2, 1024);
+  w.cand = off;
+  off = align_up(off + (size_t)std::max(m, 1) * dp * 2, 1024);
+  w.sc = off;
+  off = align_up(off + (size_t)std::max(b, 1) * std::max(m, 1) * 4, 1024);
+  w.total = off;
+}
+
+extern "C" size_t hiper_coltrast_loss_workspace_size(int32_t b, int32_t d_max_len, int32_t dim,
+                                                     int32_t dp, int32_t n_max,
+                                                     const hiper_comm* comm) {
+  if (b < 0 || dim <= 0 || dp <= 0) return 0;
+  const int32_t world = comm ? comm->world : 1;
+  const int32_t m = (int32_t)std::min<int64_t>(std::max(n_max, 0), (int64_t)world * b);
+  FullLossWs w;
+  full_loss_ws_layout(b, d_max_len, dim, dp, m, world, w);
+  return w.total;
+}
+
+extern "C" hiper_status hiper_coltrast_loss(
+    const void* q_tokens, const int32_t* q_lens, int32_t q_max_len, const void* d_tokens,
+    const int32_t* d_lens, int32_t d_max_len, int32_t dim, const void* q_pooled,
+    const void* d_pooled, int32_t dp, int32_t b, hiper_dtype dtype, uint32_t flags, int32_t n_max,
+    float tau_li, float tau_c, const hiper_comm* comm, void* workspace, size_t workspace_bytes,
+    float* out_losses, float* out_scores_c, int32_t* out_m, hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (b == 0) return fail(HIPER_ERR_EMPTY_BATCH, "empty batch");
+  if (b < 0) return fail(HIPER_ERR_INVALID_ARG, "b < 0");
+  if (n_max < b) return fail(HIPER_ERR_INVALID_ARG, "N (%d) < local batch (%d): positives must fit (SPEC NTooSmall)", n_max, b);
+  if (!(tau_c > 0.0f) || !std::isfinite(tau_c) || !(tau_li > 0.0f) || !std::isfinite(tau_li))
+    return fail(HIPER_ERR_BAD_TEMPERATURE, "temperatures must be > 0 and finite");
+  TRY(check_dims(dp, true));
+  if (!q_pooled || !d_pooled || !is_device_ptr(q_pooled) || !is_device_ptr(d_pooled) ||
+      ((uintptr_t)q_pooled & 15) || ((uintptr_t)d_pooled & 15))
+    return fail(HIPER_ERR_INVALID_ARG, "pooled inputs must be 16-B aligned device memory");
+  if (!out_losses) return fail(HIPER_ERR_INVALID_ARG, "out_losses is NULL");
+  const int32_t world = comm ? comm->world : 1;
+  const int32_t rank = comm ? comm->rank : 0;
+  const int32_t m = (int32_t)std::min<int64_t>(n_max, (int64_t)world * b);
+  FullLossWs w;
+  full_loss_ws_layout(b, d_max_len, dim, dp, m, world, w);
+  TRY(check_ws(workspace, workspace_bytes, w.total));
+  uint8_t* ws = (uint8_t*)workspace;
+  DevInfo di;
+  TRY(device_info(di));
+  // L_LI on the local rank (writes out_losses[0])
+  TRY(hiper_coltrast_scores_loss(q_tokens, q_lens, b, q_max_len, d_tokens, d_lens, b, d_max_len, dim,
+                                 dtype, flags, nullptr, tau_li, ws + w.li, w.li_bytes, nullptr,
+                                 out_losses, stream_));
+  int32_t launches = g_launches;
+  // pooled rows -> NORM'd bf16 (the length array is all ones: one row per item)
+  std::vector<int32_t> ones(b, 1);
+  int32_t* lens1 = (int32_t*)(ws + w.ones);
+  __nv_bfloat16* qp = (__nv_bfloat16*)(ws + w.qp);
+  __nv_bfloat16* dpp = (__nv_bfloat16*)(ws + w.dp);
+  __nv_bfloat16* gathered = (__nv_bfloat16*)(ws + w.gathered);
+  __nv_bfloat16* cand = (__nv_bfloat16*)(ws + w.cand);
+  float* Sc = out_scores_c ? out_scores_c : (float*)(ws + w.sc);
+  TRY(stage_h2d(lens1, ones.data(), (size_t)b * 4, stream));
+  uint32_t* status = (uint32_t*)(ws + w.li);  // the L_LI workspace's status word (same stream order)
+  g_launches = 0;
+  TRY(launch_norm(q_pooled, dtype, b, 1, lens1, b, 1, dp, flags, qp, status, stream));
+  TRY(launch_norm(d_pooled, dtype, b, 1, lens1, b, 1, dp, flags, dpp, status, stream));
+  launches += g_launches;
+  // gather: local positives first, then the other ranks in (rank, position) order, m rows
+  const size_t row_bytes = (size_t)dp * 2;
+  if (world > 1) {
+    NCCL_TRY(ncclAllGather(dpp, gathered, (size_t)b * dp, ncclBfloat16, comm->comm, stream));
+    CUDA_TRY(cudaMemcpyAsync(cand, gathered + (size_t)rank * b * dp, (size_t)b * row_bytes,
+                             cudaMemcpyDeviceToDevice, stream));
+    int64_t filled = b;
+    for (int32_t j = 0; j < world && filled < m; ++j) {
+      if (j == rank) continue;
+      const int64_t take = std::min<int64_t>(b, m - filled);
+      CUDA_TRY(cudaMemcpyAsync(cand + filled * dp, gathered + (size_t)j * b * dp, take * row_bytes,
+                               cudaMemcpyDeviceToDevice, stream));
+      filled += take;
+    }
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(cand, dpp, (size_t)b * row_bytes, cudaMemcpyDeviceToDevice, stream));
+  }
+  if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
+  // L_C scores [b][m] and loss (writes out_losses[1] and out_losses[2] = (L_LI + L_C) / 2)
+  g_launches = 0;
+  TRY(pooled_dense_raw(di, qp, b, cand, m, dp, Sc, m, stream));
+  TRY(launch_loss(Sc, b, m, m, nullptr, tau_c, out_losses + 1, stream, out_losses, out_losses + 2));
+  g_launches += launches;
+  if (out_m) *out_m = m;
+  return HIPER_OK;
 }
 
 extern "C" hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,

@@ -16,7 +16,9 @@ namespace hiper {
 __global__ void __launch_bounds__(1024) infonce_loss_kernel(const float* __restrict__ S, int32_t B,
                                                             int32_t M, int64_t ld,
                                                             const int32_t* __restrict__ pos,
-                                                            float tau, float* __restrict__ out_loss) {
+                                                            float tau, float* __restrict__ out_loss,
+                                                            const float* combine_with = nullptr,
+                                                            float* out_combined = nullptr) {
   __shared__ double warp_sum[32];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n_warps = blockDim.x >> 5;
@@ -42,7 +44,10 @@ __global__ void __launch_bounds__(1024) infonce_loss_kernel(const float* __restr
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (uint32_t w = 0; w < n_warps; ++w) s += warp_sum[w];
-    *out_loss = (float)(s / (double)B);
+    const float L = (float)(s / (double)B);
+    *out_loss = L;
+    // ColTrast total loss L = (L_LI + L_C) / 2, when the other term is given
+    if (out_combined) *out_combined = 0.5f * (*combine_with + L);
   }
 }
 

@@ -53,6 +53,35 @@ def main():
                 ok &= same_i and same_s
             del full, fidx
         del shard, idx
+    # ---- NEXT N2: full ColTrast loss with the gathered pooled candidates (min(N, W) rule)
+    import oracle
+    b, dp, Lc = 24, 768, 128
+    for n_max in (b * world, b + 5, b):
+        dt = gen.corpus(30 + rank, 0, b, Lc, d)
+        qt = gen.queries(40 + rank, b, Lq, d, corpus_seed=30 + rank, n_chunks=b, L=Lc, diagonal=True,
+                         sigma_q=gen.SIGMA_Q_HARD)
+        ones_q, ones_d = np.full(b, Lq, np.int32), np.full(b, Lc, np.int32)
+        pools = [gen.corpus(50 + r, 0, b, 1, dp)[:, 0] for r in range(world)]   # every rank's passages
+        qpool = gen.queries(60 + rank, b, 1, dp, corpus_seed=50 + rank, n_chunks=b, L=1,
+                            diagonal=True, sigma_q=np.float32(4.0))[:, 0]
+        to_dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda().view(torch.bfloat16)
+        losses, S, m = H.hiper_coltrast_loss(to_dev(qt), ones_q, to_dev(dt), ones_d, to_dev(qpool),
+                                             to_dev(pools[rank]), n_max=n_max, tau_li=1.0,
+                                             tau_c=0.05, comm=comm, want_scores=True)
+        got = losses.cpu().numpy().astype(np.float64)
+        cands = np.stack(oracle.gather_candidates([list(p) for p in pools], rank, n_max))
+        S_li = oracle.maxsim_matrix(oracle.norm_rows(qt), ones_q, oracle.norm_rows(dt), ones_d)
+        L_li = oracle.infonce(S_li, tau=1.0)
+        S_c = oracle.maxsim_matrix(oracle.norm_rows(qpool)[:, None], np.ones(b, np.int32),
+                                   oracle.norm_rows(cands)[:, None], np.ones(len(cands), np.int32))
+        L_c = oracle.infonce(S_c, tau=0.05)
+        exp = (L_li, L_c, oracle.coltrast_total(L_li, L_c))
+        good = m == len(cands) and all(abs(g - o) <= max(1e-4 * abs(o), 1e-7) for g, o in zip(got, exp))
+        print(f"rank{rank} N={n_max}: m={m} losses={got.tolist()} oracle={list(exp)} ok={good}", flush=True)
+        ok &= bool(good)
+    okt = torch.tensor([int(ok)], device="cuda")
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    ok = bool(okt.item())
     flag = torch.tensor([int(ok)], device="cuda")
     dist.broadcast(flag, 0)
     comm.close()

@@ -317,3 +317,25 @@ def test_infonce_errors():
         oracle.infonce(np.zeros((2, 3)), tau=0.0)
     with pytest.raises(oracle.OracleError):
         oracle.infonce(np.zeros((2, 3)), pos=[0, 3])
+
+
+# ----------------------------------------------------------------------------------- N2 gather / total
+def test_gather_candidates_spec_examples():
+    """SPEC.md:327-329 examples of the min(N, W) rule."""
+    ranks = [[(r, i) for i in range(12)] for r in range(4)]
+    assert len(oracle.gather_candidates(ranks, 0, 100)) == 48          # min(100, 48)
+    with pytest.raises(oracle.OracleError):
+        oracle.gather_candidates(ranks, 0, 10)                          # NTooSmall
+    c = oracle.gather_candidates(ranks, 0, 16)
+    assert c == ranks[0] + ranks[1][:4]                                 # 12 local + first 4 of rank 1
+    c = oracle.gather_candidates(ranks, 2, 30)
+    assert c == ranks[2] + ranks[0] + ranks[1][:6]                      # local first, then rank order
+    assert oracle.gather_candidates([[1, 2, 3]], 0, 5) == [1, 2, 3]     # one rank: the local batch
+
+
+def test_contrastive_and_total_spec_examples():
+    """SPEC.md:336-337 (uniform cosines -> ln m; single positive candidate -> 0) and SPEC.md:354
+    (L_C = 0.6, L_LI = 0.4 -> L = 0.5)."""
+    assert abs(oracle.infonce(np.full((5, 9), 0.3), pos=[0] * 5, tau=0.05) - math.log(9)) <= 1e-12
+    assert oracle.infonce(np.array([[0.7]]), tau=0.05) == 0.0
+    assert oracle.coltrast_total(0.4, 0.6) == 0.5
