@@ -18,6 +18,9 @@ this module only marshals numpy arrays into it.  Each wrapper names the passage 
 * :func:`gather_candidates`  min(N, W) candidates, local positives first, then (rank, position)
                          order -- plain list logic
 * :func:`coltrast_total` L = (L_LI + L_C) / 2 (PAPER.md:252)
+* :func:`li_loss_grad`   gradient of L_LI w.r.t. the raw token rows, chain rule through the argmax
+                         and the normalisation (NEXT N1; SPEC.md:357-365 grad_check pins it by
+                         central finite differences in float64)
 
 Parity status: every function above is pinned by ``tests/test_oracle_pins.py`` (no "parity
 unpinned" function).
@@ -66,6 +69,9 @@ def lib():
         _lib.oracle_topk.restype = None
         _lib.oracle_infonce.argtypes = [P, i32, i32, P, ctypes.c_double]
         _lib.oracle_infonce.restype = ctypes.c_double
+        _lib.oracle_maxsim_infonce_grad.argtypes = [P, P, i32, i32, P, P, i32, i32, i32, P,
+                                                    ctypes.c_double, i32, P, P, P, P]
+        _lib.oracle_maxsim_infonce_grad.restype = ctypes.c_double
         _lib.oracle_max_threads.argtypes = []
         _lib.oracle_max_threads.restype = i32
     return _lib
@@ -177,6 +183,28 @@ def gather_candidates(batches, local_rank: int, N: int):
 def coltrast_total(l_li: float, l_c: float) -> float:
     """PAPER.md:252: "The total loss per iteration is L = (L_LI + L_C) / 2"."""
     return (l_li + l_c) / 2.0
+
+
+def li_loss_grad(x_q, q_lens, x_d, d_lens, pos=None, tau: float = 1.0, exact_norm: bool = False):
+    """(loss, grad_q, grad_d, argmax, gap) for L_LI over raw rows x_q [B][Lq][d], x_d [M][Ld][d].
+
+    exact_norm=True normalises in float64 (differentiable; finite-difference pin); False uses the
+    library's NORM (bf16 operands, as the GPU) for the forward/argmax."""
+    xq = np.ascontiguousarray(x_q, dtype=np.float64)
+    xd = np.ascontiguousarray(x_d, dtype=np.float64)
+    B, Lq, d = xq.shape
+    M, Ld, _ = xd.shape
+    ql = np.ascontiguousarray(q_lens, dtype=np.int32)
+    dl = np.ascontiguousarray(d_lens, dtype=np.int32)
+    p = np.arange(B, dtype=np.int32) if pos is None else np.ascontiguousarray(pos, dtype=np.int32)
+    gq = np.zeros_like(xq)
+    gd = np.zeros_like(xd)
+    am = np.zeros((B, M, Lq), dtype=np.int32)
+    gap = np.zeros((B, M, Lq), dtype=np.float64)
+    loss = lib().oracle_maxsim_infonce_grad(_ptr(xq), _ptr(ql), B, Lq, _ptr(xd), _ptr(dl), M, Ld, d,
+                                            _ptr(p), float(tau), int(bool(exact_norm)), _ptr(gq),
+                                            _ptr(gd), _ptr(am), _ptr(gap))
+    return float(loss), gq, gd, am, gap
 
 
 def max_threads() -> int:

@@ -29,6 +29,9 @@
  *   oracle_infonce        L = mean_i [ logsumexp_j (S_ij / tau) - S_{i,pos_i} / tau ]  (PAPER.md:252
  *                         "L_LI is maxsim loss"; SPEC.md:339-347 [OP] li_loss; tau reading R9).
  *                         pinned: P7 closed forms, P8 torch cross_entropy float64.
+ *   oracle_maxsim_infonce_grad  NEXT N1: dL_LI/dx by the chain rule through argmax + normalisation
+ *                         (PAPER.md:247-252 training; SPEC.md:357-365 grad_check).
+ *                         pinned: central finite differences in float64 (<= 1e-4 relative).
  */
 #include <math.h>
 #include <stdint.h>
@@ -216,4 +219,129 @@ double oracle_infonce(const double* S, int32_t B, int32_t M, const int32_t* pos,
     total += lse - S[(int64_t)i * M + pos[i]] / tau;
   }
   return total / (double)B;
+}
+
+/* ---------------------------------------------------------------- NEXT N1: gradient of L_LI
+ * Backward of L = mean_i [logsumexp_j(S_ij/tau) - S_{i,pos_i}/tau], S_ij = MaxSim(Q_i, D_j), through
+ * the argmax of every max and through the row normalisation (chain rule; the paper gives no formula:
+ * the ColTrast objective is trained by backpropagation; SPEC.md:357-365 grad_check):
+ *   G_ij            = (softmax_j(S_i/tau)_j - [j == pos_i]) / (B * tau)
+ *   a(i,t,j)        = argmax_{u < len_j} <qn_{i,t}, dn_{j,u}>        (lowest u on exact ties)
+ *   dL/dqn_{i,t}    = sum_j G_ij dn_{j,a(i,t,j)}
+ *   dL/ddn_{j,u}    = sum_i sum_{t : a(i,t,j) = u} G_ij qn_{i,t}
+ *   dL/dx (row)     = (g - yn (yn . g)) / ||x||      with yn = x / ||x||
+ * x_q: [B][q_stride][d] float64 raw query rows, x_d: [M][d_stride][d] raw doc rows (only real rows used).
+ * exact_norm = 1: qn/dn = x/||x|| in float64 (differentiable: the finite-difference pin);
+ * exact_norm = 0: qn/dn = the library's NORM (bf16 rounded; the GPU's operands) -- the argmax and the
+ *                 dot products use those values, the Jacobian uses yn = x/||x|| in float64.
+ * Outputs: loss (return value), grad_q/grad_d same shapes as x_q/x_d (padding rows 0),
+ * amax_out (may be NULL): [B][M][q_stride] int32 argmax indices, gap_out (may be NULL): the gap
+ * between the best and second-best dot for each (i, t, j) (near-ties decide argmax ambiguously).
+ */
+static double o_dot(const double* a, const double* b, int32_t d) {
+  double s = 0.0;
+  for (int32_t k = 0; k < d; ++k) s += a[k] * b[k];
+  return s;
+}
+
+static void o_prepare_rows(const double* x, int64_t n_items, int32_t stride, const int32_t* lens,
+                           int32_t d, int32_t exact_norm, double* out) {
+  for (int64_t i = 0; i < n_items; ++i)
+    for (int32_t r = 0; r < stride; ++r) {
+      const double* row = x + (i * stride + r) * d;
+      double* o = out + (i * stride + r) * d;
+      if (r >= lens[i]) {
+        for (int32_t k = 0; k < d; ++k) o[k] = 0.0;
+        continue;
+      }
+      if (exact_norm) {
+        double n = sqrt(o_dot(row, row, d));
+        for (int32_t k = 0; k < d; ++k) o[k] = row[k] / n;
+      } else {
+        float f[4096];
+        uint16_t y[4096];
+        for (int32_t k = 0; k < d; ++k) f[k] = (float)row[k];
+        oracle_norm_rows(f, 0, 1, d, 0, y, NULL);
+        for (int32_t k = 0; k < d; ++k) o[k] = (double)o_bf16_to_f32(y[k]);
+      }
+    }
+}
+
+double oracle_maxsim_infonce_grad(const double* x_q, const int32_t* q_lens, int32_t B, int32_t q_stride,
+                                  const double* x_d, const int32_t* d_lens, int32_t M, int32_t d_stride,
+                                  int32_t d, const int32_t* pos, double tau, int32_t exact_norm,
+                                  double* grad_q, double* grad_d, int32_t* amax_out, double* gap_out) {
+  double* qn = (double*)malloc(sizeof(double) * (size_t)B * q_stride * d);
+  double* dn = (double*)malloc(sizeof(double) * (size_t)M * d_stride * d);
+  double* S = (double*)malloc(sizeof(double) * (size_t)B * M);
+  int32_t* a = (int32_t*)calloc((size_t)B * M * q_stride, sizeof(int32_t));
+  double* gq = (double*)calloc((size_t)B * q_stride * d, sizeof(double));
+  double* gd = (double*)calloc((size_t)M * d_stride * d, sizeof(double));
+  o_prepare_rows(x_q, B, q_stride, q_lens, d, exact_norm, qn);
+  o_prepare_rows(x_d, M, d_stride, d_lens, d, exact_norm, dn);
+  /* forward: S and the argmax of every max */
+  for (int32_t i = 0; i < B; ++i)
+    for (int32_t j = 0; j < M; ++j) {
+      double s = 0.0;
+      for (int32_t t = 0; t < q_lens[i]; ++t) {
+        double best = -INFINITY, second = -INFINITY;
+        int32_t arg = 0;
+        for (int32_t u = 0; u < d_lens[j]; ++u) {
+          double v = o_dot(qn + ((int64_t)i * q_stride + t) * d, dn + ((int64_t)j * d_stride + u) * d, d);
+          if (v > best) { second = best; best = v; arg = u; }
+          else if (v > second) second = v;
+        }
+        s += best;
+        a[((int64_t)i * M + j) * q_stride + t] = arg;
+        if (gap_out) gap_out[((int64_t)i * M + j) * q_stride + t] = best - second;
+      }
+      S[(int64_t)i * M + j] = s;
+    }
+  double loss = oracle_infonce(S, B, M, pos, tau);
+  /* G = dL/dS */
+  for (int32_t i = 0; i < B; ++i) {
+    double mx = -INFINITY, sum = 0.0;
+    for (int32_t j = 0; j < M; ++j) mx = fmax(mx, S[(int64_t)i * M + j] / tau);
+    for (int32_t j = 0; j < M; ++j) sum += exp(S[(int64_t)i * M + j] / tau - mx);
+    for (int32_t j = 0; j < M; ++j) {
+      double G = (exp(S[(int64_t)i * M + j] / tau - mx) / sum - (j == pos[i] ? 1.0 : 0.0)) / (B * tau);
+      for (int32_t t = 0; t < q_lens[i]; ++t) {
+        int32_t u = a[((int64_t)i * M + j) * q_stride + t];
+        double* g1 = gq + ((int64_t)i * q_stride + t) * d;
+        double* g2 = gd + ((int64_t)j * d_stride + u) * d;
+        const double* qv = qn + ((int64_t)i * q_stride + t) * d;
+        const double* dv = dn + ((int64_t)j * d_stride + u) * d;
+        for (int32_t k = 0; k < d; ++k) {
+          g1[k] += G * dv[k];
+          g2[k] += G * qv[k];
+        }
+      }
+    }
+  }
+  /* through the normalisation: dx = (g - y (y.g)) / ||x|| */
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* x = pass ? x_d : x_q;
+    const int32_t* lens = pass ? d_lens : q_lens;
+    int64_t n = pass ? M : B;
+    int32_t stride = pass ? d_stride : q_stride;
+    double* g = pass ? gd : gq;
+    double* out = pass ? grad_d : grad_q;
+    for (int64_t i = 0; i < n; ++i)
+      for (int32_t r = 0; r < stride; ++r) {
+        const double* row = x + (i * stride + r) * d;
+        double* gr = g + (i * stride + r) * d;
+        double* o = out + (i * stride + r) * d;
+        if (r >= lens[i]) {
+          for (int32_t k = 0; k < d; ++k) o[k] = 0.0;
+          continue;
+        }
+        double nrm = sqrt(o_dot(row, row, d));
+        double yg = 0.0;
+        for (int32_t k = 0; k < d; ++k) yg += row[k] / nrm * gr[k];
+        for (int32_t k = 0; k < d; ++k) o[k] = (gr[k] - row[k] / nrm * yg) / nrm;
+      }
+  }
+  if (amax_out) memcpy(amax_out, a, sizeof(int32_t) * (size_t)B * M * q_stride);
+  free(qn); free(dn); free(S); free(a); free(gq); free(gd);
+  return loss;
 }

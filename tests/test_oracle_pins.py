@@ -339,3 +339,51 @@ def test_contrastive_and_total_spec_examples():
     assert abs(oracle.infonce(np.full((5, 9), 0.3), pos=[0] * 5, tau=0.05) - math.log(9)) <= 1e-12
     assert oracle.infonce(np.array([[0.7]]), tau=0.05) == 0.0
     assert oracle.coltrast_total(0.4, 0.6) == 0.5
+
+
+# ----------------------------------------------------------------------------------- N1 gradient
+def _li_loss_exact(xq, ql, xd, dl, tau):
+    return oracle.li_loss_grad(xq, ql, xd, dl, tau=tau, exact_norm=True)[0]
+
+
+@pytest.mark.parametrize("tau", [1.0, 0.3])
+def test_li_grad_central_finite_differences(tau):
+    """SPEC.md:357-365 grad_check: analytic gradient (chain rule through argmax and normalisation)
+    vs central finite differences in float64, max relative error <= 1e-4."""
+    rng = np.random.default_rng(31)
+    B, Lq, M, Ld, d = 3, 4, 3, 5, 6
+    xq = rng.standard_normal((B, Lq, d))
+    xd = rng.standard_normal((M, Ld, d))
+    ql = np.array([4, 2, 3], np.int32)
+    dl = np.array([5, 1, 3], np.int32)
+    L, gq, gd, _, gap = oracle.li_loss_grad(xq, ql, xd, dl, tau=tau, exact_norm=True)
+    assert gap[gap > 0].min() > 1e-3  # no near-ties: the max is differentiable here
+    eps = 1e-6
+    for x, g, lens in ((xq, gq, ql), (xd, gd, dl)):
+        for idx in np.ndindex(*x.shape):
+            if idx[1] >= lens[idx[0]]:
+                assert g[idx] == 0.0
+                continue
+            x[idx] += eps
+            lp = _li_loss_exact(xq, ql, xd, dl, tau)
+            x[idx] -= 2 * eps
+            lm = _li_loss_exact(xq, ql, xd, dl, tau)
+            x[idx] += eps
+            fd = (lp - lm) / (2 * eps)
+            assert abs(fd - g[idx]) / max(1e-8, abs(fd) + abs(g[idx])) <= 1e-4 or abs(fd - g[idx]) < 1e-9, idx
+
+
+def test_li_grad_matches_loss_and_structure():
+    """The oracle's loss equals infonce(maxsim_matrix) on the same NORM'd operands; gradients sum
+    structure: sum over docs of dL/dS is 0 per row (softmax - onehot), so with B = 1 and one doc the
+    gradient vanishes."""
+    rng = np.random.default_rng(32)
+    xq = rng.standard_normal((4, 8, 64)).astype(np.float32)
+    xd = rng.standard_normal((5, 16, 64)).astype(np.float32)
+    ql, dl = np.array([8, 3, 1, 5], np.int32), np.array([16, 2, 9, 1, 7], np.int32)
+    L, gq, gd, am, _ = oracle.li_loss_grad(xq, ql, xd, dl, pos=[0, 1, 2, 3], tau=0.5)
+    S = oracle.maxsim_matrix(oracle.norm_rows(xq), ql, oracle.norm_rows(xd), dl)
+    assert abs(L - oracle.infonce(S, pos=[0, 1, 2, 3], tau=0.5)) <= 1e-12
+    assert (am < dl[None, :, None]).all()
+    L1, g1, g2, _, _ = oracle.li_loss_grad(xq[:1], ql[:1], xd[:1], dl[:1])
+    assert L1 == 0.0 and np.abs(g1).max() == 0.0 and np.abs(g2).max() == 0.0
