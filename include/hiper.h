@@ -200,6 +200,24 @@ HIPER_API hiper_status hiper_coltrast_loss(const void* q_tokens, const int32_t* 
                                            float* out_scores_c, int32_t* out_m,
                                            hiper_stream_t stream);
 
+/* ------------------------------------------------------------------ NEXT N1: backward of L_LI
+ * Forward exactly as hiper_coltrast_scores_loss (the fused kernel additionally records the argmax
+ * doc token of every max), then the gradient of L_LI with respect to the RAW token inputs:
+ *   G_ij = (softmax_j(S_i/tau)_j - [j == pos_i]) / (n_q tau);  a(i,t,j) = argmax_u <qn_it, dn_ju>
+ *   (lowest u on exact ties);  g_q(i,t) = sum_j G_ij dn_{j,a};  g_d(j,u) = sum_{i,t: a=u} G_ij qn_it;
+ *   grad_x = (g - y (y.g)) / ||x||, y = x/||x||  (NORM's Jacobian; identity with ASSUME_NORMALIZED).
+ * (Training the ColTrast objective by backpropagation.)
+ *   grad_q device float [n_q][q_max_len][dim], grad_d device float [n_d][d_max_len][dim]; padding
+ *   rows are 0.  Requires the CTA-pair kernel (the default).  dim in {64, 128}. */
+HIPER_API size_t hiper_coltrast_grad_workspace_size(int32_t n_q, int32_t n_d, int32_t d_max_len,
+                                                    int32_t dim);
+HIPER_API hiper_status hiper_coltrast_scores_loss_grad(
+    const void* q_tokens, const int32_t* q_lens, int32_t n_q, int32_t q_max_len,
+    const void* d_tokens, const int32_t* d_lens, int32_t n_d, int32_t d_max_len, int32_t dim,
+    hiper_dtype dtype, uint32_t flags, const int32_t* pos_idx, float temperature, void* workspace,
+    size_t workspace_bytes, float* out_scores, float* out_loss, float* grad_q, float* grad_d,
+    hiper_stream_t stream);
+
 /* Loss kernel alone over a given device score matrix S [n_q][n_d] (test support: isolates a11). */
 HIPER_API hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,
                                 const int32_t* pos_idx, float temperature, void* workspace,

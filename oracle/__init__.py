@@ -70,7 +70,7 @@ def lib():
         _lib.oracle_infonce.argtypes = [P, i32, i32, P, ctypes.c_double]
         _lib.oracle_infonce.restype = ctypes.c_double
         _lib.oracle_maxsim_infonce_grad.argtypes = [P, P, i32, i32, P, P, i32, i32, i32, P,
-                                                    ctypes.c_double, i32, P, P, P, P]
+                                                    ctypes.c_double, i32, P, P, P, P, P]
         _lib.oracle_maxsim_infonce_grad.restype = ctypes.c_double
         _lib.oracle_max_threads.argtypes = []
         _lib.oracle_max_threads.restype = i32
@@ -186,7 +186,8 @@ def coltrast_total(l_li: float, l_c: float) -> float:
 
 
 def li_loss_grad(x_q, q_lens, x_d, d_lens, pos=None, tau: float = 1.0, exact_norm: bool = False):
-    """(loss, grad_q, grad_d, argmax, gap) for L_LI over raw rows x_q [B][Lq][d], x_d [M][Ld][d].
+    """(loss, grad_q, grad_d, argmax, gap, second_argmax) for L_LI over raw rows x_q [B][Lq][d],
+    x_d [M][Ld][d].
 
     exact_norm=True normalises in float64 (differentiable; finite-difference pin); False uses the
     library's NORM (bf16 operands, as the GPU) for the forward/argmax."""
@@ -201,10 +202,11 @@ def li_loss_grad(x_q, q_lens, x_d, d_lens, pos=None, tau: float = 1.0, exact_nor
     gd = np.zeros_like(xd)
     am = np.zeros((B, M, Lq), dtype=np.int32)
     gap = np.zeros((B, M, Lq), dtype=np.float64)
+    am2 = np.zeros((B, M, Lq), dtype=np.int32)
     loss = lib().oracle_maxsim_infonce_grad(_ptr(xq), _ptr(ql), B, Lq, _ptr(xd), _ptr(dl), M, Ld, d,
                                             _ptr(p), float(tau), int(bool(exact_norm)), _ptr(gq),
-                                            _ptr(gd), _ptr(am), _ptr(gap))
-    return float(loss), gq, gd, am, gap
+                                            _ptr(gd), _ptr(am), _ptr(gap), _ptr(am2))
+    return float(loss), gq, gd, am, gap, am2
 
 
 def max_threads() -> int:

@@ -236,7 +236,8 @@ double oracle_infonce(const double* S, int32_t B, int32_t M, const int32_t* pos,
  *                 dot products use those values, the Jacobian uses yn = x/||x|| in float64.
  * Outputs: loss (return value), grad_q/grad_d same shapes as x_q/x_d (padding rows 0),
  * amax_out (may be NULL): [B][M][q_stride] int32 argmax indices, gap_out (may be NULL): the gap
- * between the best and second-best dot for each (i, t, j) (near-ties decide argmax ambiguously).
+ * between the best and second-best dot for each (i, t, j) (near-ties decide argmax ambiguously),
+ * amax2_out (may be NULL): the second-best index.
  */
 static double o_dot(const double* a, const double* b, int32_t d) {
   double s = 0.0;
@@ -270,7 +271,8 @@ static void o_prepare_rows(const double* x, int64_t n_items, int32_t stride, con
 double oracle_maxsim_infonce_grad(const double* x_q, const int32_t* q_lens, int32_t B, int32_t q_stride,
                                   const double* x_d, const int32_t* d_lens, int32_t M, int32_t d_stride,
                                   int32_t d, const int32_t* pos, double tau, int32_t exact_norm,
-                                  double* grad_q, double* grad_d, int32_t* amax_out, double* gap_out) {
+                                  double* grad_q, double* grad_d, int32_t* amax_out, double* gap_out,
+                                  int32_t* amax2_out) {
   double* qn = (double*)malloc(sizeof(double) * (size_t)B * q_stride * d);
   double* dn = (double*)malloc(sizeof(double) * (size_t)M * d_stride * d);
   double* S = (double*)malloc(sizeof(double) * (size_t)B * M);
@@ -285,12 +287,13 @@ double oracle_maxsim_infonce_grad(const double* x_q, const int32_t* q_lens, int3
       double s = 0.0;
       for (int32_t t = 0; t < q_lens[i]; ++t) {
         double best = -INFINITY, second = -INFINITY;
-        int32_t arg = 0;
+        int32_t arg = 0, arg2 = 0;
         for (int32_t u = 0; u < d_lens[j]; ++u) {
           double v = o_dot(qn + ((int64_t)i * q_stride + t) * d, dn + ((int64_t)j * d_stride + u) * d, d);
-          if (v > best) { second = best; best = v; arg = u; }
-          else if (v > second) second = v;
+          if (v > best) { second = best; arg2 = arg; best = v; arg = u; }
+          else if (v > second) { second = v; arg2 = u; }
         }
+        if (amax2_out) amax2_out[((int64_t)i * M + j) * q_stride + t] = arg2;
         s += best;
         a[((int64_t)i * M + j) * q_stride + t] = arg;
         if (gap_out) gap_out[((int64_t)i * M + j) * q_stride + t] = best - second;

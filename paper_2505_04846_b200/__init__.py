@@ -46,7 +46,7 @@ EXPORTS = [
     "hiper_maxsim_scores", "hiper_coltrast_workspace_size", "hiper_coltrast_scores_loss",
     "hiper_infonce_loss", "hiper_workspace_status", "hiper_last_launch_count",
     "hiper_profile_enable", "hiper_profile_read", "hiper_coltrast_loss_workspace_size",
-    "hiper_coltrast_loss",
+    "hiper_coltrast_loss", "hiper_coltrast_grad_workspace_size", "hiper_coltrast_scores_loss_grad",
 ]
 
 
@@ -94,6 +94,9 @@ def lib():
         "hiper_workspace_status": ([P, P], i32),
         "hiper_profile_enable": ([i32], None),
         "hiper_coltrast_loss_workspace_size": ([i32, i32, i32, i32, i32, P], sz),
+        "hiper_coltrast_grad_workspace_size": ([i32, i32, i32, i32], sz),
+        "hiper_coltrast_scores_loss_grad": ([P, P, i32, i32, P, P, i32, i32, i32, i32, u32, P,
+                                             ctypes.c_float, P, sz, P, P, P, P, P], i32),
         "hiper_coltrast_loss": ([P, P, i32, P, P, i32, i32, P, P, i32, i32, i32, u32, i32,
                                  ctypes.c_float, ctypes.c_float, P, P, sz, P, P, P, P], i32),
         "hiper_profile_read": ([P, P], i32),
@@ -410,3 +413,27 @@ def hiper_coltrast_loss(q_tokens, q_lens, d_tokens, d_lens, q_pooled, d_pooled, 
         _dev_ptr(losses), _dev_ptr(S), ctypes.byref(mo), _stream_ptr(stream)))
     losses._hiper_ws = ws
     return losses, S, mo.value
+
+
+def hiper_coltrast_scores_loss_grad(q_tokens, q_lens, d_tokens, d_lens, *, pos_idx=None,
+                                    temperature: float = 1.0, flags: int = 0, stream=None):
+    """NEXT N1: (S [n_q][n_d], loss [1], grad_q like q_tokens (fp32), grad_d like d_tokens (fp32))."""
+    torch = _torch()
+    n_q, q_max_len, dim = q_tokens.shape
+    n_d, d_max_len, _ = d_tokens.shape
+    ql, dl = _host_i32(q_lens), _host_i32(d_lens)
+    pos = None if pos_idx is None else _host_i32(pos_idx)
+    nb = lib().hiper_coltrast_grad_workspace_size(n_q, n_d, d_max_len, dim)
+    ws, wp, wn = _workspace(nb, q_tokens.device)
+    dev = q_tokens.device
+    S = torch.empty((n_q, n_d), dtype=torch.float32, device=dev)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    gq = torch.empty((n_q, q_max_len, dim), dtype=torch.float32, device=dev)
+    gd = torch.empty((n_d, d_max_len, dim), dtype=torch.float32, device=dev)
+    _check(lib().hiper_coltrast_scores_loss_grad(
+        _dev_ptr(q_tokens), _ptr(ql), n_q, q_max_len, _dev_ptr(d_tokens), _ptr(dl), n_d, d_max_len,
+        dim, _dtype_code(q_tokens), flags, _ptr(pos) if pos is not None else None,
+        float(temperature), ctypes.c_void_p(wp), wn, _dev_ptr(S), _dev_ptr(loss), _dev_ptr(gq),
+        _dev_ptr(gd), _stream_ptr(stream)))
+    loss._hiper_ws = ws
+    return S, loss, gq, gd

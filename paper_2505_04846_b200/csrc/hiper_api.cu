@@ -16,12 +16,14 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
 #include "../../include/hiper.h"
 #include "kernels/infonce.cuh"
 #include "kernels/maxsim_sm100.cuh"
+#include "kernels/maxsim_backward.cuh"
 #include "kernels/maxsim_sm100_pair.cuh"
 #include "kernels/pooled_sm100_pair.cuh"
 #include "kernels/norm_layout.cuh"
@@ -580,6 +582,10 @@ static hiper_status launch_maxsim(int mode, int k, const KernelPlan& kp, const C
                                   const CUtensorMap& td, const MaxsimArgs& a, cudaStream_t stream) {
   if (kp.grid == 0) return HIPER_OK;
   if (mode == 0) return launch_maxsim_t<0, 1>(kp, tq, td, a, stream);
+  if (mode == 2) {
+    if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "argmax capture needs the CTA-pair kernel");
+    return launch_maxsim_t<2, 1>(kp, tq, td, a, stream);
+  }
   if (k <= 32) return launch_maxsim_t<1, 1>(kp, tq, td, a, stream);
   if (k <= 64) return launch_maxsim_t<1, 2>(kp, tq, td, a, stream);
   return launch_maxsim_t<1, 4>(kp, tq, td, a, stream);
@@ -1286,6 +1292,127 @@ extern "C" hiper_status hiper_coltrast_loss(
   g_launches += launches;
   if (out_m) *out_m = m;
   return HIPER_OK;
+}
+
+
+// ============================================================================ N1: L_LI backward
+struct GradWs {
+  size_t base = 0, amax = 0, G = 0, total = 0;
+  ColtrastWs cw;
+};
+static void grad_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim, GradWs& w) {
+  coltrast_ws_layout(n_q, n_d, d_max_len, dim, w.cw);
+  size_t off = align_up(w.cw.total, 1024);
+  w.amax = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * std::max(n_d, 1) * 32, 1024);
+  w.G = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * std::max(n_d, 1) * 4, 1024);
+  w.total = off;
+}
+
+extern "C" size_t hiper_coltrast_grad_workspace_size(int32_t n_q, int32_t n_d, int32_t d_max_len,
+                                                     int32_t dim) {
+  if (n_q < 0 || n_d < 0 || dim <= 0) return 0;
+  GradWs w;
+  grad_ws_layout(n_q, n_d, d_max_len, dim, w);
+  return w.total;
+}
+
+extern "C" hiper_status hiper_coltrast_scores_loss_grad(
+    const void* q_tokens, const int32_t* q_lens, int32_t n_q, int32_t q_max_len, const void* d_tokens,
+    const int32_t* d_lens, int32_t n_d, int32_t d_max_len, int32_t dim, hiper_dtype dtype,
+    uint32_t flags, const int32_t* pos_idx, float temperature, void* workspace,
+    size_t workspace_bytes, float* out_scores, float* out_loss, float* grad_q, float* grad_d,
+    hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
+  if (d_max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "d_max_len must be >= 1");
+  if (d_max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "d_max_len %d > 256", d_max_len);
+  TRY(check_lens(d_lens, n_d, d_max_len, "doc"));
+  if (!d_tokens || !is_device_ptr(d_tokens) || ((uintptr_t)d_tokens & 15))
+    return fail(HIPER_ERR_INVALID_ARG, "d_tokens must be 16-B aligned device memory");
+  if (!out_loss || !grad_q || !grad_d) return fail(HIPER_ERR_INVALID_ARG, "outputs are NULL");
+  DevInfo di;
+  TRY(device_info(di));
+  const int32_t ld_pad = (int32_t)round_up(d_max_len, 16);
+  KernelPlan kp;
+  TRY(plan_kernel(di, n_q, n_d, ld_pad, dim, kp));
+  if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "the backward pass needs the CTA-pair kernel");
+  GradWs w;
+  grad_ws_layout(n_q, n_d, d_max_len, dim, w);
+  TRY(check_ws(workspace, workspace_bytes, w.total));
+  uint8_t* ws = (uint8_t*)workspace;
+  const ColtrastWs& c = w.cw;
+  uint32_t* status = (uint32_t*)(ws + c.status);
+  int32_t* qlens_dev = (int32_t*)(ws + c.qlens);
+  int32_t* dlens_dev = (int32_t*)(ws + c.dlens);
+  int32_t* pos_dev = (int32_t*)(ws + c.pos);
+  __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + c.qlayout);
+  __nv_bfloat16* dlayout = (__nv_bfloat16*)(ws + c.dlayout);
+  float* S = out_scores ? out_scores : (float*)(ws + c.scores);
+  uint8_t* amax = ws + w.amax;
+  float* G = (float*)(ws + w.G);
+
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
+  TRY(stage_h2d(dlens_dev, d_lens, (size_t)n_d * 4, stream));
+  TRY(launch_norm(d_tokens, dtype, n_d, d_max_len, dlens_dev, n_d, ld_pad, dim, flags, dlayout, status, stream));
+  if (pos_idx) TRY(stage_h2d(pos_dev, pos_idx, (size_t)n_q * 4, stream));
+  if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
+  alignas(64) CUtensorMap tq, td;
+  TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
+  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, ld_pad / 2));
+  MaxsimArgs a{};
+  a.n_q = n_q;
+  a.n_groups = kp.n_groups;
+  a.n_parts = kp.n_parts;
+  a.ld_pad = ld_pad;
+  a.num_kb = dim / 64;
+  a.k = 1;
+  a.n_stages = kp.n_stages;
+  a.a_bytes = kp.a_bytes;
+  a.stage_bytes = kp.stage_bytes;
+  a.n_chunks = n_d;
+  a.q_lens = qlens_dev;
+  a.d_lens = dlens_dev;
+  a.scores = S;
+  a.score_ld = n_d;
+  a.amax = amax;
+  TRY(launch_maxsim(2, 1, kp, tq, td, a, stream));                       // S + argmax (a3-a5)
+  const int32_t* pd = pos_idx ? pos_dev : nullptr;
+  TRY(launch_loss(S, n_q, n_d, n_d, pd, temperature, out_loss, stream));  // a11
+  infonce_grad_kernel<<<(n_q + 7) / 8, 256, 0, stream>>>(S, n_q, n_d, n_d, pd, temperature, G);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
+  const int64_t qrows = (int64_t)n_q * q_max_len;
+  const unsigned qblocks = (unsigned)((qrows + 7) / 8);
+  const size_t dsmem = (size_t)ld_pad * dim * 4;
+  auto launch_grads = [&](auto vpl, auto tin) -> hiper_status {
+    constexpr int VPL = decltype(vpl)::value;
+    using Tin = decltype(tin);
+    grad_q_kernel<VPL, Tin><<<qblocks, 256, 0, stream>>>(G, amax, n_q, n_d, dlayout, ld_pad,
+                                                         (const Tin*)q_tokens, q_max_len, qlens_dev,
+                                                         an, grad_q);
+    CUDA_TRY(cudaGetLastError());
+    auto gk = grad_d_kernel<VPL, Tin>;
+    CUDA_TRY(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
+    gk<<<n_d, VPL * 32, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
+                                          (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d);
+    CUDA_TRY(cudaGetLastError());
+    g_launches += 2;
+    return HIPER_OK;
+  };
+  using I2 = std::integral_constant<int, 2>;
+  using I4 = std::integral_constant<int, 4>;
+  if (dim == 128) {
+    if (dtype == HIPER_F32) return launch_grads(I4{}, float{});
+    return launch_grads(I4{}, __nv_bfloat16{});
+  }
+  if (dtype == HIPER_F32) return launch_grads(I2{}, float{});
+  return launch_grads(I2{}, __nv_bfloat16{});
 }
 
 extern "C" hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,

@@ -49,6 +49,7 @@ struct MaxsimArgs {
   int64_t score_ld;
   uint64_t* partial;      // MODE 1: [P][4G][k]
   uint32_t* progress;     // pair kernel: [n_pairs] progress words for L2 lockstep, or nullptr
+  uint8_t* amax;          // MODE 2: [n_q][score_ld][32] argmax doc-token index of every max
   int32_t window;         // chunks a pair may run ahead of the slowest pair (lockstep window)
 };
 
@@ -118,6 +119,19 @@ __device__ __forceinline__ void max64(const uint32_t (&v)[64], float (&m)[4]) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
       m[c] = fmaxf(fmaxf(m[c], __uint_as_float(v[i + 2 * c])), __uint_as_float(v[i + 2 * c + 1]));
+  }
+}
+// Running max AND argmax over 64 columns (MODE 2, for the backward pass): 4 chains over columns
+// c = i mod 4, ascending, strict '>' -> each chain keeps its lowest index on exact ties.
+__device__ __forceinline__ void max64_arg(const uint32_t (&v)[64], float (&m)[4], int (&ix)[4],
+                                          int base, int rem) {
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const float x = (i < rem) ? __uint_as_float(v[i]) : -INFINITY;
+    if (x > m[i & 3]) {
+      m[i & 3] = x;
+      ix[i & 3] = base + i;
+    }
   }
 }
 // Same, for a ragged tail: columns >= rem are excluded from the max (reading R2).

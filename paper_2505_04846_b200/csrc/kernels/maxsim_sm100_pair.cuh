@@ -209,22 +209,36 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         mbar_wait(bar_tfull(grp), mine & 1u);
         tc_fence_after();
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int ix4[4] = {0, 0, 0, 0};
         for (int32_t col = 0; col < (DBG ? 0 : ld); col += 64) {
           uint32_t v[64];
           tmem_ld64_wait(taddr_base + (uint32_t)col, v);
           const int rem = ld - col;
-          if (rem >= 64) max64(v, m4);
-          else max64_masked(v, m4, rem);
+          if constexpr (MODE == 2) {
+            max64_arg(v, m4, ix4, col, rem);
+          } else {
+            if (rem >= 64) max64(v, m4);
+            else max64_masked(v, m4, rem);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader);
         const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        if constexpr (MODE == 2) {
+          // argmax = lowest column index among the chains holding the max (reading: lowest u on ties)
+          int best = 0x7FFFFFFF;
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4)
+            if (m4[c4] == m && ix4[c4] < best) best = ix4[c4];
+          if (q < args.n_q)
+            args.amax[((int64_t)q * args.score_ld + c) * 32 + lane] = (uint8_t)best;
+        }
         float sv = ((int32_t)lane < lq) ? m : 0.0f;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
         sv += 0.0f;  // canonical +0
-        if constexpr (MODE == 0) {
+        if constexpr (MODE == 0 || MODE == 2) {
           if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + c] = sv;
         } else {
           const uint64_t key = make_key(sv, args.id_base + c);

@@ -356,7 +356,7 @@ def test_li_grad_central_finite_differences(tau):
     xd = rng.standard_normal((M, Ld, d))
     ql = np.array([4, 2, 3], np.int32)
     dl = np.array([5, 1, 3], np.int32)
-    L, gq, gd, _, gap = oracle.li_loss_grad(xq, ql, xd, dl, tau=tau, exact_norm=True)
+    L, gq, gd, _, gap, _ = oracle.li_loss_grad(xq, ql, xd, dl, tau=tau, exact_norm=True)
     assert gap[gap > 0].min() > 1e-3  # no near-ties: the max is differentiable here
     eps = 1e-6
     for x, g, lens in ((xq, gq, ql), (xd, gd, dl)):
@@ -381,9 +381,9 @@ def test_li_grad_matches_loss_and_structure():
     xq = rng.standard_normal((4, 8, 64)).astype(np.float32)
     xd = rng.standard_normal((5, 16, 64)).astype(np.float32)
     ql, dl = np.array([8, 3, 1, 5], np.int32), np.array([16, 2, 9, 1, 7], np.int32)
-    L, gq, gd, am, _ = oracle.li_loss_grad(xq, ql, xd, dl, pos=[0, 1, 2, 3], tau=0.5)
+    L, gq, gd, am, _, _ = oracle.li_loss_grad(xq, ql, xd, dl, pos=[0, 1, 2, 3], tau=0.5)
     S = oracle.maxsim_matrix(oracle.norm_rows(xq), ql, oracle.norm_rows(xd), dl)
     assert abs(L - oracle.infonce(S, pos=[0, 1, 2, 3], tau=0.5)) <= 1e-12
     assert (am < dl[None, :, None]).all()
-    L1, g1, g2, _, _ = oracle.li_loss_grad(xq[:1], ql[:1], xd[:1], dl[:1])
+    L1, g1, g2, _, _, _ = oracle.li_loss_grad(xq[:1], ql[:1], xd[:1], dl[:1])
     assert L1 == 0.0 and np.abs(g1).max() == 0.0 and np.abs(g2).max() == 0.0
