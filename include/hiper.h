@@ -218,6 +218,24 @@ HIPER_API hiper_status hiper_coltrast_scores_loss_grad(
     size_t workspace_bytes, float* out_scores, float* out_loss, float* grad_q, float* grad_d,
     hiper_stream_t stream);
 
+/* ------------------------------------------------------------------ NEXT N3: two-stage retrieval
+ * Stage 1: pooled-cosine top-k1 over pooled_idx (built with max_len 1: the paper's deployed
+ * retrieval); stage 2: exact MaxSim re-scoring of those k1 candidates over
+ * token_idx, the token rows of the SAME chunks (same n and id_base), keeping the final top-k
+ * (ColBERTv2's retrieve-then-rerank; SPEC.md:268-276 rerank; score desc, id asc).
+ *   q_pooled device [n_q][pooled dim]; q_tokens device [n_q][q_max_len][token dim]; q_lens HOST.
+ *   1 <= k <= k1 <= 16.  Single shard (comm not supported on this path yet). */
+HIPER_API size_t hiper_two_stage_workspace_size(const hiper_index* pooled_idx,
+                                                const hiper_index* token_idx, int32_t n_q,
+                                                int32_t k1);
+HIPER_API hiper_status hiper_two_stage_topk(const hiper_index* pooled_idx,
+                                            const hiper_index* token_idx, const void* q_pooled,
+                                            const void* q_tokens, hiper_dtype dtype,
+                                            const int32_t* q_lens, int32_t n_q, int32_t q_max_len,
+                                            int32_t k1, int32_t k, uint32_t flags, void* workspace,
+                                            size_t workspace_bytes, float* out_scores,
+                                            int64_t* out_ids, hiper_stream_t stream);
+
 /* Loss kernel alone over a given device score matrix S [n_q][n_d] (test support: isolates a11). */
 HIPER_API hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,
                                 const int32_t* pos_idx, float temperature, void* workspace,

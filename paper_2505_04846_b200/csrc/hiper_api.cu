@@ -1415,6 +1415,133 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   return launch_grads(I2{}, __nv_bfloat16{});
 }
 
+
+// ============================================================================ N3: two-stage retrieval
+// Stage 1: pooled cosine top-K1 (the paper's deployed retrieval) on a pooled
+// index; stage 2: exact MaxSim re-scoring of those K1 candidates on the token index of the same
+// chunks (ColBERTv2's pattern; SPEC.md:268-276 rerank), final top-k.  The stage-2
+// kernel is the CTA-pair MaxSim kernel reading candidate chunks by id (TMA coordinates), 8 queries
+// per pair scoring the union of their candidates.
+struct TwoStageWs {
+  size_t pooled = 0, pooled_bytes = 0, s1_scores = 0, s1_ids = 0, slots = 0, status = 0, qlens = 0,
+         qlayout = 0, S2 = 0, total = 0;
+};
+static void two_stage_ws_layout(const hiper_index* pix, const hiper_index* tix, int32_t n_q,
+                                int32_t k1, TwoStageWs& w) {
+  size_t off = 0;
+  w.pooled = off;
+  w.pooled_bytes = pooled_ws_size(pix, n_q, k1, nullptr);
+  off = align_up(off + w.pooled_bytes, 1024);
+  w.s1_scores = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 4, 256);
+  w.s1_ids = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 8, 256);
+  w.slots = off;
+  off = align_up(off + (size_t)n_q_pad_of(n_q) * k1 * 4, 256);
+  w.status = off;
+  off += 256;
+  w.qlens = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
+  w.qlayout = off;
+  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * tix->dim * 2, 1024);
+  w.S2 = off;
+  off = align_up(off + (size_t)n_q_pad_of(n_q) * 8 * k1 * 4, 1024);
+  w.total = off;
+}
+
+extern "C" size_t hiper_two_stage_workspace_size(const hiper_index* pooled_idx,
+                                                 const hiper_index* token_idx, int32_t n_q,
+                                                 int32_t k1) {
+  if (!pooled_idx || !token_idx || n_q < 0 || k1 < 1) return 0;
+  TwoStageWs w;
+  two_stage_ws_layout(pooled_idx, token_idx, n_q, k1, w);
+  return w.total;
+}
+
+extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper_index* tix,
+                                             const void* q_pooled, const void* q_tokens,
+                                             hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
+                                             int32_t q_max_len, int32_t k1, int32_t k,
+                                             uint32_t flags, void* workspace, size_t workspace_bytes,
+                                             float* out_scores, int64_t* out_ids,
+                                             hiper_stream_t stream_) {
+  g_launches = 0;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!pix || !tix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
+  if (pix->ld_pad != 1) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (max_len 1)");
+  if (tix->ld_pad == 1) return fail(HIPER_ERR_INVALID_ARG, "stage-2 index must hold token rows");
+  if (pix->n != tix->n || pix->id_base != tix->id_base)
+    return fail(HIPER_ERR_INVALID_ARG, "the two indexes must cover the same chunks (n, id_base)");
+  if (k1 < 1 || k < 1 || k > k1) return fail(HIPER_ERR_INVALID_ARG, "need 1 <= k <= k1");
+  if (k1 > kPooledKP) return fail(HIPER_ERR_UNSUPPORTED, "k1 %d > %d", k1, kPooledKP);
+  {
+    std::vector<int32_t> ones(std::max(n_q, 0), 1);
+    TRY(validate_queries(q_pooled, dtype, ones.data(), n_q, 1, pix->dim, flags, true));
+  }
+  TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, tix->dim, flags));
+  if (n_q == 0) return HIPER_OK;
+  if (!out_scores || !out_ids) return fail(HIPER_ERR_INVALID_ARG, "outputs are NULL");
+  DevInfo di;
+  TRY(device_info(di));
+  TwoStageWs w;
+  two_stage_ws_layout(pix, tix, n_q, k1, w);
+  TRY(check_ws(workspace, workspace_bytes, w.total));
+  uint8_t* ws = (uint8_t*)workspace;
+  float* s1s = (float*)(ws + w.s1_scores);
+  int64_t* s1i = (int64_t*)(ws + w.s1_ids);
+  int32_t* slots = (int32_t*)(ws + w.slots);
+  // stage 1: pooled top-k1 (pooled queries have one row each; lengths all 1)
+  std::vector<int32_t> ones(n_q, 1);
+  TRY(pooled_search(pix, q_pooled, dtype, ones.data(), n_q, pix->dim, k1, flags, nullptr,
+                    ws + w.pooled, w.pooled_bytes, s1s, s1i, nullptr, stream));
+  int32_t launches = g_launches;
+  // stage 2: slots, token query prep, MaxSim over each row group's candidate union
+  const int32_t nqp = n_q_pad_of(n_q);
+  ids_to_slots_kernel<<<(unsigned)(((int64_t)nqp * k1 + 255) / 256), 256, 0, stream>>>(
+      s1i, n_q, nqp, k1, pix->id_base, slots);
+  CUDA_TRY(cudaGetLastError());
+  uint32_t* status = (uint32_t*)(ws + w.status);
+  int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
+  __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
+  float* S2 = (float*)(ws + w.S2);
+  g_launches = 0;
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, tix->dim, flags, qlens_dev, qlayout,
+                   status, stream));
+  if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
+  KernelPlan kp;
+  const int32_t n_slots = 8 * k1;
+  TRY(plan_kernel(di, n_q, n_slots, tix->ld_pad, tix->dim, kp));
+  if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "rerank needs the CTA-pair kernel");
+  kp.n_parts = 1;  // a unit = one row group and its own candidate list
+  kp.grid = (int)std::min<int64_t>(kp.n_groups, di.num_sms / 2) * 2;
+  alignas(64) CUtensorMap tq;
+  TRY(make_tmap(&tq, qlayout, (int64_t)nqp * kQSlot, tix->dim, 128));
+  MaxsimArgs a{};
+  a.n_q = n_q;
+  a.n_groups = kp.n_groups;
+  a.n_parts = 1;
+  a.ld_pad = tix->ld_pad;
+  a.num_kb = tix->dim / 64;
+  a.k = 1;
+  a.n_stages = kp.n_stages;
+  a.a_bytes = kp.a_bytes;
+  a.stage_bytes = kp.stage_bytes;
+  a.n_chunks = n_slots;
+  a.id_base = tix->id_base;
+  a.q_lens = qlens_dev;
+  a.d_lens = tix->lens;
+  a.scores = S2;
+  a.score_ld = n_slots;
+  a.cand = slots;
+  TRY(launch_maxsim(0, 1, kp, tq, tix->tmap_half, a, stream));
+  rerank_select_kernel<1><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, n_slots, slots, k1, n_q,
+                                                              tix->id_base, k, out_scores, out_ids);
+  CUDA_TRY(cudaGetLastError());
+  g_launches += launches + 2;
+  return HIPER_OK;
+}
+
 extern "C" hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int32_t n_d,
                                            const int32_t* pos_idx, float temperature, void* workspace,
                                            size_t workspace_bytes, float* out_loss, hiper_stream_t stream_) {

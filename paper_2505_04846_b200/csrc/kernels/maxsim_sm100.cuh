@@ -50,6 +50,8 @@ struct MaxsimArgs {
   uint64_t* partial;      // MODE 1: [P][4G][k]
   uint32_t* progress;     // pair kernel: [n_pairs] progress words for L2 lockstep, or nullptr
   uint8_t* amax;          // MODE 2: [n_q][score_ld][32] argmax doc-token index of every max
+  const int32_t* cand;    // rerank (N3): [G][n_chunks] chunk index per slot of each row group
+                          // (-1 = empty slot), or nullptr = the corpus itself
   int32_t window;         // chunks a pair may run ahead of the slowest pair (lockstep window)
 };
 

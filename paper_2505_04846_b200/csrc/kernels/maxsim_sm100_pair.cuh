@@ -52,6 +52,16 @@ __device__ __forceinline__ void lockstep_wait(const uint32_t* progress, uint32_t
   }
 }
 
+// Chunk scored in slot c of row group g: the corpus itself, or (rerank, N3) a per-group candidate list.
+__device__ __forceinline__ int64_t slot_chunk(const MaxsimArgs& a, int32_t g, int64_t c) {
+  if (a.cand == nullptr) return c;
+  const int32_t id = __ldg(a.cand + (int64_t)g * a.n_chunks + c);
+  return id < 0 ? 0 : id;
+}
+__device__ __forceinline__ bool slot_valid(const MaxsimArgs& a, int32_t g, int64_t c) {
+  return a.cand == nullptr || __ldg(a.cand + (int64_t)g * a.n_chunks + c) >= 0;
+}
+
 template <int MODE, int KR, int DBG = 0>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
@@ -139,7 +149,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             const uint32_t full_leader = mapa_shared(bar_full(s), 0);
             for (int kb = 0; kb < args.num_kb; ++kb)
               tma_load_2d_pair(sB + s * args.stage_bytes + kb * half_tile, &tmap_d, full_leader,
-                               kb * 64, (int32_t)(c * args.ld_pad + (int64_t)rank * half_rows));
+                               kb * 64, (int32_t)(slot_chunk(args, g, c) * args.ld_pad + (int64_t)rank * half_rows));
           }
           if (++s == S) { s = 0; ph ^= 1u; }
         }
@@ -202,10 +212,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       topk.init();
       const int64_t first = c0 + (int64_t)((grp - (t & 1u)) & 1u);
       t += (uint32_t)(c1 - c0);
-      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + first) : 0;
+      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + slot_chunk(args, g, first)) : 0;
       for (int64_t c = first; c < c1; c += 2, ++mine) {
         const int32_t ld = ld_next;
-        if (c + 2 < c1) ld_next = __ldg(args.d_lens + c + 2);
+        if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk(args, g, c + 2));
         mbar_wait(bar_tfull(grp), mine & 1u);
         tc_fence_after();
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -239,7 +249,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
         sv += 0.0f;  // canonical +0
         if constexpr (MODE == 0 || MODE == 2) {
-          if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + c] = sv;
+          if (lane == 0 && q < args.n_q)
+            args.scores[(int64_t)q * args.score_ld + c] = slot_valid(args, g, c) ? sv : -INFINITY;
         } else {
           const uint64_t key = make_key(sv, args.id_base + c);
           if (key > topk.thresh) topk.insert(key, args.k, lane);
