@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--dim", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--qseed", type=int, default=2)
+    ap.add_argument("--grad", action="store_true",
+                    help="config2 only: time forward + backward (NEXT N1) instead of forward only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -402,7 +404,21 @@ def run_coltrast(a, rank, local_rank, world):
            torch.empty(1, dtype=torch.float32, device="cuda"))
     stream = torch.cuda.current_stream()
 
+    if a.grad:
+        nbg = H.lib().hiper_coltrast_grad_workspace_size(B, B, L, d)
+        gws, gwp, gwn = H._workspace(nbg, "cuda")
+        gq = torch.empty((B, Lq, d), dtype=torch.float32, device="cuda")
+        gd = torch.empty((B, L, d), dtype=torch.float32, device="cuda")
+        import ctypes
+
     def step(qd=qs, dd=docs):
+        if a.grad:
+            H._check(H.lib().hiper_coltrast_scores_loss_grad(
+                H._dev_ptr(qd), H._ptr(ql), B, Lq, H._dev_ptr(dd), H._ptr(dl), B, L, d,
+                H._dtype_code(qd), 0, None, ctypes.c_float(1.0), ctypes.c_void_p(gwp), gwn,
+                H._dev_ptr(out[0]), H._dev_ptr(out[1]), H._dev_ptr(gq), H._dev_ptr(gd),
+                H._stream_ptr(stream)))
+            return
         H.hiper_coltrast_scores_loss(qd, ql, dd, dl, temperature=1.0, workspace=ws, out=out,
                                      stream=stream)
 
@@ -464,7 +480,8 @@ def run_coltrast(a, rank, local_rank, world):
     peak, peak_src = load_peaks()
     value = world * steps / (ms / 1e3)
     line = {
-        "metric": "ColTrast in-batch MaxSim scores + InfoNCE steps/s (B=256, configs[1])",
+        "metric": ("ColTrast in-batch MaxSim scores + InfoNCE + backward (N1) steps/s (B=256, configs[1])"
+                   if a.grad else "ColTrast in-batch MaxSim scores + InfoNCE steps/s (B=256, configs[1])"),
         "value": value, "unit": "steps/s", "n_gpus": world, "steps": steps, "warmup": a.warmup,
         "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
