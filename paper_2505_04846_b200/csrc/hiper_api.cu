@@ -1340,6 +1340,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   KernelPlan kp;
   TRY(plan_kernel(di, n_q, n_d, ld_pad, dim, kp));
   if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "the backward pass needs the CTA-pair kernel");
+  if (n_q > 2048) return fail(HIPER_ERR_UNSUPPORTED, "backward supports n_q <= 2048 (got %d)", n_q);
   GradWs w;
   grad_ws_layout(n_q, n_d, d_max_len, dim, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
@@ -1389,7 +1390,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
   const int64_t qrows = (int64_t)n_q * q_max_len;
   const unsigned qblocks = (unsigned)((qrows + 7) / 8);
-  const size_t dsmem = (size_t)ld_pad * dim * 4;
+  const size_t dsmem = (size_t)n_q * 32 * 3 + (size_t)n_q * 8 + 2 * 8 * 257 * 4;
   auto launch_grads = [&](auto vpl, auto tin) -> hiper_status {
     constexpr int VPL = decltype(vpl)::value;
     using Tin = decltype(tin);
@@ -1399,7 +1400,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     CUDA_TRY(cudaGetLastError());
     auto gk = grad_d_kernel<VPL, Tin>;
     CUDA_TRY(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
-    gk<<<n_d, VPL * 32, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
+    gk<<<n_d, 256, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
                                           (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d);
     CUDA_TRY(cudaGetLastError());
     g_launches += 2;

@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(256) grad_q_kernel(const float* __restrict__ G
   float g[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) g[v] = 0.0f;
+#pragma unroll 4
   for (int32_t j = 0; j < M; ++j) {
     const float gij = G[(int64_t)i * M + j];
     const int32_t u = amax[((int64_t)i * M + j) * 32 + t];
@@ -108,10 +109,17 @@ __global__ void __launch_bounds__(256) grad_q_kernel(const float* __restrict__ G
   norm_backward_row<VPL, Tin>(xq + row * D, g, assume_normalized != 0, out, lane);
 }
 
-// One block per doc j: SMEM accumulator [ld_pad][D] fp32, thread = one dim, then one warp per row
-// for the Jacobian.  Blocks of D threads (64 or 128).
+// One block (8 warps) per doc j: invert the argmax map with a stable counting sort in SMEM, then
+// gather-sum each output row in (i, t) order.
+//  1. stage a(., ., j) (n_q x 32 bytes), G(., j) and q_lens in SMEM;
+//  2. warp w histograms its contiguous eighth of the entries (match_any per 32 entries);
+//  3. block-wide offsets: bucket u of warp w starts at base[u] + sum_{w' < w} hist[w'][u];
+//  4. warp w places its entries (stable: lane order within a chunk, chunks in order);
+//  5. warp w owns rows u = w, w+8, ...: sum G_ij qn_{i,t} over the bucket (8 gathers in flight, in
+//     sorted = (i, t) order: deterministic, no atomics), then NORM's Jacobian.
+// SMEM: n_q*32 (argmax) + n_q*32*2 (sorted entries) + n_q*8 + 8*257*4*2 bytes (n_q <= 2048).
 template <int VPL, typename Tin>
-__global__ void __launch_bounds__(128) grad_d_kernel(const float* __restrict__ G,
+__global__ void __launch_bounds__(256) grad_d_kernel(const float* __restrict__ G,
                                                      const uint8_t* __restrict__ amax, int32_t B,
                                                      int32_t M, const __nv_bfloat16* __restrict__ qlay,
                                                      const int32_t* __restrict__ q_lens,
@@ -120,25 +128,72 @@ __global__ void __launch_bounds__(128) grad_d_kernel(const float* __restrict__ G
                                                      uint32_t assume_normalized,
                                                      float* __restrict__ grad_d) {
   constexpr int D = VPL * 32;
-  extern __shared__ float acc[];  // [ld_pad][D]
+  constexpr int NB = 257;  // 256 buckets + 1 for padding entries (t >= len_q)
+  extern __shared__ uint8_t smem[];
+  const int32_t E = B * 32;  // entries (i, t)
+  uint8_t* amb = smem;                                                  // [E]
+  uint16_t* sorted = reinterpret_cast<uint16_t*>(smem + E);             // [E] entry indices (< 65536)
+  float* gcol = reinterpret_cast<float*>(smem + 3 * (size_t)E);         // [B]
+  int32_t* lq = reinterpret_cast<int32_t*>(gcol + B);                   // [B]
+  int32_t* hist = lq + B;                                               // [8][NB]
+  int32_t* offs = hist + 8 * NB;                                        // [8][NB]
+  __shared__ int32_t base[NB + 1];
   const int32_t j = blockIdx.x;
-  const uint32_t tid = threadIdx.x;  // dim (blockDim.x == D)
-  const int32_t lj = d_lens[j];
-  for (int32_t u = 0; u < lj; ++u) acc[u * D + tid] = 0.0f;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int32_t w = threadIdx.x; w < E / 4; w += blockDim.x) {
+    const int32_t i = w >> 3, k = w & 7;
+    reinterpret_cast<uint32_t*>(amb)[w] =
+        *reinterpret_cast<const uint32_t*>(amax + ((int64_t)i * M + j) * 32 + k * 4);
+  }
+  for (int32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    gcol[i] = G[(int64_t)i * M + j];
+    lq[i] = q_lens[i];
+  }
+  for (int32_t x = threadIdx.x; x < 8 * NB; x += blockDim.x) hist[x] = 0;
   __syncthreads();
-  for (int32_t i = 0; i < B; ++i) {
-    const float gij = G[(int64_t)i * M + j];
-    const uint8_t* am = amax + ((int64_t)i * M + j) * 32;
-    const __nv_bfloat16* qr = qlay + (int64_t)i * 32 * D;
-    const int32_t lq = q_lens[i];
-    for (int32_t t = 0; t < lq; ++t) {
-      const int32_t u = am[t];
-      acc[u * D + tid] = fmaf(gij, __bfloat162float(qr[t * D + tid]), acc[u * D + tid]);
+  const int32_t per = (E + 8 * 32 - 1) / (8 * 32) * 32;  // each warp's range, a multiple of 32
+  const int32_t e0 = warp * per;
+  auto bucket = [&](int32_t e) -> int32_t {  // entries past E or with t >= len_q go to bucket 256
+    return (e < E && (e & 31) < lq[e >> 5]) ? (int32_t)amb[e] : 256;
+  };
+  for (int32_t c = 0; c < per; c += 32) {
+    const int32_t e = e0 + c + lane;
+    const int32_t u = bucket(e);
+    const uint32_t m = __match_any_sync(0xffffffffu, u);
+    if (lane == (uint32_t)(__ffs(m) - 1)) hist[warp * NB + u] += __popc(m);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan over buckets of the per-bucket totals (257 adds)
+    int32_t run = 0;
+    for (int32_t u = 0; u < NB; ++u) {
+      base[u] = run;
+      for (int32_t w = 0; w < 8; ++w) run += hist[w * NB + u];
+    }
+    base[NB] = run;
+  }
+  __syncthreads();
+  for (int32_t u = threadIdx.x; u < NB; u += blockDim.x) {
+    int32_t run = base[u];
+    for (int32_t w = 0; w < 8; ++w) {
+      offs[w * NB + u] = run;
+      run += hist[w * NB + u];
     }
   }
   __syncthreads();
-  const uint32_t lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int32_t u = warp; u < d_max_len; u += nw) {
+  for (int32_t c = 0; c < per; c += 32) {
+    const int32_t e = e0 + c + lane;
+    const int32_t u = bucket(e);
+    const uint32_t m = __match_any_sync(0xffffffffu, u);
+    const int32_t rank = __popc(m & ((1u << lane) - 1u));
+    if (u < 256) sorted[offs[warp * NB + u] + rank] = (uint16_t)e;
+    __syncwarp();
+    if (lane == (uint32_t)(__ffs(m) - 1)) offs[warp * NB + u] += __popc(m);
+    __syncwarp();
+  }
+  __syncthreads();
+  const int32_t lj = d_lens[j];
+  for (int32_t u = warp; u < d_max_len; u += 8) {
     float* out = grad_d + ((int64_t)j * d_max_len + u) * D;
     if (u >= lj) {
 #pragma unroll
@@ -147,7 +202,32 @@ __global__ void __launch_bounds__(128) grad_d_kernel(const float* __restrict__ G
     }
     float g[VPL];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) g[v] = acc[u * D + lane * VPL + v];
+    for (int v = 0; v < VPL; ++v) g[v] = 0.0f;
+    const int32_t h0 = base[u], h1 = base[u + 1];
+    int32_t h = h0;
+    for (; h + 8 <= h1; h += 8) {
+      float qv[8][VPL];
+      float gv[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int32_t e = sorted[h + r];
+        gv[r] = gcol[e >> 5];
+        const __nv_bfloat16* qr = qlay + (int64_t)e * D + lane * VPL;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) qv[r][v] = __bfloat162float(qr[v]);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) g[v] = fmaf(gv[r], qv[r][v], g[v]);
+    }
+    for (; h < h1; ++h) {
+      const int32_t e = sorted[h];
+      const float gij = gcol[e >> 5];
+      const __nv_bfloat16* qr = qlay + (int64_t)e * D + lane * VPL;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) g[v] = fmaf(gij, __bfloat162float(qr[v]), g[v]);
+    }
     norm_backward_row<VPL, Tin>(xd + ((int64_t)j * d_max_len + u) * D, g, assume_normalized != 0,
                                 out, lane);
   }
