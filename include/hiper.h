@@ -76,7 +76,13 @@ enum {
   /* Query-side calls: synchronise `stream` after query preparation and return HIPER_ERR_ZERO_VECTOR /
    * HIPER_ERR_NONFINITE if a real query row is zero / non-finite.  Without it the same condition is
    * recorded in the workspace status word (hiper_workspace_status) and scores are undefined. */
-  HIPER_VALIDATE_SYNC = 8u
+  HIPER_VALIDATE_SYNC = 8u,
+  /* hiper_index_build only (NEXT N4, variable-length chunks from semantic chunking):
+   * length-bucketed packed layout.  Chunk c occupies roundup(lens[c], 16) rows of a tile of <= 256
+   * rows (hiper_pack_plan); the MaxSim kernel's MMA N is the tile's row count, so padded token
+   * columns are neither stored nor multiplied.  Results are those of the dense layout.  Exclusive
+   * with HIPER_BORROW_TOKENS; not accepted by hiper_two_stage_topk. */
+  HIPER_PACKED = 16u
 };
 
 typedef struct hiper_index_s hiper_index; /* opaque; immutable after build; shareable by readers */
@@ -115,6 +121,23 @@ HIPER_API hiper_status hiper_index_destroy(hiper_index* idx);
 HIPER_API hiper_status hiper_index_info(const hiper_index* idx, int64_t* n, int32_t* max_len, int32_t* dim,
                               int32_t* ld_pad, int64_t* id_base, const void** layout,
                               const int32_t** lens_dev);
+
+/* NEXT N4: the packing plan HIPER_PACKED uses (pure host function; no device needed).
+ *   lens       HOST [n], 1..256.
+ *   tiles_out  HOST int32 [n][4] capacity: tile t = {row0, n_rows, e0, e1}, n_rows % 16 == 0,
+ *              n_rows <= 256, tiles contiguous (row0 of t+1 = row0 + n_rows of t).
+ *   ents_out   HOST int32 [n][2]: entry e = {chunk index, (col << 16) | len}: the chunk's token j is
+ *              packed row row0 + col + j of its tile; entries [e0, e1) of a tile are its chunks,
+ *              every chunk appears in exactly one entry, col % 16 == 0.
+ *   n_tiles, n_rows: counts (either may be NULL).
+ * Greedy largest-first fill over 16 width buckets; deterministic in lens. */
+HIPER_API hiper_status hiper_pack_plan(const int32_t* lens, int64_t n, int32_t* tiles_out, int32_t* ents_out,
+                             int64_t* n_tiles, int64_t* n_rows);
+/* Packing of a built index (test support; any output may be NULL).  packed = 0 for a dense index.
+ * layout (hiper_index_info) is then bf16 [n_rows][dim]; tiles_dev int32 [n_tiles][4] and ents_dev
+ * int32 [n][2] are device copies of the hiper_pack_plan tables. */
+HIPER_API hiper_status hiper_index_pack_info(const hiper_index* idx, int32_t* packed, int64_t* n_tiles,
+                                   int64_t* n_rows, const void** tiles_dev, const void** ents_dev);
 
 /* ------------------------------------------------------------------ step a2: query preparation
  * NORM every real query row into the kernel's query layout: out device bf16 [n_q_pad][32][dim] with

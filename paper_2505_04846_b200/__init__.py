@@ -28,6 +28,7 @@ HIPER_ASSUME_NORMALIZED = 1
 HIPER_CHECK_FINITE = 2
 HIPER_BORROW_TOKENS = 4
 HIPER_VALIDATE_SYNC = 8
+HIPER_PACKED = 16
 
 STATUS = {
     0: "HIPER_OK", 1: "HIPER_ERR_INVALID_ARG", 2: "HIPER_ERR_DIM_MISMATCH",
@@ -47,7 +48,8 @@ EXPORTS = [
     "hiper_infonce_loss", "hiper_workspace_status", "hiper_last_launch_count",
     "hiper_profile_enable", "hiper_profile_read", "hiper_coltrast_loss_workspace_size",
     "hiper_coltrast_loss", "hiper_coltrast_grad_workspace_size", "hiper_coltrast_scores_loss_grad",
-    "hiper_two_stage_workspace_size", "hiper_two_stage_topk",
+    "hiper_two_stage_workspace_size", "hiper_two_stage_topk", "hiper_pack_plan",
+    "hiper_index_pack_info",
 ]
 
 
@@ -103,6 +105,8 @@ def lib():
         "hiper_coltrast_loss": ([P, P, i32, P, P, i32, i32, P, P, i32, i32, i32, u32, i32,
                                  ctypes.c_float, ctypes.c_float, P, P, sz, P, P, P, P], i32),
         "hiper_profile_read": ([P, P], i32),
+        "hiper_pack_plan": ([P, i64, P, P, P, P], i32),
+        "hiper_index_pack_info": ([P, P, P, P, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -214,15 +218,35 @@ class Index:
                                       ctypes.byref(lens)))
         self.n, self.max_len, self.dim, self.ld_pad = n.value, ml.value, dim.value, ldp.value
         self.id_base, self.layout_ptr, self.lens_ptr = idb.value, lay.value, lens.value
+        pk, nt, nr, tp, ep = (ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_void_p(),
+                              ctypes.c_void_p())
+        _check(lib().hiper_index_pack_info(handle, ctypes.byref(pk), ctypes.byref(nt),
+                                           ctypes.byref(nr), ctypes.byref(tp), ctypes.byref(ep)))
+        self.packed, self.n_tiles, self.n_rows = bool(pk.value), nt.value, nr.value
+        self._tiles_ptr, self._ents_ptr = tp.value, ep.value
 
     def layout(self):
-        """The device layout as a bf16 tensor [n][ld_pad][dim] aliasing the index (test support;
-        valid while the index lives -- clone it to keep it)."""
+        """The device layout aliasing the index (test support; valid while the index lives -- clone
+        it to keep it): bf16 [n][ld_pad][dim], or [n_rows][dim] for a packed index."""
         torch = _torch()
+        if self.packed:
+            if self.n_rows == 0:
+                return torch.empty((0, self.dim), dtype=torch.bfloat16, device="cuda")
+            src = _raw_u8_view(self.layout_ptr, self.n_rows * self.dim * 2)
+            return src.view(torch.bfloat16).view(self.n_rows, self.dim)
         if self.n == 0:
             return torch.empty((0, self.ld_pad, self.dim), dtype=torch.bfloat16, device="cuda")
         src = _raw_u8_view(self.layout_ptr, self.n * self.ld_pad * self.dim * 2)
         return src.view(torch.bfloat16).view(self.n, self.ld_pad, self.dim)
+
+    def pack_tables(self):
+        """(tiles int32 [n_tiles][4], ents int32 [n][2]) of a packed index, copied to the host."""
+        torch = _torch()
+        if not self.packed or self.n == 0:
+            return np.zeros((0, 4), np.int32), np.zeros((0, 2), np.int32)
+        t = _raw_u8_view(self._tiles_ptr, self.n_tiles * 16).view(torch.int32).view(-1, 4)
+        e = _raw_u8_view(self._ents_ptr, self.n * 8).view(torch.int32).view(-1, 2)
+        return t.cpu().numpy(), e.cpu().numpy()
 
     def close(self):
         if self.handle:
@@ -260,6 +284,19 @@ def hiper_index_build(tokens, lens, *, id_base: int = 0, flags: int = 0, stream=
                                    ctypes.byref(h)))
     keep = tokens if flags & HIPER_BORROW_TOKENS else None
     return Index(h, keep)
+
+
+def hiper_pack_plan(lens):
+    """NEXT N4 packing plan (host only): (tiles int32 [n_tiles][4] = row0, n_rows, e0, e1;
+    ents int32 [n][2] = chunk, (col << 16) | len; n_rows total)."""
+    ln = _host_i32(lens)
+    n = ln.shape[0]
+    tiles = np.zeros((max(n, 1), 4), np.int32)
+    ents = np.zeros((max(n, 1), 2), np.int32)
+    nt, nr = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().hiper_pack_plan(_ptr(ln), n, _ptr(tiles), _ptr(ents), ctypes.byref(nt),
+                                 ctypes.byref(nr)))
+    return tiles[:nt.value].copy(), ents[:n].copy(), nr.value
 
 
 def hiper_prepare_queries(q_tokens, q_lens, *, flags: int = 0, stream=None):

@@ -196,6 +196,8 @@ static bool is_device_ptr(const void* p) {
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+static bool use_pair_kernel();
+
 // ============================================================================ the index
 struct hiper_index_s {
   int64_t n = 0;
@@ -207,7 +209,73 @@ struct hiper_index_s {
   int32_t* lens = nullptr;  // device [n]
   alignas(64) CUtensorMap tmap;       // box = 64 dims x ld_pad rows   (single-CTA kernel)
   alignas(64) CUtensorMap tmap_half;  // box = 64 dims x ld_pad/2 rows (CTA-pair kernel)
+  // packed layout (HIPER_PACKED, N4): tok is bf16 [n_rows][dim]; tiles/ents as in MaxsimArgs
+  bool packed = false;
+  int64_t n_tiles = 0, n_rows = 0;
+  int4* tiles = nullptr;  // device [n_tiles]
+  int2* ents = nullptr;   // device [n]
 };
+
+// ---------------------------------------------------------------------------- N4 packing plan
+// Chunk c occupies w_c = roundup(len_c, 16) packed rows.  Tiles hold up to kTileRows rows (the MMA N
+// of the CTA pair).  Greedy largest-first fill with 16 width buckets: a tile is seeded with a chunk of
+// the largest remaining width, then repeatedly takes a chunk of the largest width that still fits.
+// Within a bucket chunks go in ascending index order, so the plan is a pure function of lens.
+static constexpr int32_t kTileRows = 256;
+static hiper_status pack_plan(const int32_t* lens, int64_t n, std::vector<int4>& tiles,
+                              std::vector<int2>& ents, std::vector<int64_t>& dst_row, int64_t& rows) {
+  constexpr int NB = kTileRows / 16;
+  std::vector<std::vector<int32_t>> bucket(NB);
+  for (int64_t c = 0; c < n; ++c) {
+    if (lens[c] < 1 || lens[c] > kTileRows)
+      return fail(HIPER_ERR_INVALID_ARG, "chunk %lld length %d outside 1..%d", (long long)c, lens[c], kTileRows);
+    bucket[(lens[c] + 15) / 16 - 1].push_back((int32_t)c);
+  }
+  std::vector<size_t> head(NB, 0);
+  tiles.clear();
+  ents.clear();
+  ents.reserve((size_t)n);
+  dst_row.assign((size_t)n, 0);
+  rows = 0;
+  int64_t left = n;
+  while (left > 0) {
+    const int32_t e0 = (int32_t)ents.size();
+    int32_t used = 0;
+    while (true) {
+      int b = std::min(NB, (kTileRows - used) / 16) - 1;
+      while (b >= 0 && head[b] == bucket[b].size()) --b;
+      if (b < 0) break;
+      const int32_t c = bucket[b][head[b]++];
+      ents.push_back(make_int2(c, (used << 16) | lens[c]));
+      dst_row[c] = rows + used;
+      used += 16 * (b + 1);
+      --left;
+    }
+    if (rows + used >= 0x7FFFFFFFll) return fail(HIPER_ERR_UNSUPPORTED, "packed rows >= 2^31; shard the corpus");
+    tiles.push_back(make_int4((int32_t)rows, used, e0, (int32_t)ents.size()));
+    rows += used;
+  }
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_pack_plan(const int32_t* lens, int64_t n, int32_t* tiles_out,
+                                        int32_t* ents_out, int64_t* n_tiles, int64_t* n_rows) {
+  if (n < 0) return fail(HIPER_ERR_INVALID_ARG, "n < 0");
+  if (n > 0 && (!lens || !tiles_out || !ents_out)) return fail(HIPER_ERR_INVALID_ARG, "NULL array");
+  if (n > 0x7FFFFFFFll) return fail(HIPER_ERR_UNSUPPORTED, "n >= 2^31");
+  std::vector<int4> tiles;
+  std::vector<int2> ents;
+  std::vector<int64_t> dst;
+  int64_t rows = 0;
+  TRY(pack_plan(lens, n, tiles, ents, dst, rows));
+  if (n > 0) {
+    memcpy(tiles_out, tiles.data(), tiles.size() * sizeof(int4));
+    memcpy(ents_out, ents.data(), ents.size() * sizeof(int2));
+  }
+  if (n_tiles) *n_tiles = (int64_t)tiles.size();
+  if (n_rows) *n_rows = rows;
+  return HIPER_OK;
+}
 
 // Token path (max_len > 1): dim in {64, 128}.  Pooled path (one row per item, a12): dim % 64 == 0,
 // 64 <= dim <= 4096.
@@ -226,7 +294,7 @@ static hiper_status check_dims(int32_t dim, bool pooled = false) {
 static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src, int32_t in_rows,
                                 const int32_t* lens_dev, int64_t n_items, int32_t out_rows,
                                 int32_t dim, uint32_t flags, __nv_bfloat16* out, uint32_t* status,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, const int64_t* dst_row = nullptr) {
   const int64_t rows = n_items * (int64_t)out_rows;
   if (rows == 0) return HIPER_OK;
   const int threads = 256;
@@ -236,11 +304,12 @@ static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src
   const uint32_t cf = (flags & HIPER_CHECK_FINITE) ? 1u : 0u;
   if (dtype == HIPER_F32)
     norm_layout_kernel<float><<<(unsigned)blocks, threads, 0, stream>>>(
-        (const float*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out, status);
+        (const float*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out, status,
+        dst_row);
   else
     norm_layout_kernel<__nv_bfloat16><<<(unsigned)blocks, threads, 0, stream>>>(
         (const __nv_bfloat16*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out,
-        status);
+        status, dst_row);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return HIPER_OK;
@@ -266,19 +335,29 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   *out = nullptr;
   if (n < 0) return fail(HIPER_ERR_INVALID_ARG, "n < 0");
   if (dtype != HIPER_F32 && dtype != HIPER_BF16) return fail(HIPER_ERR_INVALID_ARG, "bad dtype");
-  if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_BORROW_TOKENS))
+  if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_BORROW_TOKENS | HIPER_PACKED))
     return fail(HIPER_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   if (max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "max_len must be >= 1");
   if (max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "max_len %d > 256", max_len);
-  const bool pooled = (max_len == 1);  // one vector per chunk: the pooled limit case (a12)
+  const bool pooled = (max_len == 1) && !(flags & HIPER_PACKED);  // the pooled limit case (a12)
   TRY(check_dims(dim, pooled));
   if (id_base < 0 || id_base + n >= 0xFFFFFFFFll)
     return fail(HIPER_ERR_UNSUPPORTED, "global ids must be < 2^32-1");
+  const bool packed = (flags & HIPER_PACKED) != 0;
   const int32_t ld_pad = pooled ? 1 : (int32_t)round_up(max_len, 16);
-  if (n * ld_pad >= 0x7FFFFFFFll)
+  if (!packed && n * ld_pad >= 0x7FFFFFFFll)
     return fail(HIPER_ERR_UNSUPPORTED, "n * ld_pad >= 2^31 rows for one index; shard the corpus");
   TRY(check_lens(lens, n, max_len, "chunk"));
   const bool borrow = (flags & HIPER_BORROW_TOKENS) != 0;
+  if (packed && borrow)
+    return fail(HIPER_ERR_INVALID_ARG, "HIPER_PACKED and HIPER_BORROW_TOKENS are exclusive");
+  if (packed && !use_pair_kernel())
+    return fail(HIPER_ERR_UNSUPPORTED, "HIPER_PACKED needs the CTA-pair kernel (HIPER_MAXSIM_CTA=1 set)");
+  std::vector<int4> p_tiles;
+  std::vector<int2> p_ents;
+  std::vector<int64_t> p_dst;
+  int64_t p_rows = 0;
+  if (packed) TRY(pack_plan(lens, n, p_tiles, p_ents, p_dst, p_rows));
   if (borrow && (dtype != HIPER_BF16 || max_len != ld_pad || (dim % 8) != 0))
     return fail(HIPER_ERR_INVALID_ARG, "HIPER_BORROW_TOKENS needs bf16 tokens and max_len %% 16 == 0");
   if (n > 0) {
@@ -296,9 +375,13 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   ix->dim = dim;
   ix->id_base = id_base;
   ix->device = di.device;
+  int64_t* dst_dev = nullptr;
   auto cleanup = [&](hiper_status s) {
     if (ix->owns_tok && ix->tok) cudaFree(ix->tok);
     if (ix->lens) cudaFree(ix->lens);
+    if (ix->tiles) cudaFree(ix->tiles);
+    if (ix->ents) cudaFree(ix->ents);
+    if (dst_dev) cudaFree(dst_dev);
     delete ix;
     return s;
   };
@@ -307,6 +390,22 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "lens alloc"));
   if (borrow) {
     ix->tok = (__nv_bfloat16*)const_cast<void*>(tokens);
+  } else if (packed) {
+    ix->packed = true;
+    ix->n_tiles = (int64_t)p_tiles.size();
+    ix->n_rows = p_rows;
+    if (cudaMalloc(&ix->tok, (size_t)std::max<int64_t>(p_rows, 1) * dim * 2) != cudaSuccess)
+      return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "packed layout alloc %lld bytes", (long long)p_rows * dim * 2));
+    ix->owns_tok = true;
+    if (cudaMalloc(&ix->tiles, std::max<size_t>(p_tiles.size(), 1) * sizeof(int4)) != cudaSuccess ||
+        cudaMalloc(&ix->ents, std::max<size_t>(p_ents.size(), 1) * sizeof(int2)) != cudaSuccess ||
+        cudaMalloc(&dst_dev, std::max<size_t>(p_dst.size(), 1) * sizeof(int64_t)) != cudaSuccess)
+      return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "packing tables"));
+    if (n > 0 &&
+        (cudaMemcpyAsync(ix->tiles, p_tiles.data(), p_tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+         cudaMemcpyAsync(ix->ents, p_ents.data(), p_ents.size() * sizeof(int2), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+         cudaMemcpyAsync(dst_dev, p_dst.data(), p_dst.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream) != cudaSuccess))
+      return cleanup(fail(HIPER_ERR_CUDA, "packing tables copy"));
   } else {
     if (cudaMalloc(&ix->tok, (size_t)n_alloc * ld_pad * dim * 2) != cudaSuccess)
       return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "layout alloc %lld bytes",
@@ -324,7 +423,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
       st = fail(HIPER_ERR_CUDA, "lens copy"); break;
     }
     st = launch_norm(tokens, dtype, n, max_len, ix->lens, n, ld_pad, dim,
-                     flags | HIPER_CHECK_FINITE, ix->tok, status, stream);
+                     flags | HIPER_CHECK_FINITE, ix->tok, status, stream, dst_dev);
     if (st != HIPER_OK) break;
     if (cudaMemcpyAsync(&hstat, status, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
         cudaStreamSynchronize(stream) != cudaSuccess) {
@@ -335,6 +434,9 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     if (hstat & kStatusZeroRow) { st = fail(HIPER_ERR_ZERO_VECTOR, "a chunk token row has norm 0"); break; }
     if (n > 0 && pooled) {
       st = make_tmap(&ix->tmap, ix->tok, n, dim, 128);  // pooled kernel: 128 chunk rows per CTA
+    } else if (n > 0 && packed) {
+      // half a full tile per CTA; a shorter tile's MMA reads only its first n_rows/2 rows
+      st = make_tmap(&ix->tmap_half, ix->tok, p_rows, dim, kTileRows / 2);
     } else if (n > 0) {
       st = make_tmap(&ix->tmap, ix->tok, n * (int64_t)ld_pad, dim, ld_pad);
       if (st == HIPER_OK) st = make_tmap(&ix->tmap_half, ix->tok, n * (int64_t)ld_pad, dim, ld_pad / 2);
@@ -342,6 +444,10 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   } while (0);
   cudaFree(status);
   if (st != HIPER_OK) return cleanup(st);
+  if (dst_dev) {
+    cudaFree(dst_dev);  // the stream was synchronised above
+    dst_dev = nullptr;
+  }
   *out = ix;
   return HIPER_OK;
 }
@@ -350,6 +456,8 @@ extern "C" hiper_status hiper_index_destroy(hiper_index* ix) {
   if (!ix) return HIPER_OK;
   if (ix->owns_tok && ix->tok) cudaFree(ix->tok);
   if (ix->lens) cudaFree(ix->lens);
+  if (ix->tiles) cudaFree(ix->tiles);
+  if (ix->ents) cudaFree(ix->ents);
   delete ix;
   return HIPER_OK;
 }
@@ -365,6 +473,18 @@ extern "C" hiper_status hiper_index_info(const hiper_index* ix, int64_t* n, int3
   if (id_base) *id_base = ix->id_base;
   if (layout) *layout = ix->tok;
   if (lens_dev) *lens_dev = ix->lens;
+  return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_index_pack_info(const hiper_index* ix, int32_t* packed, int64_t* n_tiles,
+                                              int64_t* n_rows, const void** tiles_dev,
+                                              const void** ents_dev) {
+  if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
+  if (packed) *packed = ix->packed ? 1 : 0;
+  if (n_tiles) *n_tiles = ix->n_tiles;
+  if (n_rows) *n_rows = ix->n_rows;
+  if (tiles_dev) *tiles_dev = ix->tiles;
+  if (ents_dev) *ents_dev = ix->ents;
   return HIPER_OK;
 }
 
@@ -542,15 +662,15 @@ static int debug_mode() {
   return m;
 }
 
-template <int MODE, int KR>
+template <int MODE, int KR, bool PACKED = false>
 static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
                                     const MaxsimArgs& a, cudaStream_t stream) {
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   bool rec = false;
   if (kp.pair) {
-    auto kern = maxsim_sm100_pair_kernel<MODE, KR, 0>;
-    if (MODE == 1 && KR == 1 && debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1>;
-    if (MODE == 1 && KR == 1 && debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2>;
+    auto kern = maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED>;
+    if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1>;
+    if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)kp.grid);
@@ -581,6 +701,14 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
 static hiper_status launch_maxsim(int mode, int k, const KernelPlan& kp, const CUtensorMap& tq,
                                   const CUtensorMap& td, const MaxsimArgs& a, cudaStream_t stream) {
   if (kp.grid == 0) return HIPER_OK;
+  if (a.tiles != nullptr) {  // packed corpus (N4)
+    if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "a packed index needs the CTA-pair kernel");
+    if (mode == 0) return launch_maxsim_t<0, 1, true>(kp, tq, td, a, stream);
+    if (mode != 1) return fail(HIPER_ERR_UNSUPPORTED, "argmax capture on a packed index");
+    if (k <= 32) return launch_maxsim_t<1, 1, true>(kp, tq, td, a, stream);
+    if (k <= 64) return launch_maxsim_t<1, 2, true>(kp, tq, td, a, stream);
+    return launch_maxsim_t<1, 4, true>(kp, tq, td, a, stream);
+  }
   if (mode == 0) return launch_maxsim_t<0, 1>(kp, tq, td, a, stream);
   if (mode == 2) {
     if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "argmax capture needs the CTA-pair kernel");
@@ -693,6 +821,15 @@ static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t k,
   w.total = off;
 }
 
+// Kernel slots of an index: chunks, or the tiles of a packed index (N4).
+static int64_t index_slots(const hiper_index* ix) { return ix->packed ? ix->n_tiles : ix->n; }
+static int32_t index_slot_rows(const hiper_index* ix) { return ix->packed ? kTileRows : ix->ld_pad; }
+static void set_packed_args(const hiper_index* ix, MaxsimArgs& a) {
+  if (!ix->packed) return;
+  a.tiles = ix->tiles;
+  a.ents = ix->ents;
+}
+
 static hiper_status check_ws(const void* ws, size_t have, size_t need) {
   if (!ws) return fail(HIPER_ERR_WORKSPACE, "workspace is NULL (need %zu bytes)", need);
   if (((uintptr_t)ws & 1023) != 0) return fail(HIPER_ERR_WORKSPACE, "workspace must be 1024-B aligned");
@@ -714,7 +851,7 @@ extern "C" size_t hiper_maxsim_topk_workspace_size(const hiper_index* ix, int32_
   const bool pair = use_pair_kernel();
   const int32_t G = n_q_pad_of(n_q) / (pair ? 8 : 4);
   TopkWs w;
-  topk_ws_layout(n_q, ix->dim, choose_parts(G, ix->n, pair ? num_sms / 2 : num_sms), k,
+  topk_ws_layout(n_q, ix->dim, choose_parts(G, index_slots(ix), pair ? num_sms / 2 : num_sms), k,
                  comm ? comm->world : 1, comm != nullptr, w);
   return w.total;
 }
@@ -899,7 +1036,7 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
   TRY(device_info(di));
   if (di.device != ix->device) return fail(HIPER_ERR_INVALID_ARG, "index lives on device %d, current is %d", ix->device, di.device);
   KernelPlan kp;
-  TRY(plan_kernel(di, n_q, ix->n, ix->ld_pad, dim, kp));
+  TRY(plan_kernel(di, n_q, index_slots(ix), index_slot_rows(ix), dim, kp));
   const int32_t world = comm ? comm->world : 1;
   TopkWs w;
   topk_ws_layout(n_q, dim, kp.n_parts, k, world, comm != nullptr, w);
@@ -925,13 +1062,14 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
     a.n_q = n_q;
     a.n_groups = kp.n_groups;
     a.n_parts = kp.n_parts;
-    a.ld_pad = ix->ld_pad;
+    a.ld_pad = index_slot_rows(ix);
     a.num_kb = dim / 64;
     a.k = k;
     a.n_stages = kp.n_stages;
     a.a_bytes = kp.a_bytes;
     a.stage_bytes = kp.stage_bytes;
-    a.n_chunks = ix->n;
+    a.n_chunks = index_slots(ix);
+    set_packed_args(ix, a);
     a.id_base = ix->id_base;
     a.q_lens = qlens_dev;
     a.d_lens = ix->lens;
@@ -997,7 +1135,7 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
   DevInfo di;
   TRY(device_info(di));
   KernelPlan kp;
-  TRY(plan_kernel(di, n_q, ix->n, ix->ld_pad, dim, kp));
+  TRY(plan_kernel(di, n_q, index_slots(ix), index_slot_rows(ix), dim, kp));
   ScoresWs w;
   scores_ws_layout(n_q, dim, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
@@ -1014,18 +1152,19 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
   a.n_q = n_q;
   a.n_groups = kp.n_groups;
   a.n_parts = kp.n_parts;
-  a.ld_pad = ix->ld_pad;
+  a.ld_pad = index_slot_rows(ix);
   a.num_kb = dim / 64;
   a.k = 1;
   a.n_stages = kp.n_stages;
   a.a_bytes = kp.a_bytes;
   a.stage_bytes = kp.stage_bytes;
-  a.n_chunks = ix->n;
+  a.n_chunks = index_slots(ix);
   a.id_base = ix->id_base;
   a.q_lens = qlens_dev;
   a.d_lens = ix->lens;
   a.scores = out_scores;
   a.score_ld = ix->n;
+  set_packed_args(ix, a);
   return launch_maxsim(0, 1, kp, tq, kp.pair ? ix->tmap_half : ix->tmap, a, stream);
 }
 
@@ -1471,6 +1610,8 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   if (!pix || !tix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
   if (pix->ld_pad != 1) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (max_len 1)");
   if (tix->ld_pad == 1) return fail(HIPER_ERR_INVALID_ARG, "stage-2 index must hold token rows");
+  if (tix->packed || pix->packed)
+    return fail(HIPER_ERR_UNSUPPORTED, "two-stage retrieval reads chunks by id: build the indexes without HIPER_PACKED");
   if (pix->n != tix->n || pix->id_base != tix->id_base)
     return fail(HIPER_ERR_INVALID_ARG, "the two indexes must cover the same chunks (n, id_base)");
   if (k1 < 1 || k < 1 || k > k1) return fail(HIPER_ERR_INVALID_ARG, "need 1 <= k <= k1");

@@ -53,6 +53,12 @@ struct MaxsimArgs {
   const int32_t* cand;    // rerank (N3): [G][n_chunks] chunk index per slot of each row group
                           // (-1 = empty slot), or nullptr = the corpus itself
   int32_t window;         // chunks a pair may run ahead of the slowest pair (lockstep window)
+  // packed layout (N4, PACKED kernels): slot c of the kernel is tile c, not chunk c.
+  //   tiles[c] = {row0, n_rows, e0, e1}: n_rows (multiple of 16, <= 256) packed token rows starting
+  //              at row0 hold the chunks of entries [e0, e1);
+  //   ents[e]  = {chunk index, (col << 16) | len}: the chunk's tokens are tile columns [col, col+len).
+  const int4* tiles;
+  const int2* ents;
 };
 
 // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare; warps 4-7 = epilogue warpgroup 0 (accumulator 0, even
@@ -134,6 +140,24 @@ __device__ __forceinline__ void max64_arg(const uint32_t (&v)[64], float (&m)[4]
       m[i & 3] = x;
       ix[i & 3] = base + i;
     }
+  }
+}
+// Running max over N (16 or 32) columns, all real / only the first `rem` real (reading R2).
+template <int N>
+__device__ __forceinline__ void maxN(const uint32_t (&v)[N], float (&m)[4]) {
+#pragma unroll
+  for (int i = 0; i < N; i += 8) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      m[c] = fmaxf(fmaxf(m[c], __uint_as_float(v[i + 2 * c])), __uint_as_float(v[i + 2 * c + 1]));
+  }
+}
+template <int N>
+__device__ __forceinline__ void maxN_masked(const uint32_t (&v)[N], float (&m)[4], int rem) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float x = (i < rem) ? __uint_as_float(v[i]) : -INFINITY;
+    m[i & 3] = fmaxf(m[i & 3], x);
   }
 }
 // Same, for a ragged tail: columns >= rem are excluded from the max (reading R2).

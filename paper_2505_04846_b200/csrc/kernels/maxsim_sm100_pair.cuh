@@ -62,7 +62,9 @@ __device__ __forceinline__ bool slot_valid(const MaxsimArgs& a, int32_t g, int64
   return a.cand == nullptr || __ldg(a.cand + (int64_t)g * a.n_chunks + c) >= 0;
 }
 
-template <int MODE, int KR, int DBG = 0>
+// PACKED (N4): the slots are the tiles of a length-bucketed packed corpus (MaxsimArgs::tiles/ents):
+// the MMA N is the tile's n_rows, and the epilogue reduces each chunk over its own column segment.
+template <int MODE, int KR, int DBG = 0, bool PACKED = false>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_d, const MaxsimArgs args) {
@@ -147,9 +149,18 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           } else {
             if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
             const uint32_t full_leader = mapa_shared(bar_full(s), 0);
-            for (int kb = 0; kb < args.num_kb; ++kb)
-              tma_load_2d_pair(sB + s * args.stage_bytes + kb * half_tile, &tmap_d, full_leader,
-                               kb * 64, (int32_t)(slot_chunk(args, g, c) * args.ld_pad + (int64_t)rank * half_rows));
+            {
+              int32_t brow;
+              if constexpr (PACKED) {
+                const int4 tl = __ldg(args.tiles + c);
+                brow = tl.x + (int32_t)rank * (tl.y >> 1);
+              } else {
+                brow = (int32_t)(slot_chunk(args, g, c) * args.ld_pad + (int64_t)rank * half_rows);
+              }
+              for (int kb = 0; kb < args.num_kb; ++kb)
+                tma_load_2d_pair(sB + s * args.stage_bytes + kb * half_tile, &tmap_d, full_leader,
+                                 kb * 64, brow);
+            }
           }
           if (++s == S) { s = 0; ph ^= 1u; }
         }
@@ -171,7 +182,13 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         mbar_wait(bar_afull(ab), aph);
         tc_fence_after();
         const uint32_t a_tile = sA + ab * args.a_bytes;
+        int32_t nr_next = (PACKED && c0 < c1) ? __ldg(&args.tiles[c0].y) : 0;
         for (int64_t c = c0; c < c1; ++c, ++t) {
+          uint32_t idesc_c = idesc;
+          if constexpr (PACKED) {  // MMA N = this tile's packed rows (multiple of 16)
+            idesc_c = idesc_bf16_f32(256, (uint32_t)nr_next);
+            if (c + 1 < c1) nr_next = __ldg(&args.tiles[c + 1].y);
+          }
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
           mbar_wait(bar_tempty(acc), tph ^ 1u);
           tc_fence_after();
@@ -185,7 +202,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               mma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_kb + kk * 32),
-                               umma_desc_sw128(b_kb + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
+                               umma_desc_sw128(b_kb + kk * 32), idesc_c, (kb | kk) != 0 ? 1u : 0u);
           }
           mma_commit_pair_mc(bar_empty(s), 0x3);  // both CTAs' stage s free again
           if (++s == S) { s = 0; ph ^= 1u; }
@@ -212,6 +229,62 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       topk.init();
       const int64_t first = c0 + (int64_t)((grp - (t & 1u)) & 1u);
       t += (uint32_t)(c1 - c0);
+      if constexpr (PACKED) {
+        int4 tl_next = (first < c1) ? __ldg(args.tiles + first) : make_int4(0, 0, 0, 0);
+        for (int64_t c = first; c < c1; c += 2, ++mine) {
+          const int4 tl = tl_next;
+          const int32_t n_ent = tl.w - tl.z;  // <= 16 chunks per tile
+          // one entry per lane, loaded while the accumulator is still being computed
+          const int2 my_ent = ((int32_t)lane < n_ent) ? __ldg(args.ents + tl.z + lane) : make_int2(0, 0);
+          if (c + 2 < c1) tl_next = __ldg(args.tiles + c + 2);
+          mbar_wait(bar_tfull(grp), mine & 1u);
+          tc_fence_after();
+          for (int32_t e = 0; e < n_ent; ++e) {
+            const int32_t chunk = __shfl_sync(0xffffffffu, my_ent.x, e);
+            const int32_t cl = __shfl_sync(0xffffffffu, my_ent.y, e);
+            const int32_t len = cl & 0xFFFF;
+            const uint32_t ta = taddr_base + (uint32_t)(cl >> 16);
+            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            int32_t col = 0;
+            for (; col + 64 <= len; col += 64) {
+              uint32_t v[64];
+              tmem_ld64_wait(ta + (uint32_t)col, v);
+              max64(v, m4);
+            }
+            int32_t rem = len - col;  // 0..63; reads stay inside [col, roundup(len, 16))
+            if (rem > 32) {
+              uint32_t v[32];
+              tmem_ld32_wait(ta + (uint32_t)col, v);
+              maxN<32>(v, m4);
+              col += 32;
+              rem -= 32;
+            }
+            if (rem > 16) {
+              uint32_t v[32];
+              tmem_ld32_wait(ta + (uint32_t)col, v);
+              maxN_masked<32>(v, m4, rem);
+            } else if (rem > 0) {
+              uint32_t v[16];
+              tmem_ld16_wait(ta + (uint32_t)col, v);
+              maxN_masked<16>(v, m4, rem);
+            }
+            const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+            float sv = ((int32_t)lane < lq) ? m : 0.0f;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+            sv += 0.0f;  // canonical +0
+            if constexpr (MODE == 0) {
+              if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk] = sv;
+            } else {
+              const uint64_t key = make_key(sv, args.id_base + chunk);
+              if (key > topk.thresh) topk.insert(key, args.k, lane);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        }
+      } else {
       int32_t ld_next = (first < c1) ? __ldg(args.d_lens + slot_chunk(args, g, first)) : 0;
       for (int64_t c = first; c < c1; c += 2, ++mine) {
         const int32_t ld = ld_next;
@@ -256,6 +329,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           if (key > topk.thresh) topk.insert(key, args.k, lane);
         }
       }
+      }  // !PACKED
       if constexpr (MODE == 1) {
         // partial lists: [P][kEpiGroups][8G][k]
         uint64_t* dst = args.partial +

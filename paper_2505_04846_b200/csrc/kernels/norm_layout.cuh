@@ -44,19 +44,24 @@ __device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, flo
 // lens: device [n_src] (items >= n_src are empty)
 // d % 8 == 0 and 16-B aligned rows.  In-place (in == out) is allowed when Tin == bf16 and
 // in_rows == out_rows: every thread reads and writes only its own row.
+// dst_row (packed layout, N4; nullptr = dense): item i's rows go to packed rows dst_row[i] + j for
+// j < roundup(len, 16) only (the padding rows of its 16-row slot are zeroed); out_rows is then just
+// the per-item thread range (>= roundup(max_len, 16)).
 template <typename Tin>
 __global__ void __launch_bounds__(256) norm_layout_kernel(const Tin* in, int64_t n_src, int32_t in_rows,
                                                           const int32_t* __restrict__ lens,
                                                           int64_t n_items, int32_t out_rows, int32_t d,
                                                           uint32_t assume_normalized,
                                                           uint32_t check_finite,
-                                                          __nv_bfloat16* out, uint32_t* status) {
+                                                          __nv_bfloat16* out, uint32_t* status,
+                                                          const int64_t* __restrict__ dst_row) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n_items * (int64_t)out_rows) return;
   const int64_t item = row / out_rows;
   const int32_t j = (int32_t)(row - item * out_rows);
-  uint4* dst = reinterpret_cast<uint4*>(out + row * d);
   const int32_t len = item < n_src ? lens[item] : 0;
+  if (dst_row != nullptr && j >= ((len + 15) & ~15)) return;
+  uint4* dst = reinterpret_cast<uint4*>(out + (dst_row != nullptr ? dst_row[item] + j : row) * d);
   if (j >= len) {
     for (int32_t k = 0; k < d; k += 8) dst[k / 8] = make_uint4(0, 0, 0, 0);
     return;

@@ -17,7 +17,8 @@ Recipe (DESIGN.md "Input recipe"):
 * planted queries: query ``q`` copies tokens of a target chunk ``c*(q)`` and adds
   ``sigma_q * g(...)`` noise; ``c*(q) = h(qseed, QTARGET, q) % C`` or ``q`` (diagonal, for the
   in-batch ColTrast step where query i's positive is chunk i).
-* lengths: fixed, or ``1 + h(seed, LEN, c) % L`` (variable, for masking parity).
+* lengths: fixed, or ``1 + h(seed, LEN, c) % L`` (variable, for masking parity), or the
+  semantic-chunking recipe ``semantic_lengths`` (NEXT N4 workload).
 """
 from __future__ import annotations
 
@@ -26,7 +27,7 @@ import numpy as np
 M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 # stream ids
-TOK, CENT, TOPIC, TOPIC2, MIX, LEN, QTARGET, QPOS, QTOK, QLEN = range(1, 11)
+TOK, CENT, TOPIC, TOPIC2, MIX, LEN, QTARGET, QPOS, QTOK, QLEN, SEMLEN = range(1, 12)
 
 N_TOPICS = 4096
 SIGMA_TOKEN = np.float32(0.75)      # token noise around the topic centroid
@@ -77,6 +78,38 @@ def lengths(seed: int, n: int, max_len: int, variable: bool, start: int = 0,
         return np.full(n, max_len, dtype=np.int32)
     idx = np.arange(start, start + n, dtype=np.uint64)
     return (np.uint64(1) + h(seed, stream, idx) % np.uint64(max_len)).astype(np.int32)
+
+
+# Semantic-chunk lengths (NEXT N4 workload).  The paper's chunker keeps "adding to a segment as long
+# as the cosine similarity between consecutive sentences remains above a predetermined threshold"
+# (PAPER.md:274), so the sentence count of a chunk is 1 + Geometric: each next sentence joins with a
+# fixed probability P_CONT.  Sentence lengths are U[SENT_MIN, SENT_MAX] tokens; the encoder truncates
+# at max_len.  Paper silent on both numbers -- DESIGN.md records the reading (mean ~104 tokens).
+SEM_P_CONT = 0.75
+SEM_SENT_MIN, SEM_SENT_MAX = 12, 40
+SEM_MAX_SENT = 64
+
+
+def semantic_lengths(seed: int, n: int, max_len: int, start: int = 0) -> np.ndarray:
+    """int32 [n] chunk lengths of chunks start..start+n-1 (counter-based: any slice regenerates).
+
+    u_s = h(seed, SEMLEN, c*64 + s); sentence s has 12 + (u_s >> 16) % 29 tokens; sentence s+1 joins
+    iff (u_{s+1} & 0xFFFF) < 0.75 * 65536 (and every earlier one joined)."""
+    out = np.empty(n, dtype=np.int32)
+    thr = np.uint64(int(SEM_P_CONT * 65536))
+    span = np.uint64(SEM_SENT_MAX - SEM_SENT_MIN + 1)
+    for b0 in range(0, n, 1 << 16):
+        c = np.arange(start + b0, start + min(n, b0 + (1 << 16)), dtype=np.uint64)
+        s = np.arange(SEM_MAX_SENT, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            u = h(seed, SEMLEN, c.reshape(-1, 1) * np.uint64(SEM_MAX_SENT) + s.reshape(1, -1))
+        slen = (np.uint64(SEM_SENT_MIN) + (u >> np.uint64(16)) % span).astype(np.int64)
+        join = (u & np.uint64(0xFFFF)) < thr
+        join[:, 0] = True                                   # the first sentence always starts it
+        alive = np.cumprod(join, axis=1).astype(bool)       # stops at the first failed join
+        tot = (slen * alive).sum(axis=1)
+        out[b0:b0 + len(c)] = np.minimum(tot, max_len).astype(np.int32)
+    return out
 
 
 # ---------------------------------------------------------------- corpus
