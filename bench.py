@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 METRIC = "queries/s (exact MaxSim top-10, 3.6M chunks) at 1/2/4/8 B200; % bf16 TC peak"
 UNIT = "queries/s"
 FALLBACK_PEAK_SUSTAINED = 1400.0  # B200_PROFILING.md fallback (sustained under the power cap)
+FALLBACK_PEAK_BURST = 1590.0
 
 
 def parse():
@@ -39,11 +40,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["config3", "config4", "config5", "config2"],
+    ap.add_argument("--workload", choices=["config3", "config4", "config5", "config2", "config3v"],
                     default="config3",
                     help="config3 (default, N=1 headline): 1M x 256-token chunks, Q=1024, top-10; "
                          "config4: 3.6M chunks, top-100 (N>=2); config5: pooled 3.6M x 768, "
-                         "Q=4096, top-10; config2: ColTrast step B=256 scores + InfoNCE")
+                         "Q=4096, top-10; config2: ColTrast step B=256 scores + InfoNCE; "
+                         "config3v (NEXT N4): config3 with semantic-chunking lengths (<= 256) on "
+                         "the packed layout")
+    ap.add_argument("--no-pack", action="store_true",
+                    help="config3v: dense padded layout instead of HIPER_PACKED (the N4 ablation)")
     ap.add_argument("--chunks", type=int, default=None)
     ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
@@ -64,16 +69,26 @@ def parse():
         "config4": dict(chunks=3_600_000, queries=1024, k=100, chunk_len=256, query_len=32, dim=128),
         "config5": dict(chunks=3_600_000, queries=4096, k=10, chunk_len=1, query_len=1, dim=768),
         "config2": dict(chunks=256, queries=256, k=1, chunk_len=256, query_len=32, dim=128),
+        "config3v": dict(chunks=1_000_000, queries=1024, k=10, chunk_len=256, query_len=32, dim=128),
     }[a.workload]
     for key, v in defaults.items():
         if getattr(a, key) is None:
             setattr(a, key, v)
+    a.semantic = a.workload == "config3v"
+    a.packed = a.semantic and not a.no_pack
+    a.mean_len = a.chunk_len
+    if a.semantic:
+        from synth import gen
+        a.mean_len = float(gen.semantic_lengths(a.seed, min(a.chunks, 200_000), a.chunk_len).mean())
     return a
 
 
 def workload_config(a, world):
+    toks = (f"semantic-chunking lengths <= {a.chunk_len} tokens (mean {a.mean_len:.1f}), "
+            f"{'packed (HIPER_PACKED)' if a.packed else 'dense padded'} layout"
+            if a.semantic else f"{a.chunk_len} tokens")
     return {
-        "workload": (f"{a.workload}: {a.chunks} chunks x {a.chunk_len} tokens, dim {a.dim}, bf16, "
+        "workload": (f"{a.workload}: {a.chunks} chunks x {toks}, dim {a.dim}, bf16, "
                      f"query batch {a.queries} x {a.query_len} tokens, top-{a.k}"
                      + (" (pooled single-vector limit case)" if a.chunk_len == 1 else "")),
         "chunks": a.chunks, "chunk_len": a.chunk_len, "dim": a.dim, "query_batch": a.queries,
@@ -81,7 +96,7 @@ def workload_config(a, world):
         "parallelism": f"corpus-sharded x{world}, one ncclAllGather of top-k keys" if world > 1
         else "single GPU",
         "l2": "inputs larger than L2: the corpus (%.1f GB) is streamed every step, no flush needed"
-              % (a.chunks * a.chunk_len * a.dim * 2 / 1e9),
+              % (a.chunks * (a.mean_len if a.semantic else a.chunk_len) * a.dim * 2 / 1e9),
         "generator": f"synth planted-topic corpus seed {a.seed}, planted queries seed {a.qseed}",
     }
 
@@ -90,13 +105,20 @@ def flops_per_pair(a):
     return 2.0 * a.query_len * a.chunk_len * a.dim
 
 
-def load_peaks():
+def load_peaks(timed_s: float, clocks: dict | None):
+    """Roofline denominator (B200_PROFILING.md): the measured SUSTAINED cuBLAS bf16 figure for a kernel
+    timed inside a long, power-capped run; the measured BURST figure for one timed alone (short runs
+    that never reach the power cap).  Long = the timed region lasts > 1 s or saw sw_power_cap."""
+    long_run = timed_s > 1.0 or (clocks is not None and "sw_power_cap" in (clocks.get("reasons") or []))
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        if "bf16_tflops_sustained" in d:
-            return float(d["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained (measured)"
-    return FALLBACK_PEAK_SUSTAINED, "B200_PROFILING.md fallback, sustained"
+        key = "bf16_tflops_sustained" if long_run else "bf16_tflops"
+        if key in d:
+            return float(d[key]), f"MEASURED_PEAKS.json {key} (measured; {'long power-capped' if long_run else 'short'} timed region {timed_s:.2f} s)"
+    if long_run:
+        return FALLBACK_PEAK_SUSTAINED, "B200_PROFILING.md fallback, sustained"
+    return FALLBACK_PEAK_BURST, "B200_PROFILING.md fallback, burst"
 
 
 def ncu_traffic(a, world):
@@ -106,7 +128,8 @@ def ncu_traffic(a, world):
     if not os.path.exists(p):
         return None
     ent = json.load(open(p)).get("maxsim_sm100_kernel", {})
-    if ent.get("chunks_per_gpu") == a.chunks // world and ent.get("queries") == a.queries:
+    if (ent.get("workload", "config3") == a.workload and ent.get("chunks_per_gpu") == a.chunks // world
+            and ent.get("queries") == a.queries):
         return float(ent["dram_bytes_per_launch"])
     return None
 
@@ -177,14 +200,16 @@ def oracle_sample(a, n_chunks_sample, n_queries_sample=None):
         n_queries_sample = 256 if a.chunk_len == 1 else 4
     C_s = int(n_chunks_sample)
     corp = gen.corpus(a.seed, 0, C_s, a.chunk_len, a.dim)
+    clen = (gen.semantic_lengths(a.seed, C_s, a.chunk_len) if getattr(a, "semantic", False)
+            else np.full(C_s, a.chunk_len, np.int32))
     cn = oracle.norm_rows(corp)
     q = gen.queries(a.qseed, n_queries_sample, a.query_len, a.dim, corpus_seed=a.seed,
                     n_chunks=a.chunks, L=a.chunk_len)
     ids = np.arange(C_s, dtype=np.int64)
     t0 = time.perf_counter()
     qn = oracle.norm_rows(q)
-    S = oracle.maxsim_matrix(qn, np.full(n_queries_sample, a.query_len, np.int32), cn,
-                             np.full(C_s, a.chunk_len, np.int32), n_threads=cores)
+    S = oracle.maxsim_matrix(qn, np.full(n_queries_sample, a.query_len, np.int32), cn, clen,
+                             n_threads=cores)
     for r in range(n_queries_sample):
         oracle.topk(S[r], ids, a.k)
     dt = time.perf_counter() - t0
@@ -249,11 +274,23 @@ def run_ours(a, rank, local_rank, world):
     n_local = c1 - c0
     corpus = torch.empty((n_local, a.chunk_len, a.dim), dtype=torch.bfloat16, device="cuda")
     device.corpus_(corpus, a.seed, c0)
-    lens = np.full(n_local, a.chunk_len, np.int32)
-    idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_BORROW_TOKENS)
+    all_lens = None
+    if a.semantic:
+        all_lens = gen.semantic_lengths(a.seed, a.chunks, a.chunk_len)
+        lens = all_lens[c0:c1].copy()
+    else:
+        lens = np.full(n_local, a.chunk_len, np.int32)
+    if a.packed:  # N4: packed copy of the real rows, then the padded source is freed
+        idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_PACKED)
+        torch.cuda.synchronize()
+        del corpus
+        torch.cuda.empty_cache()
+    else:
+        idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_BORROW_TOKENS)
     comm = H.Comm() if world > 1 else None
     q = torch.empty((a.queries, a.query_len, a.dim), dtype=torch.bfloat16, device="cuda")
-    device.queries_(q, a.qseed, corpus_seed=a.seed, n_chunks=a.chunks, L=a.chunk_len)
+    device.queries_(q, a.qseed, corpus_seed=a.seed, n_chunks=a.chunks, L=a.chunk_len,
+                    chunk_lens=None if all_lens is None else torch.from_numpy(all_lens).cuda())
     qlen = np.full(a.queries, a.query_len, np.int32)
     ws = H.TopkWorkspace(idx, a.queries, a.k, comm)
     out = (torch.empty((a.queries, a.k), dtype=torch.float32, device="cuda"),
@@ -299,6 +336,10 @@ def run_ours(a, rank, local_rank, world):
     value = a.queries * a.steps / (ms / 1e3)
 
     # planted-target sanity (the planted target chunk must be the top-1 hit)
+    if a.packed:
+        line_pack = {"tiles": idx.n_tiles, "packed_rows": idx.n_rows,
+                     "tile_fill": idx.n_rows / max(1, 256 * idx.n_tiles),
+                     "rows_vs_dense": idx.n_rows / max(1, n_local * a.chunk_len)}
     tgt = torch.from_numpy(gen.query_targets(a.qseed, a.queries, a.chunks, False)).cuda()
     top1 = float((out[1][:, 0] == tgt).float().mean().item())
 
@@ -332,8 +373,10 @@ def run_ours(a, rank, local_rank, world):
             dist.destroy_process_group()
         return
 
-    peak, peak_src = load_peaks()
-    flops_launch = flops_per_pair(a) * a.queries * n_local
+    peak, peak_src = load_peaks(ms / 1e3, clk)
+    # algorithmic FLOPs: 2 * len_q * len_c * d per (query, chunk) pair over real tokens only
+    fpp = 2.0 * a.query_len * a.dim * (float(lens.mean()) if n_local else 0.0)
+    flops_launch = fpp * a.queries * n_local
     achieved = flops_launch / (kern_avg_ms / 1e3) / 1e12
     traffic = ncu_traffic(a, world)
     line = {
@@ -346,15 +389,17 @@ def run_ours(a, rank, local_rank, world):
                      "kernel": ("pooled_sm100_pair_kernel (fused TMA + tcgen05.mma cta_group::2 GEMM + per-query top-k)" if a.chunk_len == 1 else "maxsim_sm100_pair_kernel (fused TMA + tcgen05.mma cta_group::2 + masked max/sum + top-k)"),
                      "kernel_ms_per_launch": kern_avg_ms, "kernel_launches": kern_n,
                      "algorithmic_flops_per_launch": flops_launch,
-                     "flops_per_pair": flops_per_pair(a), "peak_source": peak_src,
+                     "flops_per_pair": fpp, "peak_source": peak_src,
                      "kernel_share_of_step": kern_avg_ms / (ms / a.steps)},
         "e2e": e2e,
         "gpu_launches": launches_per_step * a.steps,
         "clocks": clk,
         "extra": {"chunk_pairs_per_s": value * a.chunks,
-                  "tflops_step": flops_per_pair(a) * a.queries * a.chunks * a.steps / (ms / 1e3) / 1e12,
+                  "tflops_step": fpp * a.queries * a.chunks * a.steps / (ms / 1e3) / 1e12,
                   "top1_is_planted_target": top1, "launches_per_step": launches_per_step},
     }
+    if a.packed:
+        line["extra"]["packing"] = line_pack
     if world == 1 and not a.no_cpu_baseline:
         import oracle
         oracle.build()
@@ -477,7 +522,7 @@ def run_coltrast(a, rank, local_rank, world):
             dist.destroy_process_group()
         return
     flops = 2.0 * B * B * Lq * L * d
-    peak, peak_src = load_peaks()
+    peak, peak_src = load_peaks(ms / 1e3, clk)
     value = world * steps / (ms / 1e3)
     line = {
         "metric": ("ColTrast in-batch MaxSim scores + InfoNCE + backward (N1) steps/s (B=256, configs[1])"
