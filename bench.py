@@ -109,7 +109,9 @@ def load_peaks(timed_s: float, clocks: dict | None):
     """Roofline denominator (B200_PROFILING.md): the measured SUSTAINED cuBLAS bf16 figure for a kernel
     timed inside a long, power-capped run; the measured BURST figure for one timed alone (short runs
     that never reach the power cap).  Long = the timed region lasts > 1 s or saw sw_power_cap."""
-    long_run = timed_s > 1.0 or (clocks is not None and "sw_power_cap" in (clocks.get("reasons") or []))
+    capped = (clocks is not None and "sw_power_cap" in (clocks.get("reasons") or [])
+              and (clocks.get("sm_mhz") or 0) < 0.97 * (clocks.get("sm_max_mhz") or 1))
+    long_run = timed_s > 1.0 or capped
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))

@@ -194,6 +194,22 @@ static bool is_device_ptr(const void* p) {
 }
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size): it is a
+// synchronous driver call that otherwise costs microseconds on every launch of a short step.
+static cudaError_t set_max_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& d : done)
+    if (d.first.first == dev && d.first.second == fn && d.second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back({{dev, fn}, bytes});
+  return e;
+}
 static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 static bool use_pair_kernel();
@@ -212,7 +228,8 @@ struct hiper_index_s {
   // packed layout (HIPER_PACKED, N4): tok is bf16 [n_rows][dim]; tiles/ents as in MaxsimArgs
   bool packed = false;
   int64_t n_tiles = 0, n_rows = 0;
-  int4* tiles = nullptr;  // device [n_tiles]
+  int4* tiles = nullptr;     // device [n_tiles]: the plan's tiles (hiper_pack_plan layout)
+  uint32_t* recs = nullptr;  // device [n_tiles][32]: kernel tile records (tile_records)
   int2* ents = nullptr;   // device [n]
 };
 
@@ -256,6 +273,41 @@ static hiper_status pack_plan(const int32_t* lens, int64_t n, std::vector<int4>&
     rows += used;
   }
   return HIPER_OK;
+}
+
+// Kernel-side tile records (not part of hiper_pack_plan's ABI): one 128-B record per tile, so the
+// kernel reads everything it needs about a tile with ONE coalesced warp load (lane i <- word i):
+//   w0 = n_rows | n_ent << 16, w1 = start mask (bit g: a chunk begins at column group g; also set
+//   for every group past n_rows, so no chunk's suffix max reaches them),
+//   w2/w3 = 4 bits per column group of 16 = real columns - 1, w4 = row0, w5 = tail mask (groups with
+//   padding columns), w16 + e = chunk of slot e.
+static constexpr int kTileRecWords = 32;
+static std::vector<uint32_t> tile_records(const std::vector<int4>& tiles, const std::vector<int2>& ents) {
+  std::vector<uint32_t> rec(tiles.size() * kTileRecWords, 0u);
+  for (size_t t = 0; t < tiles.size(); ++t) {
+    uint32_t* r = rec.data() + t * kTileRecWords;
+    uint64_t vcw = 0;
+    uint32_t start = 0, tail = 0;
+    for (int32_t e = tiles[t].z; e < tiles[t].w; ++e) {
+      const int32_t col = ents[e].y >> 16, len = ents[e].y & 0xFFFF;
+      const int32_t g0 = col / 16, ng = (len + 15) / 16;
+      start |= 1u << g0;
+      for (int32_t j = 0; j < ng; ++j) {
+        const int32_t vc = (j == ng - 1) ? len - 16 * j : 16;
+        vcw |= (uint64_t)(vc - 1) << (4 * (g0 + j));
+        if (vc < 16) tail |= 1u << (g0 + j);
+      }
+      r[16 + (e - tiles[t].z)] = (uint32_t)ents[e].x;
+    }
+    r[0] = (uint32_t)tiles[t].y | ((uint32_t)(tiles[t].w - tiles[t].z) << 16);
+    r[1] = start | (0xFFFFu & ~((1u << (tiles[t].y / 16)) - 1u));  // groups past n_rows: own "chunks"
+
+    r[2] = (uint32_t)vcw;
+    r[3] = (uint32_t)(vcw >> 32);
+    r[4] = (uint32_t)tiles[t].x;
+    r[5] = tail;
+  }
+  return rec;
 }
 
 extern "C" hiper_status hiper_pack_plan(const int32_t* lens, int64_t n, int32_t* tiles_out,
@@ -310,6 +362,31 @@ static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src
     norm_layout_kernel<__nv_bfloat16><<<(unsigned)blocks, threads, 0, stream>>>(
         (const __nv_bfloat16*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out,
         status, dst_row);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return HIPER_OK;
+}
+
+// Query and document layouts of one ColTrast step in a single launch (norm_layout2_kernel).
+static hiper_status launch_norm2(const void* in_a, int64_t n_a, int32_t in_rows_a, const int32_t* lens_a,
+                                 int64_t items_a, int32_t out_rows_a, __nv_bfloat16* out_a,
+                                 const void* in_b, int64_t n_b, int32_t in_rows_b, const int32_t* lens_b,
+                                 int64_t items_b, int32_t out_rows_b, __nv_bfloat16* out_b,
+                                 hiper_dtype dtype, int32_t dim, uint32_t flags, uint32_t* status,
+                                 cudaStream_t stream) {
+  const int threads = 256;
+  const int64_t ba = (items_a * out_rows_a + threads - 1) / threads;
+  const int64_t bb = (items_b * out_rows_b + threads - 1) / threads;
+  if (ba + bb == 0) return HIPER_OK;
+  if (ba + bb > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
+  const NormSeg a{in_a, n_a, in_rows_a, lens_a, items_a, out_rows_a, out_a};
+  const NormSeg b{in_b, n_b, in_rows_b, lens_b, items_b, out_rows_b, out_b};
+  const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
+  const uint32_t cf = (flags & HIPER_CHECK_FINITE) ? 1u : 0u;
+  if (dtype == HIPER_F32)
+    norm_layout2_kernel<float><<<(unsigned)(ba + bb), threads, 0, stream>>>(a, b, ba, dim, an, cf, status);
+  else
+    norm_layout2_kernel<__nv_bfloat16><<<(unsigned)(ba + bb), threads, 0, stream>>>(a, b, ba, dim, an, cf, status);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return HIPER_OK;
@@ -380,6 +457,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     if (ix->owns_tok && ix->tok) cudaFree(ix->tok);
     if (ix->lens) cudaFree(ix->lens);
     if (ix->tiles) cudaFree(ix->tiles);
+    if (ix->recs) cudaFree(ix->recs);
     if (ix->ents) cudaFree(ix->ents);
     if (dst_dev) cudaFree(dst_dev);
     delete ix;
@@ -397,6 +475,10 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     if (cudaMalloc(&ix->tok, (size_t)std::max<int64_t>(p_rows, 1) * dim * 2) != cudaSuccess)
       return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "packed layout alloc %lld bytes", (long long)p_rows * dim * 2));
     ix->owns_tok = true;
+    const std::vector<uint32_t> p_rec = tile_records(p_tiles, p_ents);
+    if (cudaMalloc(&ix->recs, std::max<size_t>(p_rec.size(), 1) * sizeof(uint32_t)) != cudaSuccess ||
+        (n > 0 && cudaMemcpyAsync(ix->recs, p_rec.data(), p_rec.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, stream) != cudaSuccess))
+      return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "tile records"));
     if (cudaMalloc(&ix->tiles, std::max<size_t>(p_tiles.size(), 1) * sizeof(int4)) != cudaSuccess ||
         cudaMalloc(&ix->ents, std::max<size_t>(p_ents.size(), 1) * sizeof(int2)) != cudaSuccess ||
         cudaMalloc(&dst_dev, std::max<size_t>(p_dst.size(), 1) * sizeof(int64_t)) != cudaSuccess)
@@ -457,6 +539,7 @@ extern "C" hiper_status hiper_index_destroy(hiper_index* ix) {
   if (ix->owns_tok && ix->tok) cudaFree(ix->tok);
   if (ix->lens) cudaFree(ix->lens);
   if (ix->tiles) cudaFree(ix->tiles);
+  if (ix->recs) cudaFree(ix->recs);
   if (ix->ents) cudaFree(ix->ents);
   delete ix;
   return HIPER_OK;
@@ -671,7 +754,7 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     auto kern = maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED>;
     if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1>;
     if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
+    CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)kp.grid);
     cfg.blockDim = dim3(kMaxsimThreads);
@@ -684,11 +767,30 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
+    unsigned long long* st = nullptr;
+    MaxsimArgs b = a;
+    if (stats_on) {
+      CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
+      CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
+      b.stats = st;
+    }
     TRY(profile_begin(stream, &ev, &rec));
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, td, a));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, td, b));
+    if (st) {
+      unsigned long long h[8];
+      CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaStreamSynchronize(stream));
+      cudaFree(st);
+      const double pairs = kp.grid / 2.0, ep = 8.0 * kp.grid;
+      fprintf(stderr, "[hiper pipe] maxsim%s: MMA thread %.0f cyc avg; waits acc %.1f%% full %.1f%%; "
+              "epilogue drain %.0f cyc/tile, wait %.0f cyc/tile, tiles/warp %.0f\n",
+              PACKED ? " (packed)" : "", h[2] / pairs, 100.0 * h[0] / h[2], 100.0 * h[1] / h[2],
+              (double)h[3] / h[5], (double)h[4] / h[5], h[5] / ep);
+    }
   } else {
     auto kern = maxsim_sm100_kernel<MODE, KR>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kp.smem_bytes));
+    CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
     TRY(profile_begin(stream, &ev, &rec));
     kern<<<kp.grid, kMaxsimThreads, kp.smem_bytes, stream>>>(tq, td, a);
   }
@@ -701,7 +803,7 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
 static hiper_status launch_maxsim(int mode, int k, const KernelPlan& kp, const CUtensorMap& tq,
                                   const CUtensorMap& td, const MaxsimArgs& a, cudaStream_t stream) {
   if (kp.grid == 0) return HIPER_OK;
-  if (a.tiles != nullptr) {  // packed corpus (N4)
+  if (a.recs != nullptr) {  // packed corpus (N4)
     if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "a packed index needs the CTA-pair kernel");
     if (mode == 0) return launch_maxsim_t<0, 1, true>(kp, tq, td, a, stream);
     if (mode != 1) return fail(HIPER_ERR_UNSUPPORTED, "argmax capture on a packed index");
@@ -826,8 +928,7 @@ static int64_t index_slots(const hiper_index* ix) { return ix->packed ? ix->n_ti
 static int32_t index_slot_rows(const hiper_index* ix) { return ix->packed ? kTileRows : ix->ld_pad; }
 static void set_packed_args(const hiper_index* ix, MaxsimArgs& a) {
   if (!ix->packed) return;
-  a.tiles = ix->tiles;
-  a.ents = ix->ents;
+  a.recs = ix->recs;
 }
 
 static hiper_status check_ws(const void* ws, size_t have, size_t need) {
@@ -879,8 +980,11 @@ static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks
   const int64_t ct = (n_chunks + 255) / 256;
   if (ct > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many chunks");
   pp.n_ctiles = (int32_t)ct;
-  const int pairs = di.num_sms / 2;
-  pp.n_parts = choose_parts(pp.n_qtiles, pp.n_ctiles, pairs);
+  int pairs = di.num_sms / 2;
+  // ablation only: fewer resident pairs (the per-SM vs chip-wide L2->SMEM throughput experiment);
+  // must keep choose_parts() equal to the workspace sizing (it does for divisors of num_sms / 2)
+  if (const char* e = getenv("HIPER_POOLED_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));
+  pp.n_parts = choose_parts(pp.n_qtiles, pp.n_ctiles, di.num_sms / 2);
   const uint32_t fixed = 1024u + 512u;  // align slack, barriers
   pp.n_stages = (int32_t)std::min<uint32_t>(8u, ((uint32_t)di.max_smem - fixed) / pp.stage_bytes);
   if (pp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory");
@@ -893,8 +997,12 @@ template <int MODE>
 static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, const CUtensorMap& tc,
                                   const PooledArgs& a, cudaStream_t stream) {
   if (pp.grid == 0 || pp.n_parts == 0) return HIPER_OK;
-  auto kern = pooled_sm100_pair_kernel<MODE, kPooledKP>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem_bytes));
+  auto kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
+  if (MODE == 1 && debug_mode() == 1) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 1>;
+  if (MODE == 1 && debug_mode() == 2) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 2>;
+  if (MODE == 1 && debug_mode() == 3) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 3>;
+  if (MODE == 1 && debug_mode() == 4) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 4>;
+  CUDA_TRY(set_max_smem((const void*)kern, (int)pp.smem_bytes));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)pp.grid);
   cfg.blockDim = dim3(kMaxsimThreads);
@@ -909,16 +1017,37 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   cfg.numAttrs = 1;
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   bool rec = false;
+  // diagnostics only (HIPER_PIPE_STATS=1): pipeline wait/drain cycle counters, printed to stderr
+  static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
+  unsigned long long* st = nullptr;
+  PooledArgs b = a;
+  if (stats_on) {
+    CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
+    b.stats = st;
+  }
   TRY(profile_begin(stream, &ev, &rec));
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, tc, a));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, tc, b));
   TRY(profile_end(stream, ev, rec));
   ++g_launches;
+  if (st) {
+    unsigned long long h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    cudaFree(st);
+    const double pairs = pp.grid / 2.0, ep = 8.0 * pp.grid;  // MMA threads, epilogue warps
+    fprintf(stderr, "[hiper pipe] pooled: MMA thread %.0f cyc avg; waits acc %.1f%% full %.1f%%; "
+            "epilogue drain %.0f cyc/tile, wait %.0f cyc/tile, tiles/warp %.0f; per thread-tile: "
+            "blocks past the threshold %.3f, inserts %.3f\n",
+            h[2] / pairs, 100.0 * h[0] / h[2], 100.0 * h[1] / h[2], (double)h[3] / h[5],
+            (double)h[4] / h[5], h[5] / ep, (double)h[6] / (32.0 * h[5]), (double)h[7] / (32.0 * h[5]));
+  }
   return HIPER_OK;
 }
 
 struct PooledWs {
   size_t status = 0, progress = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0,
-         total = 0;
+         gthr = 0, total = 0;
 };
 static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t q_pad, int32_t k,
                              int32_t world, bool with_comm, PooledWs& w) {
@@ -937,6 +1066,8 @@ static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t 
   if (with_comm) off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
   w.gathered = off;
   if (with_comm) off = align_up(off + (size_t)world * std::max(n_q, 1) * k * 8, 256);
+  w.gthr = off;
+  off = align_up(off + (size_t)q_pad * 8, 256);
   w.total = off;
 }
 
@@ -982,6 +1113,10 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   a.score_ld = ix->n;
   a.progress = getenv("HIPER_NO_LOCKSTEP") == nullptr ? (uint32_t*)(ws + w.progress) : nullptr;
   a.window = 16;
+  if (!dense_scores && getenv("HIPER_NO_SHARED_BOUND") == nullptr) {
+    a.gthr = (unsigned long long*)(ws + w.gthr);
+    CUDA_TRY(cudaMemsetAsync(a.gthr, 0, (size_t)pp.q_pad * 8, stream));
+  }
   if (ix->n > 0) {
     alignas(64) CUtensorMap tq;
     TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
@@ -1170,19 +1305,24 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
 
 // ============================================================================ ColTrast scores + loss
 struct ColtrastWs {
-  size_t status = 0, qlens = 0, dlens = 0, pos = 0, qlayout = 0, dlayout = 0, scores = 0, total = 0;
+  size_t status = 0, qlens = 0, dlens = 0, pos = 0, rowloss = 0, qlayout = 0, dlayout = 0, scores = 0,
+         total = 0;
 };
+static constexpr size_t kLossCounterOff = 4;  // u32 completion counter of the loss kernel (zeroed with status)
+// The small host-fed region [status | qlens | dlens | pos] is contiguous so one staged copy fills it.
 static void coltrast_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim, ColtrastWs& w) {
   const int32_t ld_pad = (int32_t)round_up(std::max(d_max_len, 1), 16);
   size_t off = 0;
   w.status = off;
-  off += 256;
+  off += 16;
   w.qlens = off;
-  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 256);
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 16);
   w.dlens = off;
-  off = align_up(off + (size_t)std::max(n_d, 1) * 4, 256);
+  off = align_up(off + (size_t)std::max(n_d, 1) * 4, 16);
   w.pos = off;
-  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
+  off = align_up(off + (size_t)std::max(n_q, 1) * 4, 256);
+  w.rowloss = off;
+  off = align_up(off + (size_t)std::max(n_q, 1) * 8, 1024);
   w.qlayout = off;
   off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
   w.dlayout = off;
@@ -1192,6 +1332,19 @@ static void coltrast_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int3
   w.total = off;
 }
 
+// One staged H2D copy fills the small region of a ColTrast workspace: status = 0, query / doc
+// lengths, positives (replaces a memset and up to three copies per step).
+static hiper_status stage_small(const ColtrastWs& w, uint8_t* ws, const int32_t* q_lens, int32_t n_q,
+                                const int32_t* d_lens, int32_t n_d, const int32_t* pos_idx,
+                                cudaStream_t stream) {
+  thread_local std::vector<uint8_t> host;
+  host.assign(w.pos + (size_t)n_q * 4, 0);
+  memcpy(host.data() + w.qlens, q_lens, (size_t)n_q * 4);
+  memcpy(host.data() + w.dlens, d_lens, (size_t)n_d * 4);
+  if (pos_idx) memcpy(host.data() + w.pos, pos_idx, (size_t)n_q * 4);
+  return stage_h2d(ws + w.status, host.data(), pos_idx ? host.size() : w.pos, stream);
+}
+
 extern "C" size_t hiper_coltrast_workspace_size(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim) {
   if (n_q < 0 || n_d < 0 || dim <= 0) return 0;
   ColtrastWs w;
@@ -1199,12 +1352,19 @@ extern "C" size_t hiper_coltrast_workspace_size(int32_t n_q, int32_t n_d, int32_
   return w.total;
 }
 
+// rows/counter (optional): the row-parallel kernel's scratch ([n_q] fp64, one zeroed u32 counter);
+// without them one 1024-thread block does everything.
 static hiper_status launch_loss(const float* S, int32_t n_q, int32_t n_d, int64_t ld,
                                 const int32_t* pos_dev, float tau, float* out_loss,
                                 cudaStream_t stream, const float* combine_with = nullptr,
-                                float* out_combined = nullptr) {
-  infonce_loss_kernel<<<1, 1024, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, out_loss, combine_with,
-                                              out_combined);
+                                float* out_combined = nullptr, double* rows = nullptr,
+                                uint32_t* counter = nullptr) {
+  if (rows != nullptr && counter != nullptr && combine_with == nullptr)
+    infonce_rows_kernel<<<(n_q + 7) / 8, 256, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, rows,
+                                                            counter, out_loss);
+  else
+    infonce_loss_kernel<<<1, 1024, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, out_loss, combine_with,
+                                                out_combined);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return HIPER_OK;
@@ -1259,11 +1419,9 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
   __nv_bfloat16* dlayout = (__nv_bfloat16*)(ws + w.dlayout);
   float* S = out_scores ? out_scores : (float*)(ws + w.scores);
 
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
-  TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
-  TRY(stage_h2d(dlens_dev, d_lens, (size_t)n_d * 4, stream));
-  TRY(launch_norm(d_tokens, dtype, n_d, d_max_len, dlens_dev, n_d, ld_pad, dim, flags, dlayout, status, stream));
-  if (pos_idx) TRY(stage_h2d(pos_dev, pos_idx, (size_t)n_q * 4, stream));
+  TRY(stage_small(w, ws, q_lens, n_q, d_lens, n_d, pos_idx, stream));
+  TRY(launch_norm2(q_tokens, n_q, q_max_len, qlens_dev, n_q_pad_of(n_q), kQSlot, qlayout, d_tokens, n_d,
+                   d_max_len, dlens_dev, n_d, ld_pad, dlayout, dtype, dim, flags, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
 
   alignas(64) CUtensorMap tq, td;
@@ -1286,7 +1444,8 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
   a.scores = S;
   a.score_ld = n_d;
   TRY(launch_maxsim(0, 1, kp, tq, td, a, stream));
-  return launch_loss(S, n_q, n_d, n_d, pos_idx ? pos_dev : nullptr, temperature, out_loss, stream);
+  return launch_loss(S, n_q, n_d, n_d, pos_idx ? pos_dev : nullptr, temperature, out_loss, stream,
+                     nullptr, nullptr, (double*)(ws + w.rowloss), (uint32_t*)(ws + w.status + kLossCounterOff));
 }
 
 
@@ -1495,11 +1654,9 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   uint8_t* amax = ws + w.amax;
   float* G = (float*)(ws + w.G);
 
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
-  TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
-  TRY(stage_h2d(dlens_dev, d_lens, (size_t)n_d * 4, stream));
-  TRY(launch_norm(d_tokens, dtype, n_d, d_max_len, dlens_dev, n_d, ld_pad, dim, flags, dlayout, status, stream));
-  if (pos_idx) TRY(stage_h2d(pos_dev, pos_idx, (size_t)n_q * 4, stream));
+  TRY(stage_small(c, ws, q_lens, n_q, d_lens, n_d, pos_idx, stream));
+  TRY(launch_norm2(q_tokens, n_q, q_max_len, qlens_dev, n_q_pad_of(n_q), kQSlot, qlayout, d_tokens, n_d,
+                   d_max_len, dlens_dev, n_d, ld_pad, dlayout, dtype, dim, flags, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
   alignas(64) CUtensorMap tq, td;
   TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
@@ -1522,7 +1679,8 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   a.amax = amax;
   TRY(launch_maxsim(2, 1, kp, tq, td, a, stream));                       // S + argmax (a3-a5)
   const int32_t* pd = pos_idx ? pos_dev : nullptr;
-  TRY(launch_loss(S, n_q, n_d, n_d, pd, temperature, out_loss, stream));  // a11
+  TRY(launch_loss(S, n_q, n_d, n_d, pd, temperature, out_loss, stream, nullptr, nullptr,
+                  (double*)(ws + c.rowloss), (uint32_t*)(ws + c.status + kLossCounterOff)));  // a11
   infonce_grad_kernel<<<(n_q + 7) / 8, 256, 0, stream>>>(S, n_q, n_d, n_d, pd, temperature, G);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
@@ -1538,7 +1696,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
                                                          an, grad_q);
     CUDA_TRY(cudaGetLastError());
     auto gk = grad_d_kernel<VPL, Tin>;
-    CUDA_TRY(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
+    CUDA_TRY(set_max_smem((const void*)gk, (int)dsmem));
     gk<<<n_d, 256, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
                                           (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d);
     CUDA_TRY(cudaGetLastError());

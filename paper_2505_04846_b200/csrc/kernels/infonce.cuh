@@ -13,6 +13,56 @@
 
 namespace hiper {
 
+// l_i of one row (one warp; fixed-order lane partials and butterflies).
+__device__ __forceinline__ float infonce_row(const float* __restrict__ row, int32_t M, int32_t p,
+                                             float tau, uint32_t lane) {
+  float mx = -INFINITY;
+  for (int32_t j = lane; j < M; j += 32) mx = fmaxf(mx, __fdiv_rn(row[j], tau));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float zp = __fdiv_rn(row[p], tau);
+  float r = 0.0f;
+  for (int32_t j = lane; j < M; j += 32)
+    if (j != p) r += expf(__fdiv_rn(row[j], tau) - mx);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return (mx == zp) ? log1pf(r) : (mx - zp) + logf(expf(zp - mx) + r);
+}
+
+// Row-parallel form (the ColTrast step): one warp per row over ceil(B/8) blocks; each row's l_i goes to
+// rowloss[i]; the last block to finish (completion counter, zeroed by the caller, reset here) sums
+// rowloss in index order in fp64 -> L.  Deterministic: the order depends on nothing but B.
+__global__ void __launch_bounds__(256) infonce_rows_kernel(const float* __restrict__ S, int32_t B,
+                                                           int32_t M, int64_t ld,
+                                                           const int32_t* __restrict__ pos, float tau,
+                                                           double* __restrict__ rowloss,
+                                                           uint32_t* counter, float* __restrict__ out_loss) {
+  __shared__ double part[256];
+  __shared__ bool last;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t i = (int32_t)blockIdx.x * 8 + (int32_t)warp;
+  if (i < B) {
+    const float li = infonce_row(S + (int64_t)i * ld, M, pos ? pos[i] : i, tau, lane);
+    if (lane == 0) rowloss[i] = (double)li;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a = 0.0;
+  for (int32_t r = threadIdx.x; r < B; r += blockDim.x) a += __ldcg(rowloss + r);
+  part[threadIdx.x] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (uint32_t w = 0; w < blockDim.x; ++w) t += part[w];
+    *out_loss = (float)(t / (double)B);
+    *counter = 0u;
+  }
+}
+
 __global__ void __launch_bounds__(1024) infonce_loss_kernel(const float* __restrict__ S, int32_t B,
                                                             int32_t M, int64_t ld,
                                                             const int32_t* __restrict__ pos,
@@ -24,20 +74,7 @@ __global__ void __launch_bounds__(1024) infonce_loss_kernel(const float* __restr
   const uint32_t n_warps = blockDim.x >> 5;
   double acc = 0.0;
   for (int32_t i = warp; i < B; i += n_warps) {
-    const float* row = S + (int64_t)i * ld;
-    const int32_t p = pos ? pos[i] : i;
-    float mx = -INFINITY;
-    for (int32_t j = lane; j < M; j += 32) mx = fmaxf(mx, __fdiv_rn(row[j], tau));
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float zp = __fdiv_rn(row[p], tau);
-    float r = 0.0f;
-    for (int32_t j = lane; j < M; j += 32)
-      if (j != p) r += expf(__fdiv_rn(row[j], tau) - mx);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    const float li = (mx == zp) ? log1pf(r) : (mx - zp) + logf(expf(zp - mx) + r);
-    acc += (double)li;
+    acc += (double)infonce_row(S + (int64_t)i * ld, M, pos ? pos[i] : i, tau, lane);
   }
   if (lane == 0) warp_sum[warp] = acc;
   __syncthreads();

@@ -53,12 +53,14 @@ struct MaxsimArgs {
   const int32_t* cand;    // rerank (N3): [G][n_chunks] chunk index per slot of each row group
                           // (-1 = empty slot), or nullptr = the corpus itself
   int32_t window;         // chunks a pair may run ahead of the slowest pair (lockstep window)
-  // packed layout (N4, PACKED kernels): slot c of the kernel is tile c, not chunk c.
-  //   tiles[c] = {row0, n_rows, e0, e1}: n_rows (multiple of 16, <= 256) packed token rows starting
-  //              at row0 hold the chunks of entries [e0, e1);
-  //   ents[e]  = {chunk index, (col << 16) | len}: the chunk's tokens are tile columns [col, col+len).
-  const int4* tiles;
-  const int2* ents;
+  // packed layout (N4, PACKED kernels): slot c of the kernel is tile c of a length-bucketed packed
+  // corpus, described by a 128-B record recs[c][0..32): w0 = n_rows | n_ent << 16 (n_rows a multiple
+  // of 16, <= 256; n_ent <= 16 chunks), w1 = start mask (bit g: a chunk begins at column group g of
+  // 16), w2/w3 = 4 bits per column group = real columns - 1, w4 = first packed row, w5 = tail mask
+  // (groups holding padding columns), w16 + e = chunk
+  // index of slot e (slots in column order).
+  const uint32_t* recs;
+  unsigned long long* stats;  // HIPER_PIPE_STATS diagnostics (see pooled_sm100_pair.cuh), or nullptr
 };
 
 // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare; warps 4-7 = epilogue warpgroup 0 (accumulator 0, even

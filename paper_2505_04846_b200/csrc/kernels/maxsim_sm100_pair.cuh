@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   auto bar_tfull = [&](int b) { return sBar + 8u * (2 * S + 4 + b); };
   auto bar_tempty = [&](int b) { return sBar + 8u * (2 * S + 6 + b); };
   const uint32_t sTmemPtr = sBar + 8u * (2 * S + 8);
+  const uint32_t sMeta = sTmemPtr + 16u;  // [S] u32: MMA N per stage (packed corpus)
   uint32_t* tmem_ptr_generic =
       reinterpret_cast<uint32_t*>(smem_raw + (sTmemPtr - smem_u32(smem_raw)));
 
@@ -114,20 +115,26 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr_generic);
 
   const int32_t n_units = args.n_groups * args.n_parts;  // n_groups = row-group pairs (8 queries)
+  long long st_drain_g = 0, st_ewait_g = 0, st_tiles_g = 0;  // HIPER_PIPE_STATS (epilogue warps)
   const int32_t half_rows = args.ld_pad >> 1;
   const uint32_t half_tile = (uint32_t)half_rows * 128u;  // one 64-dim K-block of this CTA's half chunk
 
   if (warp == kPairProducerWarp) {
     // ================= TMA producer (both CTAs) =================
+    // The whole warp walks the units; lane 0 waits on barriers and issues the TMA.  For a packed
+    // corpus the warp loads the tile descriptors 32 at a time, one batch ahead, so no dependent
+    // global load sits between two stages (a miss costs ~1 us, about two tiles of MMA work).
     if (lane == 0) {
       prefetch_tmap(&tmap_q);
       prefetch_tmap(&tmap_d);
-      int s = 0;
-      uint32_t ph = 0, it = 0;
-      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
-        int32_t g, p;
-        int64_t c0, c1;
-        unit_decode(args, u, g, p, c0, c1);
+    }
+    int s = 0;
+    uint32_t ph = 0, it = 0;
+    for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
+      int32_t g, p;
+      int64_t c0, c1;
+      unit_decode(args, u, g, p, c0, c1);
+      if (lane == 0) {
         const uint32_t ab = it & 1u, aph = (it >> 1) & 1u;
         mbar_wait(bar_aempty(ab), aph ^ 1u);
         if (rank == 0) mbar_arrive_expect_tx(bar_afull(ab), 2u * args.a_bytes);
@@ -135,7 +142,33 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         for (int kb = 0; kb < args.num_kb; ++kb)
           tma_load_2d_pair(sA + ab * args.a_bytes + kb * 16384u, &tmap_q, afull_leader, kb * 64,
                            (int32_t)((2 * g + (int32_t)rank) * 128));
-        for (int64_t c = c0; c < c1; ++c) {
+      }
+      int2 cur = make_int2(0, 0), nxt = make_int2(0, 0);
+      auto load_batch = [&](int64_t cb) {  // lane i: (row0, n_rows) of tile cb + i
+        const int64_t ci = cb + lane;
+        if (ci < c1) {
+          const uint32_t* r = args.recs + ci * 32;
+          return make_int2((int32_t)__ldg(r + 4), (int32_t)(__ldg(r) & 0xFFFFu));
+        }
+        return make_int2(0, 0);
+      };
+      if constexpr (PACKED) nxt = load_batch(c0);
+      for (int64_t c = c0; c < c1; ++c) {
+        int32_t brow;
+        uint32_t nrows = (uint32_t)args.ld_pad;
+        if constexpr (PACKED) {
+          const int j = (int)((c - c0) & 31);
+          if (j == 0) {
+            cur = nxt;
+            nxt = load_batch(c + 32);
+          }
+          brow = __shfl_sync(0xffffffffu, cur.x, j);
+          nrows = (uint32_t)__shfl_sync(0xffffffffu, cur.y, j);
+          brow += (int32_t)rank * (int32_t)(nrows >> 1);
+        } else {
+          brow = (int32_t)(slot_chunk(args, g, c) * args.ld_pad + (int64_t)rank * half_rows);
+        }
+        if (lane == 0) {
           if (args.progress != nullptr && rank == 0 && ((c - c0) & 15) == 0) {
             const int64_t off = c - c0 < 0xFFFFF ? c - c0 : 0xFFFFF;
             const uint32_t pos = (it << 20) | (uint32_t)off;
@@ -144,29 +177,22 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           }
           // one stage = this CTA's half of one whole chunk (all dim/64 K-blocks)
           mbar_wait(bar_empty(s), ph ^ 1u);
+          if constexpr (PACKED) st_shared_u32(sMeta + 4u * s, nrows);  // MMA N of this stage
           if (DBG == 2 && (c > c0 || it > 0)) {
             if (rank == 0) mbar_arrive(bar_full(s));
           } else {
             if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
             const uint32_t full_leader = mapa_shared(bar_full(s), 0);
-            {
-              int32_t brow;
-              if constexpr (PACKED) {
-                const int4 tl = __ldg(args.tiles + c);
-                brow = tl.x + (int32_t)rank * (tl.y >> 1);
-              } else {
-                brow = (int32_t)(slot_chunk(args, g, c) * args.ld_pad + (int64_t)rank * half_rows);
-              }
-              for (int kb = 0; kb < args.num_kb; ++kb)
-                tma_load_2d_pair(sB + s * args.stage_bytes + kb * half_tile, &tmap_d, full_leader,
-                                 kb * 64, brow);
-            }
+            for (int kb = 0; kb < args.num_kb; ++kb)
+              tma_load_2d_pair(sB + s * args.stage_bytes + kb * half_tile, &tmap_d, full_leader,
+                               kb * 64, brow);
           }
-          if (++s == S) { s = 0; ph ^= 1u; }
         }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1u; }
       }
-      if (args.progress != nullptr && rank == 0) lockstep_publish(args.progress, pair, 0xFFFFFFFFu);
     }
+    if (lane == 0 && args.progress != nullptr && rank == 0) lockstep_publish(args.progress, pair, 0xFFFFFFFFu);
   } else if (warp == kPairMmaWarp) {
     // ================= MMA issuer: leader CTA, single thread =================
     // (highest warp id: the SMSP arbiter favours it over the epilogue warps sharing its SMSP)
@@ -174,6 +200,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       const uint32_t idesc = idesc_bf16_f32(256, (uint32_t)args.ld_pad);
       int s = 0;
       uint32_t ph = 0, it = 0, t = 0;
+      long long st_acc = 0, st_full = 0;
+      const long long st_t0 = clock64();
       for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
         int32_t g, p;
         int64_t c0, c1;
@@ -182,19 +210,22 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         mbar_wait(bar_afull(ab), aph);
         tc_fence_after();
         const uint32_t a_tile = sA + ab * args.a_bytes;
-        int32_t nr_next = (PACKED && c0 < c1) ? __ldg(&args.tiles[c0].y) : 0;
         for (int64_t c = c0; c < c1; ++c, ++t) {
-          uint32_t idesc_c = idesc;
-          if constexpr (PACKED) {  // MMA N = this tile's packed rows (multiple of 16)
-            idesc_c = idesc_bf16_f32(256, (uint32_t)nr_next);
-            if (c + 1 < c1) nr_next = __ldg(&args.tiles[c + 1].y);
-          }
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
+          long long w0 = args.stats ? clock64() : 0;
           mbar_wait(bar_tempty(acc), tph ^ 1u);
+          if (args.stats) {
+            st_acc += clock64() - w0;
+            w0 = clock64();
+          }
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
           mbar_wait(bar_full(s), ph);
+          if (args.stats) st_full += clock64() - w0;
           tc_fence_after();
+          uint32_t idesc_c = idesc;
+          if constexpr (PACKED)  // MMA N = this tile's packed rows (written by the producer)
+            idesc_c = idesc_bf16_f32(256, ld_shared_u32(sMeta + 4u * s));
           const uint32_t b_st = sB + s * args.stage_bytes;
           for (int kb = 0; kb < args.num_kb; ++kb) {
             const uint32_t a_kb = a_tile + kb * 16384u;
@@ -209,6 +240,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           mma_commit_pair_mc(bar_tfull(acc), 0x3);  // both CTAs' accumulator rows ready
         }
         mma_commit_pair_mc(bar_aempty(ab), 0x3);
+      }
+      if (args.stats) {
+        atomicAdd(args.stats + 0, (unsigned long long)st_acc);
+        atomicAdd(args.stats + 1, (unsigned long long)st_full);
+        atomicAdd(args.stats + 2, (unsigned long long)(clock64() - st_t0));
       }
     }
   } else if (warp < 8) {
@@ -230,66 +266,123 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       const int64_t first = c0 + (int64_t)((grp - (t & 1u)) & 1u);
       t += (uint32_t)(c1 - c0);
       if constexpr (PACKED) {
-        int4 tl_next = (first < c1) ? __ldg(args.tiles + first) : make_int4(0, 0, 0, 0);
+        // Tile columns = 16 groups of 16, each inside one chunk.  Pass 1 reads the tile with the
+        // same x64 TMEM loads as the dense kernel and keeps one masked max per group; pass 2 turns
+        // them into per-chunk maxima (suffix max inside each chunk); pass 3 finishes each chunk.
+        // The tile's 128-B record is one coalesced warp load (lane i <- word i), issued two of this
+        // group's tiles (four MMA periods) ahead, so its DRAM latency never reaches the drain.
+        auto load_rec = [&](int64_t ci) { return ci < c1 ? __ldg(args.recs + ci * 32 + lane) : 0u; };
+        uint32_t rec_n1 = load_rec(first), rec_n2 = load_rec(first + 2);
         for (int64_t c = first; c < c1; c += 2, ++mine) {
-          const int4 tl = tl_next;
-          const int32_t n_ent = tl.w - tl.z;  // <= 16 chunks per tile
-          // one entry per lane, loaded while the accumulator is still being computed
-          const int2 my_ent = ((int32_t)lane < n_ent) ? __ldg(args.ents + tl.z + lane) : make_int2(0, 0);
-          if (c + 2 < c1) tl_next = __ldg(args.tiles + c + 2);
+          const uint32_t rec = rec_n1;
+          rec_n1 = rec_n2;
+          rec_n2 = load_rec(c + 4);
+          const uint32_t w0 = __shfl_sync(0xffffffffu, rec, 0);
+          const uint32_t gstart = __shfl_sync(0xffffffffu, rec, 1);
+          const uint64_t vcw = ((uint64_t)__shfl_sync(0xffffffffu, rec, 3) << 32) |
+                               __shfl_sync(0xffffffffu, rec, 2);
+          const int32_t n_grp = (int32_t)(w0 & 0xFFFFu) >> 4;  // column groups in use
+          const uint32_t tailmask = __shfl_sync(0xffffffffu, rec, 5);  // groups with padding columns
+          long long e0 = args.stats ? clock64() : 0;
           mbar_wait(bar_tfull(grp), mine & 1u);
+          long long e1 = args.stats ? clock64() : 0;
+          if (args.stats) st_ewait_g += e1 - e0;
           tc_fence_after();
-          for (int32_t e = 0; e < n_ent; ++e) {
-            const int32_t chunk = __shfl_sync(0xffffffffu, my_ent.x, e);
-            const int32_t cl = __shfl_sync(0xffffffffu, my_ent.y, e);
-            const int32_t len = cl & 0xFFFF;
-            const uint32_t ta = taddr_base + (uint32_t)(cl >> 16);
-            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            int32_t col = 0;
-            for (; col + 64 <= len; col += 64) {
+          // Pass 1: one running max per column group of 16 -- 4 independent FMNMX3 chains per
+          // 64-column TMEM load, the dense kernel's instruction mix -- then the few tail groups
+          // (a chunk's last group, when its length is not a multiple of 16) are re-read with one
+          // x16 load each and reduced over their real columns only (reading R2).
+          float m16[16];
+#pragma unroll
+          for (int blk = 0; blk < 4; ++blk) {
+            if (blk * 4 < n_grp) {
               uint32_t v[64];
-              tmem_ld64_wait(ta + (uint32_t)col, v);
-              max64(v, m4);
+              tmem_ld64_wait(taddr_base + (uint32_t)(blk * 64), v);
+#pragma unroll
+              for (int gg = 0; gg < 4; ++gg) {
+                float a0 = fmaxf(__uint_as_float(v[gg * 16]), __uint_as_float(v[gg * 16 + 1]));
+#pragma unroll
+                for (int i = 2; i < 16; i += 2)
+                  a0 = fmaxf(fmaxf(a0, __uint_as_float(v[gg * 16 + i])), __uint_as_float(v[gg * 16 + i + 1]));
+                m16[blk * 4 + gg] = a0;
+              }
+            } else {
+#pragma unroll
+              for (int gg = 0; gg < 4; ++gg) m16[blk * 4 + gg] = -INFINITY;
             }
-            int32_t rem = len - col;  // 0..63; reads stay inside [col, roundup(len, 16))
-            if (rem > 32) {
-              uint32_t v[32];
-              tmem_ld32_wait(ta + (uint32_t)col, v);
-              maxN<32>(v, m4);
-              col += 32;
-              rem -= 32;
-            }
-            if (rem > 16) {
-              uint32_t v[32];
-              tmem_ld32_wait(ta + (uint32_t)col, v);
-              maxN_masked<32>(v, m4, rem);
-            } else if (rem > 0) {
-              uint32_t v[16];
-              tmem_ld16_wait(ta + (uint32_t)col, v);
-              maxN_masked<16>(v, m4, rem);
-            }
-            const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-            float sv = ((int32_t)lane < lq) ? m : 0.0f;
+          }
+          for (uint32_t tails = tailmask; tails != 0u; tails &= tails - 1u) {
+            const int g = __ffs(tails) - 1;
+            const int vc = (int)((vcw >> (4 * g)) & 15u) + 1;
+            uint32_t v[16];
+            tmem_ld16_wait(taddr_base + (uint32_t)(g * 16), v);
+            float a0 = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) a0 = fmaxf(a0, i < vc ? __uint_as_float(v[i]) : -INFINITY);
+#pragma unroll
+            for (int gg = 0; gg < 16; ++gg) m16[gg] = (gg == g) ? a0 : m16[gg];
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader);  // TMEM drained: release the accumulator
+          if (args.stats) {
+            st_drain_g += clock64() - e1;
+            ++st_tiles_g;
+          }
+          // Pass 2: suffix max inside each chunk -> m16[first group of a chunk] = the chunk maximum
+          // (start bits are set for every group >= n_grp, so unused groups never merge into a chunk)
+#pragma unroll
+          for (int g = 14; g >= 0; --g)
+            m16[g] = ((gstart >> (g + 1)) & 1u) ? m16[g] : fmaxf(m16[g], m16[g + 1]);
+          // Pass 3: the masked sum over query tokens for every group (16 independent butterflies,
+          // the dense kernel's fixed order); only chunk-start groups are results.  Top-k: a score
+          // pre-filter against the list threshold, exact key test and insert for the rare rest.
+          const uint32_t starts = gstart & (n_grp >= 16 ? 0xFFFFu : ((1u << n_grp) - 1u));
+          float sums[16];
+#pragma unroll
+          for (int g = 0; g < 16; ++g) {
+            float sv = ((int32_t)lane < lq) ? m16[g] : 0.0f;
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-            sv += 0.0f;  // canonical +0
-            if constexpr (MODE == 0) {
-              if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk] = sv;
-            } else {
+            sums[g] = sv + 0.0f;  // canonical +0
+          }
+          if constexpr (MODE == 0) {
+#pragma unroll
+            for (int g = 0; g < 16; ++g) {
+              if ((starts >> g) & 1u) {
+                const int e = __popc(gstart & ((1u << g) - 1u));
+                const int32_t chunk = (int32_t)__shfl_sync(0xffffffffu, rec, 16 + e);
+                if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk] = sums[g];
+              }
+            }
+          } else {
+            const uint32_t thr_hi = (uint32_t)(topk.thresh >> 32);
+            uint32_t cand = 0u;
+#pragma unroll
+            for (int g = 0; g < 16; ++g)
+              cand |= (uint32_t)(((starts >> g) & 1u) && float_orderable(sums[g]) >= thr_hi) << g;
+            while (cand != 0u) {
+              const int g = __ffs(cand) - 1;
+              cand &= cand - 1u;
+              const int e = __popc(gstart & ((1u << g) - 1u));
+              const int32_t chunk = (int32_t)__shfl_sync(0xffffffffu, rec, 16 + e);
+              float sv = sums[0];
+#pragma unroll
+              for (int gg = 1; gg < 16; ++gg) sv = (gg == g) ? sums[gg] : sv;
               const uint64_t key = make_key(sv, args.id_base + chunk);
               if (key > topk.thresh) topk.insert(key, args.k, lane);
             }
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader);
         }
       } else {
       int32_t ld_next = (first < c1) ? __ldg(args.d_lens + slot_chunk(args, g, first)) : 0;
       for (int64_t c = first; c < c1; c += 2, ++mine) {
         const int32_t ld = ld_next;
         if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk(args, g, c + 2));
+        long long e0 = args.stats ? clock64() : 0;
         mbar_wait(bar_tfull(grp), mine & 1u);
+        long long e1 = args.stats ? clock64() : 0;
+        if (args.stats) st_ewait_g += e1 - e0;
         tc_fence_after();
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         int ix4[4] = {0, 0, 0, 0};
@@ -307,6 +400,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        if (args.stats) {
+          st_drain_g += clock64() - e1;
+          ++st_tiles_g;
+        }
         const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         if constexpr (MODE == 2) {
           // argmax = lowest column index among the chains holding the max (reading: lowest u on ties)
@@ -343,6 +440,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     }
   }
 
+  if (warp < 8 && args.stats && lane == 0) {
+    atomicAdd(args.stats + 3, (unsigned long long)st_drain_g);
+    atomicAdd(args.stats + 4, (unsigned long long)st_ewait_g);
+    atomicAdd(args.stats + 5, (unsigned long long)st_tiles_g);
+  }
   // teardown: every multicast commit / remote arrive has landed before either CTA exits
   tc_fence_before();
   cluster_sync();

@@ -48,14 +48,11 @@ __device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, flo
 // j < roundup(len, 16) only (the padding rows of its 16-row slot are zeroed); out_rows is then just
 // the per-item thread range (>= roundup(max_len, 16)).
 template <typename Tin>
-__global__ void __launch_bounds__(256) norm_layout_kernel(const Tin* in, int64_t n_src, int32_t in_rows,
-                                                          const int32_t* __restrict__ lens,
-                                                          int64_t n_items, int32_t out_rows, int32_t d,
-                                                          uint32_t assume_normalized,
-                                                          uint32_t check_finite,
-                                                          __nv_bfloat16* out, uint32_t* status,
-                                                          const int64_t* __restrict__ dst_row) {
-  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void norm_row(int64_t row, const Tin* in, int64_t n_src, int32_t in_rows,
+                                         const int32_t* __restrict__ lens, int64_t n_items,
+                                         int32_t out_rows, int32_t d, uint32_t assume_normalized,
+                                         uint32_t check_finite, __nv_bfloat16* out, uint32_t* status,
+                                         const int64_t* __restrict__ dst_row) {
   if (row >= n_items * (int64_t)out_rows) return;
   const int64_t item = row / out_rows;
   const int32_t j = (int32_t)(row - item * out_rows);
@@ -110,6 +107,40 @@ __global__ void __launch_bounds__(256) norm_layout_kernel(const Tin* in, int64_t
     }
     dst[k / 8] = make_uint4(w[0], w[1], w[2], w[3]);
   }
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(256) norm_layout_kernel(const Tin* in, int64_t n_src, int32_t in_rows,
+                                                          const int32_t* __restrict__ lens,
+                                                          int64_t n_items, int32_t out_rows, int32_t d,
+                                                          uint32_t assume_normalized,
+                                                          uint32_t check_finite,
+                                                          __nv_bfloat16* out, uint32_t* status,
+                                                          const int64_t* __restrict__ dst_row) {
+  norm_row<Tin>((int64_t)blockIdx.x * blockDim.x + threadIdx.x, in, n_src, in_rows, lens, n_items,
+                out_rows, d, assume_normalized, check_finite, out, status, dst_row);
+}
+
+// Two layouts in one launch (the ColTrast step: queries and documents): blocks [0, blocks_a) lay out
+// segment A, the rest segment B.  Same per-row NORM as above.
+struct NormSeg {
+  const void* in;
+  int64_t n_src;
+  int32_t in_rows;
+  const int32_t* lens;
+  int64_t n_items;
+  int32_t out_rows;
+  __nv_bfloat16* out;
+};
+template <typename Tin>
+__global__ void __launch_bounds__(256) norm_layout2_kernel(NormSeg a, NormSeg b, int64_t blocks_a,
+                                                           int32_t d, uint32_t assume_normalized,
+                                                           uint32_t check_finite, uint32_t* status) {
+  const bool first = (int64_t)blockIdx.x < blocks_a;
+  const NormSeg& g = first ? a : b;
+  const int64_t blk = first ? (int64_t)blockIdx.x : (int64_t)blockIdx.x - blocks_a;
+  norm_row<Tin>(blk * blockDim.x + threadIdx.x, (const Tin*)g.in, g.n_src, g.in_rows, g.lens,
+                g.n_items, g.out_rows, d, assume_normalized, check_finite, g.out, status, nullptr);
 }
 
 }  // namespace hiper

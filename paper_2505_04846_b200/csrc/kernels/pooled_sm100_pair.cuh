@@ -34,6 +34,14 @@ struct PooledArgs {
   uint64_t* partial;  // MODE 1: [P][kEpiGroups][q_pad][k]
   uint32_t* progress; // [n_pairs] L2 lockstep words (see maxsim_sm100_pair.cuh), or nullptr
   int32_t window;     // chunk tiles a pair may run ahead of the slowest pair
+  // Shared pruning bound per query (MODE 1; nullptr = off): gthr[q] = max over every partial list of
+  // query q of that list's k-th best key.  Each list holds k distinct items of a disjoint partition,
+  // so no item with a key <= gthr[q] can be in the final top-k: the lists skip such items.  Without
+  // it each list pays ~k(1 + ln(n/k)) insertions for its own n items (~0.5 per thread per tile here).
+  unsigned long long* gthr;
+  unsigned long long* stats;  // pipeline statistics (HIPER_PIPE_STATS), or nullptr: [0] MMA cycles
+                              // waiting for a free accumulator, [1] for a full stage, [2] MMA
+                              // thread total, [3] epilogue drain cycles, [4] epilogue wait, [5] tiles
 };
 
 // Per-thread register top-k: the epilogue thread of query q keeps KP sortable keys in registers.
@@ -46,7 +54,10 @@ __device__ __forceinline__ float pooled_thr_score(uint64_t thr) {
   return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
-template <int MODE, int KP>
+// DBG (ablation builds only, HIPER_DEBUG_MODE): 1 = the epilogue only waits/releases the
+// accumulator (no TMEM reads, no top-k); 2 = additionally no TMA after the first stage fill;
+// 3 = the epilogue reads TMEM but does no arithmetic; 4 = arithmetic without TMEM reads.
+template <int MODE, int KP, int DBG = 0>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     pooled_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_c, const PooledArgs args) {
@@ -115,6 +126,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           }
           for (int kb = 0; kb < args.num_kb; ++kb) {
             mbar_wait(bar_empty(s), ph ^ 1u);
+            if (DBG == 2 && (it > 0 || ct - t0 >= 1)) {
+              if (rank == 0) mbar_arrive(bar_full(s));
+              if (++s == S) { s = 0; ph ^= 1u; }
+              continue;
+            }
             if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
             const uint32_t full_leader = mapa_shared(bar_full(s), 0);
             const uint32_t st = sStage + s * args.stage_bytes;
@@ -131,16 +147,22 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       const uint32_t idesc = idesc_bf16_f32(256, 256);
       int s = 0;
       uint32_t ph = 0, t = 0;
+      long long st_acc = 0, st_full = 0;
+      const long long st_t0 = clock64();
       for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
         int32_t qt, p, t0, t1;
         decode(u, qt, p, t0, t1);
         for (int32_t ct = t0; ct < t1; ++ct, ++t) {
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
+          long long w0 = args.stats ? clock64() : 0;
           mbar_wait(bar_tempty(acc), tph ^ 1u);
+          if (args.stats) st_acc += clock64() - w0;
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
           for (int kb = 0; kb < args.num_kb; ++kb) {
+            if (args.stats) w0 = clock64();
             mbar_wait(bar_full(s), ph);
+            if (args.stats) st_full += clock64() - w0;
             tc_fence_after();
             const uint32_t st = sStage + s * args.stage_bytes;
 #pragma unroll
@@ -154,6 +176,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           mma_commit_pair_mc(bar_tfull(acc), 0x3);
         }
       }
+      if (args.stats) {
+        atomicAdd(args.stats + 0, (unsigned long long)st_acc);
+        atomicAdd(args.stats + 1, (unsigned long long)st_full);
+        atomicAdd(args.stats + 2, (unsigned long long)(clock64() - st_t0));
+      }
     }
   } else if (warp < 8) {
     const uint32_t qslot = warp & 3u;
@@ -162,6 +189,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), 0);
     const int32_t k = args.k;
     uint32_t t = 0, mine = 0;
+    long long st_drain = 0, st_ewait = 0, st_tiles = 0, st_any = 0, st_ins = 0;
     for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
       int32_t qt, p, t0, t1;
       decode(u, qt, p, t0, t1);
@@ -170,18 +198,31 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
 #pragma unroll
       for (int m = 0; m < KP; ++m) v[m] = 0ull;
       uint64_t thr = 0ull;        // key of rank k-1 (0 while the list is not full)
-      float thr_f = -INFINITY;    // its score: candidates below it are rejected with one compare
+      uint64_t gth = 0ull, pub = 0ull;  // shared bound seen / own thr last published
+      if (args.gthr != nullptr && q < args.q_pad)
+        gth = *reinterpret_cast<volatile unsigned long long*>(args.gthr + q);
+      uint64_t lim = gth;         // max(thr, gth): only keys above it can enter
+      float thr_f = pooled_thr_score(lim);  // its score: most candidates fail one float compare
       const int32_t first = t0 + (int32_t)((grp - (t & 1u)) & 1u);
       t += (uint32_t)(t1 - t0);
       for (int32_t ct = first; ct < t1; ct += 2, ++mine) {
+        long long e0 = args.stats ? clock64() : 0;
         mbar_wait(bar_tfull(grp), mine & 1u);
+        long long e1 = args.stats ? clock64() : 0;
+        if (args.stats) st_ewait += e1 - e0;
         tc_fence_after();
         const int64_t cbase = (int64_t)ct * 256;
         const int64_t left = args.n_chunks - cbase;
-        const int32_t ncols = left < 256 ? (int32_t)left : 256;
+        const int32_t ncols = (DBG == 1 || DBG == 2) ? 0 : (left < 256 ? (int32_t)left : 256);
         for (int32_t col = 0; col < ncols; col += 64) {
           uint32_t r[64];
-          tmem_ld64_wait(taddr_base + (uint32_t)col, r);
+          if constexpr (DBG == 4) {  // ablation: no TMEM read, compute on fixed data
+#pragma unroll
+            for (int j = 0; j < 64; ++j) r[j] = __float_as_uint(-1.0f - (float)j);
+          } else {
+            tmem_ld64_wait(taddr_base + (uint32_t)col, r);
+          }
+          if constexpr (DBG == 3) continue;  // ablation: TMEM read only
           if constexpr (MODE == 0) {
             if (q < args.n_q) {
               float* dst = args.scores + (int64_t)q * args.score_ld + cbase + col;
@@ -191,10 +232,23 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             }
           } else {
             const int32_t nj = ncols - col;  // >= 64 except in the corpus' last tile
+            // common case first: one max over the block (21 FMNMX3) and a single compare; the
+            // per-column hit mask is built only when some column can enter the list
+            bool any;
+            if (nj >= 64) {
+              float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+              max64(r, m4);
+              any = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) >= thr_f;
+            } else {
+              any = true;
+            }
             uint64_t hits = 0ull;
+            if (any) {
+              if (args.stats) ++st_any;
 #pragma unroll
-            for (int j = 0; j < 64; ++j)
-              hits |= (uint64_t)(__uint_as_float(r[j]) >= thr_f && j < nj) << j;
+              for (int j = 0; j < 64; ++j)
+                hits |= (uint64_t)(__uint_as_float(r[j]) >= thr_f && j < nj) << j;
+            }
             if (hits) {
               float xs[64];  // rare path: a local copy so the hits can be indexed dynamically
 #pragma unroll
@@ -203,7 +257,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                 const int j = __ffsll((long long)hits) - 1;
                 hits &= hits - 1;
                 uint64_t key = make_key(xs[j], args.id_base + cbase + col + j);
-                if (key > thr) {
+                if (key > lim) {
+                  if (args.stats) ++st_ins;
 #pragma unroll
                   for (int m = 0; m < KP; ++m) {
                     const uint64_t hi = v[m] > key ? v[m] : key;
@@ -215,7 +270,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                   for (int m = 0; m < KP; ++m)
                     if (m == k - 1) nt = v[m];
                   thr = nt;
-                  thr_f = pooled_thr_score(thr);
+                  lim = thr > gth ? thr : gth;
+                  thr_f = pooled_thr_score(lim);
                 }
               }
             }
@@ -224,6 +280,27 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        if (args.stats) {
+          st_drain += clock64() - e1;
+          ++st_tiles;
+        }
+        if constexpr (MODE == 1) {
+          if (args.gthr != nullptr && q < args.q_pad) {
+            if (thr > pub) {  // publish this list's k-th key; learn the others'
+              const uint64_t old = atomicMax(args.gthr + q, (unsigned long long)thr);
+              pub = thr;
+              gth = old > gth ? old : gth;
+            } else if ((mine & 7u) == 0) {
+              const uint64_t cur = *reinterpret_cast<volatile unsigned long long*>(args.gthr + q);
+              gth = cur > gth ? cur : gth;
+            }
+            const uint64_t nl = thr > gth ? thr : gth;
+            if (nl != lim) {
+              lim = nl;
+              thr_f = pooled_thr_score(lim);
+            }
+          }
+        }
       }
       if constexpr (MODE == 1) {
         if (q < args.n_q) {
@@ -233,6 +310,15 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             if (m < k) dst[m] = v[m];
         }
       }
+    }
+    if (args.stats && lane == 0) {
+      atomicAdd(args.stats + 3, (unsigned long long)st_drain);
+      atomicAdd(args.stats + 4, (unsigned long long)st_ewait);
+      atomicAdd(args.stats + 5, (unsigned long long)st_tiles);
+    }
+    if (args.stats) {
+      atomicAdd(args.stats + 6, (unsigned long long)st_any);
+      atomicAdd(args.stats + 7, (unsigned long long)st_ins);
     }
   }
 
