@@ -47,6 +47,8 @@ def parse():
                          "Q=4096, top-10; config2: ColTrast step B=256 scores + InfoNCE; "
                          "config3v (NEXT N4): config3 with semantic-chunking lengths (<= 256) on "
                          "the packed layout")
+    ap.add_argument("--fixed-len", action="store_true",
+                    help="config3v: every chunk at full length (isolates the packed machinery)")
     ap.add_argument("--no-pack", action="store_true",
                     help="config3v: dense padded layout instead of HIPER_PACKED (the N4 ablation)")
     ap.add_argument("--chunks", type=int, default=None)
@@ -278,7 +280,8 @@ def run_ours(a, rank, local_rank, world):
     device.corpus_(corpus, a.seed, c0)
     all_lens = None
     if a.semantic:
-        all_lens = gen.semantic_lengths(a.seed, a.chunks, a.chunk_len)
+        all_lens = (np.full(a.chunks, a.chunk_len, np.int32) if a.fixed_len
+                    else gen.semantic_lengths(a.seed, a.chunks, a.chunk_len))
         lens = all_lens[c0:c1].copy()
     else:
         lens = np.full(n_local, a.chunk_len, np.int32)

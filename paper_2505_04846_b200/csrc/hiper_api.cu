@@ -350,10 +350,27 @@ static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src
   const int64_t rows = n_items * (int64_t)out_rows;
   if (rows == 0) return HIPER_OK;
   const int threads = 256;
-  const int64_t blocks = (rows + threads - 1) / threads;
-  if (blocks > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
   const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
   const uint32_t cf = (flags & HIPER_CHECK_FINITE) ? 1u : 0u;
+  if (dim == 64 || dim == 128) {  // d/16 threads per row: coalesced, same fma order (bit-identical)
+    const int tpr = dim / 16;
+    const int64_t blocks = (rows * tpr + threads - 1) / threads;
+    if (blocks > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
+#define HIPER_NORM_TPR(T, TPR)                                                                       \
+  norm_layout_tpr_kernel<T, TPR><<<(unsigned)blocks, threads, 0, stream>>>(                          \
+      (const T*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out, status, dst_row)
+    if (dtype == HIPER_F32) {
+      if (tpr == 4) HIPER_NORM_TPR(float, 4); else HIPER_NORM_TPR(float, 8);
+    } else {
+      if (tpr == 4) HIPER_NORM_TPR(__nv_bfloat16, 4); else HIPER_NORM_TPR(__nv_bfloat16, 8);
+    }
+#undef HIPER_NORM_TPR
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    return HIPER_OK;
+  }
+  const int64_t blocks = (rows + threads - 1) / threads;
+  if (blocks > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
   if (dtype == HIPER_F32)
     norm_layout_kernel<float><<<(unsigned)blocks, threads, 0, stream>>>(
         (const float*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out, status,
@@ -375,18 +392,24 @@ static hiper_status launch_norm2(const void* in_a, int64_t n_a, int32_t in_rows_
                                  hiper_dtype dtype, int32_t dim, uint32_t flags, uint32_t* status,
                                  cudaStream_t stream) {
   const int threads = 256;
-  const int64_t ba = (items_a * out_rows_a + threads - 1) / threads;
-  const int64_t bb = (items_b * out_rows_b + threads - 1) / threads;
+  if (dim != 64 && dim != 128) return fail(HIPER_ERR_UNSUPPORTED, "token dim %d", dim);
+  const int tpr = dim / 16;
+  const int64_t ba = (items_a * out_rows_a * tpr + threads - 1) / threads;
+  const int64_t bb = (items_b * out_rows_b * tpr + threads - 1) / threads;
   if (ba + bb == 0) return HIPER_OK;
   if (ba + bb > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
   const NormSeg a{in_a, n_a, in_rows_a, lens_a, items_a, out_rows_a, out_a};
   const NormSeg b{in_b, n_b, in_rows_b, lens_b, items_b, out_rows_b, out_b};
   const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
   const uint32_t cf = (flags & HIPER_CHECK_FINITE) ? 1u : 0u;
-  if (dtype == HIPER_F32)
-    norm_layout2_kernel<float><<<(unsigned)(ba + bb), threads, 0, stream>>>(a, b, ba, dim, an, cf, status);
-  else
-    norm_layout2_kernel<__nv_bfloat16><<<(unsigned)(ba + bb), threads, 0, stream>>>(a, b, ba, dim, an, cf, status);
+#define HIPER_NORM2(T, TPR) \
+  norm_layout2_kernel<T, TPR><<<(unsigned)(ba + bb), threads, 0, stream>>>(a, b, ba, dim, an, cf, status)
+  if (dtype == HIPER_F32) {
+    if (tpr == 4) HIPER_NORM2(float, 4); else HIPER_NORM2(float, 8);
+  } else {
+    if (tpr == 4) HIPER_NORM2(__nv_bfloat16, 4); else HIPER_NORM2(__nv_bfloat16, 8);
+  }
+#undef HIPER_NORM2
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return HIPER_OK;
@@ -672,7 +695,7 @@ static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int64_t n_chunks
   // one stage = one 64-dim K-block of a whole chunk
   kp.stage_bytes = kp.pair ? (uint32_t)(ld_pad / 2) * 128u * (uint32_t)(dim / 64)
                            : (uint32_t)ld_pad * 128u;
-  const uint32_t fixed = 1024u /*align slack*/ + 2u * kp.a_bytes + 512u /*barriers*/;
+  const uint32_t fixed = 1024u /*align slack*/ + 2u * kp.a_bytes + 1024u /*barriers, meta, ring*/;
   const uint32_t avail = (uint32_t)di.max_smem > fixed ? (uint32_t)di.max_smem - fixed : 0u;
   kp.n_stages = (int32_t)std::min<uint32_t>(kp.pair ? 12u : 8u, avail / kp.stage_bytes);
   if (kp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory for 2 stages");

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   auto bar_tempty = [&](int b) { return sBar + 8u * (2 * S + 6 + b); };
   const uint32_t sTmemPtr = sBar + 8u * (2 * S + 8);
   const uint32_t sMeta = sTmemPtr + 16u;  // [S] u32: MMA N per stage (packed corpus)
+  const uint32_t sRing = sBar + 512u;     // [2][32] x {w0, row0}: producer's tile batches (packed)
   uint32_t* tmem_ptr_generic =
       reinterpret_cast<uint32_t*>(smem_raw + (sTmemPtr - smem_u32(smem_raw)));
 
@@ -143,28 +144,30 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           tma_load_2d_pair(sA + ab * args.a_bytes + kb * 16384u, &tmap_q, afull_leader, kb * 64,
                            (int32_t)((2 * g + (int32_t)rank) * 128));
       }
-      int2 cur = make_int2(0, 0), nxt = make_int2(0, 0);
-      auto load_batch = [&](int64_t cb) {  // lane i: (row0, n_rows) of tile cb + i
+      // packed: (w0, row0) of 32 tiles at a time land in an SMEM ring by cp.async, one batch ahead
+      auto load_batch = [&](int64_t cb, uint32_t slot) {
         const int64_t ci = cb + lane;
         if (ci < c1) {
-          const uint32_t* r = args.recs + ci * 32;
-          return make_int2((int32_t)__ldg(r + 4), (int32_t)(__ldg(r) & 0xFFFFu));
+          const uint32_t dst = sRing + slot * 256u + lane * 8u;
+          cp_async4(dst, args.recs + ci * 32);
+          cp_async4(dst + 4u, args.recs + ci * 32 + 4);
         }
-        return make_int2(0, 0);
+        cp_async_commit();
       };
-      if constexpr (PACKED) nxt = load_batch(c0);
+      if constexpr (PACKED) load_batch(c0, 0u);
       for (int64_t c = c0; c < c1; ++c) {
         int32_t brow;
         uint32_t nrows = (uint32_t)args.ld_pad;
         if constexpr (PACKED) {
-          const int j = (int)((c - c0) & 31);
+          const uint32_t j = (uint32_t)((c - c0) & 31), b = (uint32_t)((c - c0) >> 5);
           if (j == 0) {
-            cur = nxt;
-            nxt = load_batch(c + 32);
+            load_batch(c + 32, (b + 1) & 1u);
+            cp_async_wait<1>();  // batch b (issued 32 tiles ago) has landed
+            __syncwarp();
           }
-          brow = __shfl_sync(0xffffffffu, cur.x, j);
-          nrows = (uint32_t)__shfl_sync(0xffffffffu, cur.y, j);
-          brow += (int32_t)rank * (int32_t)(nrows >> 1);
+          const uint32_t e = sRing + (b & 1u) * 256u + j * 8u;
+          nrows = ld_shared_u32(e) & 0xFFFFu;
+          brow = (int32_t)ld_shared_u32(e + 4u) + (int32_t)rank * (int32_t)(nrows >> 1);
         } else {
           brow = (int32_t)(slot_chunk(args, g, c) * args.ld_pad + (int64_t)rank * half_rows);
         }

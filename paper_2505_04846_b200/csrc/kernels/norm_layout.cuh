@@ -121,6 +121,104 @@ __global__ void __launch_bounds__(256) norm_layout_kernel(const Tin* in, int64_t
                 out_rows, d, assume_normalized, check_finite, out, status, dst_row);
 }
 
+// Same NORM with TPR = d/16 threads per row (d <= 512): each lane owns 16 consecutive elements, the
+// loads and stores are coalesced, and the fp32 fma chain still runs over k in ascending order -- lane t
+// continues the accumulator it receives from lane t-1 -- so the result is bit-identical to the
+// one-thread-per-row form above.
+template <typename Tin>
+__device__ __forceinline__ void load16(const Tin* p, float (&x)[16]) {
+  float a[8], b[8];
+  load8<Tin>(p, a);
+  load8<Tin>(p + 8, b);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    x[i] = a[i];
+    x[8 + i] = b[i];
+  }
+}
+template <typename Tin, int TPR>
+__device__ __forceinline__ void norm_row_group(int64_t row, uint32_t sub, const Tin* in, int64_t n_src,
+                                               int32_t in_rows, const int32_t* __restrict__ lens,
+                                               int64_t n_items, int32_t out_rows, int32_t d,
+                                               uint32_t assume_normalized, uint32_t check_finite,
+                                               __nv_bfloat16* out, uint32_t* status,
+                                               const int64_t* __restrict__ dst_row) {
+  const bool in_range = row < n_items * (int64_t)out_rows;
+  int64_t item = 0;
+  int32_t j = 0, len = 0;
+  bool write = false, real = false;
+  if (in_range) {
+    item = row / out_rows;
+    j = (int32_t)(row - item * out_rows);
+    len = item < n_src ? lens[item] : 0;
+    write = !(dst_row != nullptr && j >= ((len + 15) & ~15));
+    real = j < len;
+  }
+  float x[16];
+  if (real) {
+    load16<Tin>(in + (item * in_rows + j) * (int64_t)d + sub * 16, x);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = 0.0f;
+  }
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) finite &= isfinite(x[i]);
+  uint32_t nonfinite = finite ? 0u : 1u;
+#pragma unroll
+  for (int o = TPR / 2; o >= 1; o >>= 1) nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, o, TPR);
+  float acc = 0.0f;
+  if (!assume_normalized) {
+#pragma unroll
+    for (int t = 0; t < TPR; ++t) {
+      if (sub == (uint32_t)t) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc = __fmaf_rn(x[i], x[i], acc);
+      }
+      acc = __shfl_sync(0xffffffffu, acc, t, TPR);
+    }
+  }
+  if (real && sub == 0 && status != nullptr) {
+    if (!assume_normalized) {
+      if (nonfinite) atomicOr(status, kStatusNonFinite);
+      else if (acc == 0.0f) atomicOr(status, kStatusZeroRow);
+    } else if (check_finite && nonfinite) {
+      atomicOr(status, kStatusNonFinite);
+    }
+  }
+  if (!write) return;
+  uint4* dst = reinterpret_cast<uint4*>(out + (dst_row != nullptr ? dst_row[item] + j : row) * d + sub * 16);
+  if (!real) {
+    dst[0] = make_uint4(0, 0, 0, 0);
+    dst[1] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const float inv = assume_normalized ? 1.0f : __fdiv_rn(1.0f, __fsqrt_rn(acc));
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float a = assume_normalized ? x[2 * i] : __fmul_rn(x[2 * i], inv);
+    const float b = assume_normalized ? x[2 * i + 1] : __fmul_rn(x[2 * i + 1], inv);
+    w[i] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
+           ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+  }
+  dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+template <typename Tin, int TPR>
+__global__ void __launch_bounds__(256) norm_layout_tpr_kernel(const Tin* in, int64_t n_src, int32_t in_rows,
+                                                              const int32_t* __restrict__ lens,
+                                                              int64_t n_items, int32_t out_rows, int32_t d,
+                                                              uint32_t assume_normalized,
+                                                              uint32_t check_finite,
+                                                              __nv_bfloat16* out, uint32_t* status,
+                                                              const int64_t* __restrict__ dst_row) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  norm_row_group<Tin, TPR>(tid / TPR, (uint32_t)(tid % TPR), in, n_src, in_rows, lens, n_items, out_rows,
+                           d, assume_normalized, check_finite, out, status, dst_row);
+}
+
 // Two layouts in one launch (the ColTrast step: queries and documents): blocks [0, blocks_a) lay out
 // segment A, the rest segment B.  Same per-row NORM as above.
 struct NormSeg {
@@ -132,15 +230,17 @@ struct NormSeg {
   int32_t out_rows;
   __nv_bfloat16* out;
 };
-template <typename Tin>
+template <typename Tin, int TPR>
 __global__ void __launch_bounds__(256) norm_layout2_kernel(NormSeg a, NormSeg b, int64_t blocks_a,
                                                            int32_t d, uint32_t assume_normalized,
                                                            uint32_t check_finite, uint32_t* status) {
   const bool first = (int64_t)blockIdx.x < blocks_a;
   const NormSeg& g = first ? a : b;
   const int64_t blk = first ? (int64_t)blockIdx.x : (int64_t)blockIdx.x - blocks_a;
-  norm_row<Tin>(blk * blockDim.x + threadIdx.x, (const Tin*)g.in, g.n_src, g.in_rows, g.lens,
-                g.n_items, g.out_rows, d, assume_normalized, check_finite, g.out, status, nullptr);
+  const int64_t tid = blk * blockDim.x + threadIdx.x;
+  norm_row_group<Tin, TPR>(tid / TPR, (uint32_t)(tid % TPR), (const Tin*)g.in, g.n_src, g.in_rows,
+                           g.lens, g.n_items, g.out_rows, d, assume_normalized, check_finite, g.out,
+                           status, nullptr);
 }
 
 }  // namespace hiper
