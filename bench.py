@@ -40,7 +40,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["config3", "config4", "config5", "config2", "config3v"],
+    ap.add_argument("--workload", choices=["config3", "config4", "config5", "config2", "config3v",
+                                           "config4v"],
                     default="config3",
                     help="config3 (default, N=1 headline): 1M x 256-token chunks, Q=1024, top-10; "
                          "config4: 3.6M chunks, top-100 (N>=2); config5: pooled 3.6M x 768, "
@@ -72,12 +73,16 @@ def parse():
         "config5": dict(chunks=3_600_000, queries=4096, k=10, chunk_len=1, query_len=1, dim=768),
         "config2": dict(chunks=256, queries=256, k=1, chunk_len=256, query_len=32, dim=128),
         "config3v": dict(chunks=1_000_000, queries=1024, k=10, chunk_len=256, query_len=32, dim=128),
+        # config4 on semantic-chunk lengths: generated straight into each shard's packed layout
+        # (HIPER_PACKED | HIPER_BORROW_TOKENS); --chunks 16400000 is the paper's SLC corpus size
+        "config4v": dict(chunks=3_600_000, queries=1024, k=100, chunk_len=256, query_len=32, dim=128),
     }[a.workload]
     for key, v in defaults.items():
         if getattr(a, key) is None:
             setattr(a, key, v)
-    a.semantic = a.workload == "config3v"
+    a.semantic = a.workload in ("config3v", "config4v")
     a.packed = a.semantic and not a.no_pack
+    a.gen_packed = a.workload == "config4v"
     a.mean_len = a.chunk_len
     if a.semantic:
         from synth import gen
@@ -276,8 +281,10 @@ def run_ours(a, rank, local_rank, world):
     c0 = rank * a.chunks // world
     c1 = (rank + 1) * a.chunks // world
     n_local = c1 - c0
-    corpus = torch.empty((n_local, a.chunk_len, a.dim), dtype=torch.bfloat16, device="cuda")
-    device.corpus_(corpus, a.seed, c0)
+    corpus = None
+    if not a.gen_packed:
+        corpus = torch.empty((n_local, a.chunk_len, a.dim), dtype=torch.bfloat16, device="cuda")
+        device.corpus_(corpus, a.seed, c0)
     all_lens = None
     if a.semantic:
         all_lens = (np.full(a.chunks, a.chunk_len, np.int32) if a.fixed_len
@@ -285,7 +292,14 @@ def run_ours(a, rank, local_rank, world):
         lens = all_lens[c0:c1].copy()
     else:
         lens = np.full(n_local, a.chunk_len, np.int32)
-    if a.packed:  # N4: packed copy of the real rows, then the padded source is freed
+    if a.gen_packed:  # N4 at paper scale: generate into the packed layout, NORM in place
+        dst, n_rows = H.hiper_pack_dst_rows(lens)
+        corpus = torch.empty((max(n_rows, 1), a.dim), dtype=torch.bfloat16, device="cuda")
+        device.corpus_packed_(corpus, a.seed, c0, torch.from_numpy(dst).cuda(),
+                              torch.from_numpy(lens).cuda(), a.chunk_len)
+        idx = H.hiper_index_build(corpus, lens, id_base=c0,
+                                  flags=H.HIPER_PACKED | H.HIPER_BORROW_TOKENS)
+    elif a.packed:  # N4: packed copy of the real rows, then the padded source is freed
         idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_PACKED)
         torch.cuda.synchronize()
         del corpus

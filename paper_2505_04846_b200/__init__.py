@@ -272,10 +272,19 @@ def _raw_u8_view(ptr: int, nbytes: int):
     return torch.as_tensor(_Arr(), device="cuda")
 
 
-def hiper_index_build(tokens, lens, *, id_base: int = 0, flags: int = 0, stream=None) -> Index:
-    """Step a1.  tokens: CUDA tensor [n][max_len][dim] (f32/bf16); lens: host ints [n]."""
-    n, max_len, dim = tokens.shape
+def hiper_index_build(tokens, lens, *, id_base: int = 0, flags: int = 0, max_len: int | None = None,
+                      stream=None) -> Index:
+    """Step a1.  tokens: CUDA tensor [n][max_len][dim] (f32/bf16); lens: host ints [n].
+    With HIPER_PACKED | HIPER_BORROW_TOKENS, tokens is the packed bf16 buffer [n_rows][dim]
+    (hiper_pack_dst_rows) and n = len(lens); max_len defaults to 256."""
     ln = _host_i32(lens)
+    if tokens.dim() == 2:
+        if not (flags & HIPER_PACKED and flags & HIPER_BORROW_TOKENS):
+            raise HiperError(1, "a 2-D token buffer needs HIPER_PACKED | HIPER_BORROW_TOKENS")
+        n, dim = ln.shape[0], tokens.shape[1]
+        max_len = max_len or 256
+    else:
+        n, max_len, dim = tokens.shape
     if ln.shape != (n,):
         raise HiperError(1, f"lens shape {ln.shape} != ({n},)")
     h = ctypes.c_void_p()
@@ -297,6 +306,19 @@ def hiper_pack_plan(lens):
     _check(lib().hiper_pack_plan(_ptr(ln), n, _ptr(tiles), _ptr(ents), ctypes.byref(nt),
                                  ctypes.byref(nr)))
     return tiles[:nt.value].copy(), ents[:n].copy(), nr.value
+
+
+def hiper_pack_dst_rows(lens):
+    """(dst_row int64 [n], n_rows) of hiper_pack_plan(lens): chunk c's token j lives at packed row
+    dst_row[c] + j.  For callers that generate or copy a corpus straight into the packed layout and
+    then build with HIPER_PACKED | HIPER_BORROW_TOKENS."""
+    tiles, ents, n_rows = hiper_pack_plan(lens)
+    n = ents.shape[0]
+    dst = np.zeros(n, np.int64)
+    if n:
+        tile_of_ent = np.repeat(np.arange(len(tiles)), tiles[:, 3] - tiles[:, 2])
+        dst[ents[:, 0]] = tiles[tile_of_ent, 0].astype(np.int64) + (ents[:, 1] >> 16)
+    return dst, n_rows
 
 
 def hiper_prepare_queries(q_tokens, q_lens, *, flags: int = 0, stream=None):

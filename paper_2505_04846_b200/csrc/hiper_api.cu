@@ -449,8 +449,8 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     return fail(HIPER_ERR_UNSUPPORTED, "n * ld_pad >= 2^31 rows for one index; shard the corpus");
   TRY(check_lens(lens, n, max_len, "chunk"));
   const bool borrow = (flags & HIPER_BORROW_TOKENS) != 0;
-  if (packed && borrow)
-    return fail(HIPER_ERR_INVALID_ARG, "HIPER_PACKED and HIPER_BORROW_TOKENS are exclusive");
+  if (packed && borrow && (dtype != HIPER_BF16 || (dim != 64 && dim != 128)))
+    return fail(HIPER_ERR_INVALID_ARG, "HIPER_PACKED | HIPER_BORROW_TOKENS needs bf16 packed tokens");
   if (packed && !use_pair_kernel())
     return fail(HIPER_ERR_UNSUPPORTED, "HIPER_PACKED needs the CTA-pair kernel (HIPER_MAXSIM_CTA=1 set)");
   std::vector<int4> p_tiles;
@@ -458,7 +458,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   std::vector<int64_t> p_dst;
   int64_t p_rows = 0;
   if (packed) TRY(pack_plan(lens, n, p_tiles, p_ents, p_dst, p_rows));
-  if (borrow && (dtype != HIPER_BF16 || max_len != ld_pad || (dim % 8) != 0))
+  if (borrow && !packed && (dtype != HIPER_BF16 || max_len != ld_pad || (dim % 8) != 0))
     return fail(HIPER_ERR_INVALID_ARG, "HIPER_BORROW_TOKENS needs bf16 tokens and max_len %% 16 == 0");
   if (n > 0) {
     if (!tokens) return fail(HIPER_ERR_INVALID_ARG, "tokens is NULL");
@@ -489,15 +489,19 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   const int64_t n_alloc = std::max<int64_t>(n, 1);
   if (cudaMalloc(&ix->lens, n_alloc * sizeof(int32_t)) != cudaSuccess)
     return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "lens alloc"));
-  if (borrow) {
+  if (borrow && !packed) {
     ix->tok = (__nv_bfloat16*)const_cast<void*>(tokens);
   } else if (packed) {
     ix->packed = true;
     ix->n_tiles = (int64_t)p_tiles.size();
     ix->n_rows = p_rows;
-    if (cudaMalloc(&ix->tok, (size_t)std::max<int64_t>(p_rows, 1) * dim * 2) != cudaSuccess)
-      return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "packed layout alloc %lld bytes", (long long)p_rows * dim * 2));
-    ix->owns_tok = true;
+    if (borrow) {  // the caller's buffer already has the hiper_pack_plan layout: NORM in place
+      ix->tok = (__nv_bfloat16*)const_cast<void*>(tokens);
+    } else {
+      if (cudaMalloc(&ix->tok, (size_t)std::max<int64_t>(p_rows, 1) * dim * 2) != cudaSuccess)
+        return cleanup(fail(HIPER_ERR_OUT_OF_MEMORY, "packed layout alloc %lld bytes", (long long)p_rows * dim * 2));
+      ix->owns_tok = true;
+    }
     const std::vector<uint32_t> p_rec = tile_records(p_tiles, p_ents);
     if (cudaMalloc(&ix->recs, std::max<size_t>(p_rec.size(), 1) * sizeof(uint32_t)) != cudaSuccess ||
         (n > 0 && cudaMemcpyAsync(ix->recs, p_rec.data(), p_rec.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, stream) != cudaSuccess))
@@ -665,6 +669,33 @@ static int32_t choose_parts(int32_t n_groups, int64_t n_chunks, int num_sms) {
   return (int32_t)std::max<int64_t>(1, std::min<int64_t>(p0, n_chunks));
 }
 
+// Top-k path: L2 bands.  Units are (row group, corpus partition), ordered partition-major, and a wave
+// of resident pairs covers at most two consecutive partitions.  With partitions of ~kBandBytes of
+// corpus, both stay resident in the 126 MB L2 while every row group streams them, so HBM reads the
+// corpus ~once per query batch (37 partitions at config 3 re-read it 2.7x).  The partition count is
+// a multiple of p0 (full waves) and is capped so the per-(partition, group) top-k lists stay small.
+// HIPER_BAND_MB overrides the band size (0 = the minimal partition count).
+static int64_t band_bytes() {
+  static const int64_t b = [] {
+    const char* e = getenv("HIPER_BAND_MB");
+    return e ? (int64_t)atoll(e) << 20 : (int64_t)48 << 20;
+  }();
+  return b;
+}
+static int32_t choose_parts_topk(int32_t n_groups, int64_t n_slots, int num_slots, int64_t slot_bytes,
+                                 int32_t n_q_pad, int32_t k) {
+  if (n_slots <= 0) return 0;
+  const int64_t p0 = num_slots / std::gcd(n_groups, num_slots);
+  int64_t p = p0;
+  if (band_bytes() > 0) {
+    const int64_t want = (n_slots * slot_bytes + band_bytes() - 1) / band_bytes();
+    p = std::max<int64_t>(p0, (want + p0 - 1) / p0 * p0);
+    const int64_t cap = ((int64_t)512 << 20) / ((int64_t)kEpiGroups * n_q_pad * k * 8);
+    p = std::min<int64_t>(p, std::max<int64_t>(p0, cap / p0 * p0));
+  }
+  return (int32_t)std::max<int64_t>(1, std::min<int64_t>(p, n_slots));
+}
+
 // Kernel shape: the CTA-pair kernel (cta_group::2, M = 256) is the production path; the
 // single-CTA kernel (M = 128) is kept for ablation only (HIPER_MAXSIM_CTA=1).
 static bool use_pair_kernel() {
@@ -684,12 +715,14 @@ struct KernelPlan {
 };
 
 static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int64_t n_chunks, int32_t ld_pad,
-                                int32_t dim, KernelPlan& kp) {
+                                int32_t dim, KernelPlan& kp, int32_t topk_k = 0) {
   kp.pair = use_pair_kernel();
   kp.qpg = kp.pair ? 8 : 4;
   const int slots = kp.pair ? di.num_sms / 2 : di.num_sms;  // CTA pairs or CTAs
   kp.n_groups = n_q_pad_of(n_q) / kp.qpg;
-  kp.n_parts = choose_parts(kp.n_groups, n_chunks, slots);
+  kp.n_parts = topk_k > 0 ? choose_parts_topk(kp.n_groups, n_chunks, slots, (int64_t)ld_pad * dim * 2,
+                                              n_q_pad_of(n_q), topk_k)
+                          : choose_parts(kp.n_groups, n_chunks, slots);
   kp.a_bytes = (uint32_t)(dim / 64) * 16384u;
   // pair kernel: one stage = this CTA's half of a whole chunk (all K-blocks); single-CTA kernel:
   // one stage = one 64-dim K-block of a whole chunk
@@ -783,13 +816,17 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     cfg.blockDim = dim3(kMaxsimThreads);
     cfg.dynamicSmemBytes = kp.smem_bytes;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: the kernel's set-up (barriers, TMEM, tensor-map prefetch)
+    // overlaps the previous kernel's tail; it waits (griddepcontrol.wait) before reading its inputs
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
     unsigned long long* st = nullptr;
     MaxsimArgs b = a;
@@ -975,7 +1012,9 @@ extern "C" size_t hiper_maxsim_topk_workspace_size(const hiper_index* ix, int32_
   const bool pair = use_pair_kernel();
   const int32_t G = n_q_pad_of(n_q) / (pair ? 8 : 4);
   TopkWs w;
-  topk_ws_layout(n_q, ix->dim, choose_parts(G, index_slots(ix), pair ? num_sms / 2 : num_sms), k,
+  topk_ws_layout(n_q, ix->dim,
+                 choose_parts_topk(G, index_slots(ix), pair ? num_sms / 2 : num_sms,
+                                   (int64_t)index_slot_rows(ix) * ix->dim * 2, n_q_pad_of(n_q), k), k,
                  comm ? comm->world : 1, comm != nullptr, w);
   return w.total;
 }
@@ -1194,7 +1233,7 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
   TRY(device_info(di));
   if (di.device != ix->device) return fail(HIPER_ERR_INVALID_ARG, "index lives on device %d, current is %d", ix->device, di.device);
   KernelPlan kp;
-  TRY(plan_kernel(di, n_q, index_slots(ix), index_slot_rows(ix), dim, kp));
+  TRY(plan_kernel(di, n_q, index_slots(ix), index_slot_rows(ix), dim, kp, k));
   const int32_t world = comm ? comm->world : 1;
   TopkWs w;
   topk_ws_layout(n_q, dim, kp.n_parts, k, world, comm != nullptr, w);
@@ -1382,10 +1421,19 @@ static hiper_status launch_loss(const float* S, int32_t n_q, int32_t n_d, int64_
                                 cudaStream_t stream, const float* combine_with = nullptr,
                                 float* out_combined = nullptr, double* rows = nullptr,
                                 uint32_t* counter = nullptr) {
-  if (rows != nullptr && counter != nullptr && combine_with == nullptr)
-    infonce_rows_kernel<<<(n_q + 7) / 8, 256, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, rows,
-                                                            counter, out_loss);
-  else
+  if (rows != nullptr && counter != nullptr && combine_with == nullptr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((n_q + 7) / 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see launch_maxsim_t)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, infonce_rows_kernel, S, n_q, n_d, ld, pos_dev, tau, rows,
+                                counter, out_loss));
+  } else
     infonce_loss_kernel<<<1, 1024, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, out_loss, combine_with,
                                                 out_combined);
   CUDA_TRY(cudaGetLastError());

@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) infonce_rows_kernel(const float* __restri
                                                            uint32_t* counter, float* __restrict__ out_loss) {
   __shared__ double part[256];
   __shared__ bool last;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: S is the previous kernel's output
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t i = (int32_t)blockIdx.x * 8 + (int32_t)warp;
   if (i < B) {

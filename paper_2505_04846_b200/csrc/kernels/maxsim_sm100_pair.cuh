@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr_generic);
+  // PDL: the set-up above overlapped the previous kernel's tail; its outputs (the query / doc
+  // layouts, lengths) are read only after this point.
+  grid_dependency_wait();
 
   const int32_t n_units = args.n_groups * args.n_parts;  // n_groups = row-group pairs (8 queries)
   long long st_drain_g = 0, st_ewait_g = 0, st_tiles_g = 0;  // HIPER_PIPE_STATS (epilogue warps)

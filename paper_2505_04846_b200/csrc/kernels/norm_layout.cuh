@@ -156,7 +156,12 @@ __device__ __forceinline__ void norm_row_group(int64_t row, uint32_t sub, const 
   }
   float x[16];
   if (real) {
-    load16<Tin>(in + (item * in_rows + j) * (int64_t)d + sub * 16, x);
+    // in == out with dst_row set: a caller-packed buffer normalised in place (HIPER_PACKED |
+    // HIPER_BORROW_TOKENS); each lane reads, then writes, only its own 16 elements
+    const int64_t src_row = (dst_row != nullptr && (const void*)in == (const void*)out)
+                                ? dst_row[item] + j
+                                : item * in_rows + j;
+    load16<Tin>(in + src_row * (int64_t)d + sub * 16, x);
   } else {
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] = 0.0f;

@@ -85,6 +85,26 @@ __global__ void query_kernel(void* out, int out_bf16, uint64_t q0, uint64_t n_q,
   }
 }
 
+// Corpus chunks written straight into a packed layout: chunk c's token j (< len[c]) goes to row
+// dst_row[c] + j of out [rows][d] (bf16); rows len[c] .. roundup(len[c], 16) - 1 are zeroed.  The
+// values are those of corpus_kernel for the same (chunk, token, dim) (L = the hash's token stride).
+__global__ void corpus_packed_kernel(uint16_t* out, uint64_t c0, uint64_t n, uint64_t L, uint64_t d,
+                                     const int64_t* dst_row, const int32_t* lens, Keys K, int planted,
+                                     float sigma) {
+  const uint64_t total = n * L * d;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = e % d;
+    const uint64_t row = e / d;
+    const uint64_t j = row % L;
+    const uint64_t c = row / L;
+    const uint64_t len = (uint64_t)lens[c];
+    if (j >= ((len + 15) & ~15ull)) continue;
+    const float v = j < len ? corpus_value(K, planted, c0 + c, j, k, L, d, sigma) : 0.0f;
+    out[((uint64_t)dst_row[c] + j) * d + k] = f2bf(v);
+  }
+}
+
 Keys make_keys(uint64_t seed) {
   return Keys{key_of(seed, TOK), key_of(seed, CENT), key_of(seed, TOPIC), key_of(seed, TOPIC2),
               key_of(seed, MIX)};
@@ -119,5 +139,16 @@ extern "C" __attribute__((visibility("default"))) int synth_queries(void* out, i
       key_of(qseed, QTOK), key_of(qseed, QTARGET), key_of(qseed, QPOS), diagonal, query_planted,
       (uint64_t)n_chunks, (uint64_t)L, chunk_lens_dev, make_keys(corpus_seed), corpus_planted, sigma,
       sigma_q);
+  return (int)cudaGetLastError();
+}
+
+extern "C" __attribute__((visibility("default"))) int synth_corpus_packed(
+    void* out, int64_t chunk_start, int64_t n, int32_t L, int32_t d, uint64_t seed, int planted,
+    float sigma, const int64_t* dst_row_dev, const int32_t* lens_dev, void* stream) {
+  if (n <= 0) return 0;
+  const uint64_t total = (uint64_t)n * L * d;
+  corpus_packed_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(
+      (uint16_t*)out, (uint64_t)chunk_start, (uint64_t)n, (uint64_t)L, (uint64_t)d, dst_row_dev,
+      lens_dev, make_keys(seed), planted, sigma);
   return (int)cudaGetLastError();
 }

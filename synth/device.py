@@ -26,6 +26,8 @@ def lib():
         L.synth_queries.argtypes = [P, i32, i64, i64, i32, i32, u64, i32, i32, i64, i32, P, u64,
                                     i32, f32, f32, P]
         L.synth_queries.restype = i32
+        L.synth_corpus_packed.argtypes = [P, i64, i64, i32, i32, u64, i32, f32, P, P, P]
+        L.synth_corpus_packed.restype = i32
         _lib = L
     return _lib
 
@@ -61,4 +63,20 @@ def queries_(out, qseed: int, *, corpus_seed: int, n_chunks: int, L: int, chunk_
                             float(gen.SIGMA_TOKEN), float(sigma_q), _stream(stream))
     if r != 0:
         raise RuntimeError(f"synth_queries CUDA error {r}")
+    return out
+
+
+def corpus_packed_(out, seed: int, chunk_start: int, dst_row, lens, L: int, kind: str = "planted",
+                   stream=None):
+    """Fill the packed bf16 CUDA tensor out [rows][d] with chunks chunk_start.. (count = len(lens)):
+    chunk c's token j at row dst_row[c] + j (dst_row: CUDA int64, lens: CUDA int32), zero padding up
+    to the chunk's 16-row slot; token values as corpus_() with token stride L."""
+    n = lens.shape[0]
+    d = out.shape[-1]
+    r = lib().synth_corpus_packed(ctypes.c_void_p(out.data_ptr()), chunk_start, n, L, d,
+                                  seed & (2**64 - 1), int(kind == "planted"), float(gen.SIGMA_TOKEN),
+                                  ctypes.c_void_p(dst_row.data_ptr()), ctypes.c_void_p(lens.data_ptr()),
+                                  _stream(stream))
+    if r != 0:
+        raise RuntimeError(f"synth_corpus_packed CUDA error {r}")
     return out

@@ -152,8 +152,8 @@ def test_packed_edge_cases(H):
     idx = packed_index(H, docs, dl)
     S = H.hiper_maxsim_scores(idx, to_dev(qv), np.ones(4, np.int32)).cpu().numpy()
     assert (S < 0).all()
-    with pytest.raises(H.HiperError) as ex:
-        H.hiper_index_build(to_dev(docs.astype(np.float32)).to(torch.bfloat16), dl,
+    with pytest.raises(H.HiperError) as ex:  # a borrowed packed buffer must be bf16
+        H.hiper_index_build(to_dev(docs.astype(np.float32)), dl,
                             flags=H.HIPER_PACKED | H.HIPER_BORROW_TOKENS)
     assert ex.value.name == "HIPER_ERR_INVALID_ARG"
 
@@ -173,3 +173,22 @@ def test_packed_fake_sharding_bitwise(H):
         cand = [(float(s), int(i)) for ps, pi in parts for s, i in zip(ps[r], pi[r]) if i >= 0]
         cand.sort(key=lambda t: (-t[0], t[1]))
         assert [c[1] for c in cand[:k]] == i_ref[r].tolist()
+
+
+def test_packed_borrow_in_place(H):
+    """HIPER_PACKED | HIPER_BORROW_TOKENS: a corpus generated straight into the packed layout and
+    NORM'd in place gives the same layout and results as packing a padded tensor."""
+    from synth import device
+    C, L, d = 500, 256, 128
+    corp, clen, q, qlen = semantic_case(C, L, 9, d)
+    ref = packed_index(H, corp, clen)
+    dst, n_rows = H.hiper_pack_dst_rows(clen)
+    buf = torch.full((n_rows, d), 7.0, dtype=torch.bfloat16, device="cuda")  # junk must not matter
+    device.corpus_packed_(buf, 11, 0, torch.from_numpy(dst).cuda(), torch.from_numpy(clen).cuda(), L)
+    idx = H.hiper_index_build(buf, clen, flags=H.HIPER_PACKED | H.HIPER_BORROW_TOKENS)
+    assert idx.packed and idx.layout_ptr == buf.data_ptr() and idx.n_rows == n_rows
+    got = bits(idx.layout().clone())
+    assert np.array_equal(got, bits(ref.layout().clone()))
+    s1, i1 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(idx, to_dev(q), qlen, 10)]
+    s0, i0 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(ref, to_dev(q), qlen, 10)]
+    assert np.array_equal(i1, i0) and np.array_equal(s1.view(np.uint32), s0.view(np.uint32))

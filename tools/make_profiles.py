@@ -44,7 +44,8 @@ def main():
     md = [f"# Profiles and bench evidence, round {tag}\n",
           "All numbers below come from `tools/run_evidence.sh` on one B200 (gpurun). ncu runs used "
           "`--clock-control none`; a number measured under ncu is never a bench value.\n"]
-    for name in ("bench_final", "bench_ref", "bench_c5", "bench_c2"):
+    for name in ("bench_final", "bench_ref", "bench_c3v", "bench_c3v_dense", "bench_c5", "bench_c2",
+                 "bench_c2_grad"):
         d = jline(os.path.join(G, f"{name}.json"))
         if d is None:
             continue
@@ -99,8 +100,16 @@ def main():
         md.append(f"* dram read+write {dram / 1e9:.1f} GB per launch; algorithmic (corpus once) "
                   f"{alg / 1e9:.1f} GB -> {dram / max(alg, 1):.2f}x")
         md.append(f"* L2 (lts) bytes {vals.get('lts__t_bytes.sum', 0) / 1e12:.2f} TB\n")
+    sp = os.path.join(G, "pipe_stats.log")
+    if os.path.exists(sp):
+        lines = sorted(set(l.strip() for l in open(sp) if l.startswith("[hiper pipe]")))
+        open(os.path.join(P, f"{tag}_pipe_stats.txt"), "w").write("\n".join(lines) + "\n")
+        md.append("## Pipeline statistics (HIPER_PIPE_STATS=1, 300k-chunk runs of config3 / config3v / config5)\n")
+        md.append("MMA-thread waits are issue-side (the tensor pipe may still be busy); drain = cycles an "
+                  "epilogue warp holds an accumulator after it is full.\n\n```\n" + "\n".join(lines) + "\n```\n")
     for rep, label in (("prof_final", "fused MaxSim kernel, config-3 shape at C=100k"),
-                       ("prof_pooled", "pooled kernel, config-5 shape at C=360k")):
+                       ("prof_packed", "fused MaxSim kernel on the packed layout (N4), config3v at C=200k"),
+                       ("prof_pooled", "pooled kernel, config-5 full size (3.6M x 768, Q=4096)")):
         rp = os.path.join(G, f"{rep}.ncu-rep")
         if os.path.exists(rp):
             shutil.copy(rp, os.path.join(P, f"{tag}_{rep}.ncu-rep"))

@@ -1,13 +1,19 @@
-# Round evidence: tests, plain benches, launch list, DRAM traffic of the bench's own fused-kernel launch,
-# and one ncu --set full capture of each fused kernel on a reduced corpus.
+# Round evidence: tests, plain benches of every workload, launch list, DRAM traffic of the bench's own
+# fused-kernel launch, pipeline statistics, and one ncu --set full capture of each fused kernel.
 set -x
 python __graft_entry__.py > gpurun_out/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$? >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 python bench.py --workload config3v > gpurun_out/bench_c3v.json 2> gpurun_out/bench_c3v.err
+timeout 900 python bench.py --workload config3v --no-pack --no-cpu-baseline > gpurun_out/bench_c3v_dense.json 2> gpurun_out/bench_c3v_dense.err
 timeout 900 python bench.py --workload config5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 timeout 900 python bench.py --workload config2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 900 python bench.py --workload config2 --grad --no-cpu-baseline > gpurun_out/bench_c2_grad.json 2> gpurun_out/bench_c2_grad.err
+for W in "" "--workload config3v" "--workload config5"; do
+  HIPER_PIPE_STATS=1 timeout 300 python bench.py $W --chunks 300000 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>> gpurun_out/pipe_stats.log
+done
 B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 600 $B > gpurun_out/plain_b.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1 && \
@@ -15,7 +21,10 @@ timeout 600 $B > gpurun_out/plain_b.log 2>&1 && \
 C="python bench.py --chunks 100000 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 300 $C > gpurun_out/plain_c.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:maxsim -s 1 -c 1 -o gpurun_out/prof_final $C > gpurun_out/ncu_full.log 2>&1
-P="python bench.py --workload config5 --chunks 360000 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+V="python bench.py --workload config3v --chunks 200000 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 300 $V > gpurun_out/plain_v.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:maxsim -s 1 -c 1 -o gpurun_out/prof_packed $V > gpurun_out/ncu_packed.log 2>&1
+P="python bench.py --workload config5 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 300 $P > gpurun_out/plain_p.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:pooled -s 1 -c 1 -o gpurun_out/prof_pooled $P > gpurun_out/ncu_pooled.log 2>&1
 echo done
