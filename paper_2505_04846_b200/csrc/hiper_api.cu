@@ -678,7 +678,7 @@ static int32_t choose_parts(int32_t n_groups, int64_t n_chunks, int num_sms) {
 static int64_t band_bytes() {
   static const int64_t b = [] {
     const char* e = getenv("HIPER_BAND_MB");
-    return e ? (int64_t)atoll(e) << 20 : (int64_t)48 << 20;
+    return e ? (int64_t)atoll(e) << 20 : (int64_t)24 << 20;
   }();
   return b;
 }

@@ -30,9 +30,11 @@ constexpr uint32_t kPairAllocWarp = 8, kPairProducerWarp = 10, kPairMmaWarp = 11
 
 // L2 lockstep.  All pairs of a wave stream the same corpus partition(s); left alone they drift
 // apart by more than the L2 can hold (measured: 5.6 TB of DRAM reads per launch for a 65.5 GB
-// corpus at Q = 1024).  Each leader publishes its position (unit iteration << 20 | chunk offset)
-// every 16 chunks and waits while it is more than `window` chunks ahead of the slowest pair, so the
-// chunks in flight across the GPU stay inside a few MB of L2.  Finished pairs publish ~0u.
+// corpus at Q = 1024).  Each leader publishes its position -- the number of chunks it has streamed
+// so far, continuous across its units (units are equal to within one chunk) -- every 16 chunks and
+// waits while it is more than `window` chunks ahead of the slowest pair, so the chunks in flight
+// across the GPU stay inside a few MB of L2.  (An earlier (unit << 20 | offset) position turned every
+// unit boundary into a grid-wide barrier.)  Finished pairs publish ~0u.
 __device__ __forceinline__ void lockstep_publish(uint32_t* progress, uint32_t pair, uint32_t pos) {
   *reinterpret_cast<volatile uint32_t*>(progress + pair) = pos;
 }
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       prefetch_tmap(&tmap_d);
     }
     int s = 0;
-    uint32_t ph = 0, it = 0;
+    uint32_t ph = 0, it = 0, streamed = 0;  // streamed: chunks of this pair's finished units
     for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
       int32_t g, p;
       int64_t c0, c1;
@@ -176,8 +178,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         }
         if (lane == 0) {
           if (args.progress != nullptr && rank == 0 && ((c - c0) & 15) == 0) {
-            const int64_t off = c - c0 < 0xFFFFF ? c - c0 : 0xFFFFF;
-            const uint32_t pos = (it << 20) | (uint32_t)off;
+            const uint32_t pos = streamed + (uint32_t)(c - c0);
             lockstep_publish(args.progress, pair, pos);
             lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
           }
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         __syncwarp();
         if (++s == S) { s = 0; ph ^= 1u; }
       }
+      streamed += (uint32_t)(c1 - c0);
     }
     if (lane == 0 && args.progress != nullptr && rank == 0) lockstep_publish(args.progress, pair, 0xFFFFFFFFu);
   } else if (warp == kPairMmaWarp) {

@@ -114,13 +114,13 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       prefetch_tmap(&tmap_q);
       prefetch_tmap(&tmap_c);
       int s = 0;
-      uint32_t ph = 0, it = 0;
+      uint32_t ph = 0, it = 0, streamed = 0;  // streamed: chunk tiles of this pair's finished units
       for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
         int32_t qt, p, t0, t1;
         decode(u, qt, p, t0, t1);
         for (int32_t ct = t0; ct < t1; ++ct) {
           if (args.progress != nullptr && rank == 0 && ((ct - t0) & 3) == 0) {
-            const uint32_t pos = (it << 20) | (uint32_t)(ct - t0);
+            const uint32_t pos = streamed + (uint32_t)(ct - t0);  // continuous across units
             lockstep_publish(args.progress, pair, pos);
             lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
           }
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             if (++s == S) { s = 0; ph ^= 1u; }
           }
         }
+        streamed += (uint32_t)(t1 - t0);
       }
       if (args.progress != nullptr && rank == 0) lockstep_publish(args.progress, pair, 0xFFFFFFFFu);
     }

@@ -30,11 +30,14 @@ def main():
                     chunk_lens=torch.from_numpy(lens_all).cuda())
     qlen = gen.lengths(qseed, Q, Lq, True, stream=gen.QLEN)
     ok = True
-    for k in (10, 100):
+    sem_all = gen.semantic_lengths(seed, C, L)  # N4: packed shards of a semantic-length corpus
+    for k, packed in ((10, False), (100, False), (10, True)):
+        lens_use = sem_all if packed else lens_all
+        flags = H.HIPER_PACKED if packed else 0
         c0, c1 = rank * C // world, (rank + 1) * C // world
         shard = torch.empty((c1 - c0, L, d), dtype=torch.bfloat16, device="cuda")
         device.corpus_(shard, seed, c0)
-        idx = H.hiper_index_build(shard, lens_all[c0:c1], id_base=c0)
+        idx = H.hiper_index_build(shard, lens_use[c0:c1], id_base=c0, flags=flags)
         s, i = H.hiper_maxsim_topk(idx, q, qlen, k, comm=comm)
         torch.cuda.synchronize()
         gs = [torch.empty_like(s) for _ in range(world)]
@@ -44,12 +47,13 @@ def main():
         if rank == 0:
             full = torch.empty((C, L, d), dtype=torch.bfloat16, device="cuda")
             device.corpus_(full, seed, 0)
-            fidx = H.hiper_index_build(full, lens_all)
+            fidx = H.hiper_index_build(full, lens_use, flags=flags)
             fs, fi = H.hiper_maxsim_topk(fidx, q, qlen, k)
             for r in range(world):
                 same_i = torch.equal(gi[r], fi)
                 same_s = torch.equal(gs[r].view(torch.int32), fs.view(torch.int32))
-                print(f"k={k} rank{r}: ids equal {same_i}, scores bitwise {same_s}", flush=True)
+                print(f"k={k} packed={packed} rank{r}: ids equal {same_i}, scores bitwise {same_s}",
+                      flush=True)
                 ok &= same_i and same_s
             del full, fidx
         del shard, idx
