@@ -998,12 +998,13 @@ static hiper_status check_ws(const void* ws, size_t have, size_t need) {
   return HIPER_OK;
 }
 
-static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, const hiper_comm* comm);
+static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, const hiper_comm* comm,
+                             bool topk);
 
 extern "C" size_t hiper_maxsim_topk_workspace_size(const hiper_index* ix, int32_t n_q, int32_t k,
                                                    const hiper_comm* comm) {
   if (!ix || n_q < 0 || k < 1) return 0;
-  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, k, comm);
+  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, k, comm, true);
   int num_sms = 148;
   if (cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ix->device) != cudaSuccess) {
     cudaGetLastError();
@@ -1033,11 +1034,27 @@ constexpr int kPooledKP = 16;  // register top-k slots per query thread (k <= 16
 struct PooledPlan {
   int32_t n_qtiles = 0, n_ctiles = 0, n_parts = 0, n_stages = 0, q_pad = 0;
   uint32_t stage_bytes = 32768u, smem_bytes = 0;
-  int grid = 0;
+  int grid = 0, cl = 2;
 };
 
-static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks, PooledPlan& pp) {
-  pp.n_qtiles = (int32_t)((std::max(n_q, 1) + 255) / 256);
+// Pooled top-k cluster shape: 4 = two CTA pairs sharing each chunk tile through TMA multicast
+// (HIPER_POOLED_MC=1), 2 = one pair per cluster.
+static int pooled_cluster(bool topk) {
+  static const int cl = [] {
+    const char* e = getenv("HIPER_POOLED_MC");
+    return (e && e[0] == '1') ? 4 : 2;
+  }();
+  return topk ? cl : 2;
+}
+static int32_t pooled_qtiles(int32_t n_q, int cl) {
+  const int32_t qt = (int32_t)((std::max(n_q, 1) + 255) / 256);
+  return cl == 4 ? (qt + 1) / 2 * 2 : qt;
+}
+
+static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks, PooledPlan& pp,
+                                bool topk = true) {
+  pp.cl = pooled_cluster(topk);
+  pp.n_qtiles = pooled_qtiles(n_q, pp.cl);
   pp.q_pad = pp.n_qtiles * 256;
   const int64_t ct = (n_chunks + 255) / 256;
   if (ct > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many chunks");
@@ -1046,12 +1063,13 @@ static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks
   // ablation only: fewer resident pairs (the per-SM vs chip-wide L2->SMEM throughput experiment);
   // must keep choose_parts() equal to the workspace sizing (it does for divisors of num_sms / 2)
   if (const char* e = getenv("HIPER_POOLED_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));
-  pp.n_parts = choose_parts(pp.n_qtiles, pp.n_ctiles, di.num_sms / 2);
+  pp.n_parts = choose_parts(pp.n_qtiles / (pp.cl / 2), pp.n_ctiles, di.num_sms / pp.cl);
   const uint32_t fixed = 1024u + 512u;  // align slack, barriers
   pp.n_stages = (int32_t)std::min<uint32_t>(8u, ((uint32_t)di.max_smem - fixed) / pp.stage_bytes);
   if (pp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory");
   pp.smem_bytes = fixed + pp.n_stages * pp.stage_bytes;
-  pp.grid = (int)std::min<int64_t>((int64_t)pp.n_qtiles * pp.n_parts, pairs) * 2;
+  pp.grid = (int)std::min<int64_t>((int64_t)(pp.n_qtiles / (pp.cl / 2)) * pp.n_parts,
+                                   pairs / (pp.cl / 2)) * pp.cl;
   return HIPER_OK;
 }
 
@@ -1059,7 +1077,8 @@ template <int MODE>
 static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, const CUtensorMap& tc,
                                   const PooledArgs& a, cudaStream_t stream) {
   if (pp.grid == 0 || pp.n_parts == 0) return HIPER_OK;
-  auto kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
+  auto kern = pp.cl == 4 ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 4>
+                         : pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
   if (MODE == 1 && debug_mode() == 1) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 1>;
   if (MODE == 1 && debug_mode() == 2) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 2>;
   if (MODE == 1 && debug_mode() == 3) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 3>;
@@ -1072,7 +1091,7 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = (unsigned)pp.cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -1143,7 +1162,7 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   DevInfo di;
   TRY(device_info(di));
   PooledPlan pp;
-  TRY(plan_pooled(di, n_q, ix->n, pp));
+  TRY(plan_pooled(di, n_q, ix->n, pp, dense_scores == nullptr));
   const int32_t world = comm ? comm->world : 1;
   PooledWs w;
   pooled_ws_layout(n_q, dim, pp.n_parts, pp.q_pad, dense_scores ? 1 : k, world, comm != nullptr, w);
@@ -1183,7 +1202,13 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
     alignas(64) CUtensorMap tq;
     TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
     if (dense_scores) return launch_pooled<0>(pp, tq, ix->tmap, a, stream);
-    TRY(launch_pooled<1>(pp, tq, ix->tmap, a, stream));
+    if (pp.cl == 4) {  // chunk halves of 64 rows, multicast to both pairs of a cluster
+      alignas(64) CUtensorMap tc64;
+      TRY(make_tmap(&tc64, ix->tok, ix->n, dim, 64));
+      TRY(launch_pooled<1>(pp, tq, tc64, a, stream));
+    } else {
+      TRY(launch_pooled<1>(pp, tq, ix->tmap, a, stream));
+    }
   }
   const int32_t n_lists = ix->n > 0 ? pp.n_parts * kEpiGroups : 0;
   const int64_t list_stride = (int64_t)pp.q_pad * k;
@@ -1196,16 +1221,18 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   return launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream);
 }
 
-static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, const hiper_comm* comm) {
+static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, const hiper_comm* comm,
+                             bool topk) {
   int num_sms = 148;
   if (cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ix->device) != cudaSuccess) {
     cudaGetLastError();
     num_sms = 148;
   }
-  const int32_t qt = (std::max(n_q, 1) + 255) / 256;
+  const int cl = pooled_cluster(topk);
+  const int32_t qt = pooled_qtiles(n_q, cl);
   const int32_t ct = (int32_t)((ix->n + 255) / 256);
   PooledWs w;
-  pooled_ws_layout(n_q, ix->dim, choose_parts(qt, ct, num_sms / 2), qt * 256, k,
+  pooled_ws_layout(n_q, ix->dim, choose_parts(qt / (cl / 2), ct, num_sms / cl), qt * 256, k,
                    comm ? comm->world : 1, comm != nullptr, w);
   return w.total;
 }
@@ -1307,7 +1334,7 @@ static void scores_ws_layout(int32_t n_q, int32_t dim, ScoresWs& w) {
 
 extern "C" size_t hiper_maxsim_scores_workspace_size(const hiper_index* ix, int32_t n_q) {
   if (!ix || n_q < 0) return 0;
-  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, 1, nullptr);
+  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, 1, nullptr, false);
   ScoresWs w;
   scores_ws_layout(n_q, ix->dim, w);
   return w.total;
@@ -1532,7 +1559,7 @@ static hiper_status pooled_dense_raw(const DevInfo& di, const __nv_bfloat16* qla
                                      const __nv_bfloat16* clayout, int64_t m, int32_t dim, float* S,
                                      int64_t ld, cudaStream_t stream) {
   PooledPlan pp;
-  TRY(plan_pooled(di, n_q, m, pp));
+  TRY(plan_pooled(di, n_q, m, pp, false));
   alignas(64) CUtensorMap tq, tc;
   TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
   TRY(make_tmap(&tc, clayout, m, dim, 128));
@@ -1799,7 +1826,7 @@ static void two_stage_ws_layout(const hiper_index* pix, const hiper_index* tix, 
                                 int32_t k1, TwoStageWs& w) {
   size_t off = 0;
   w.pooled = off;
-  w.pooled_bytes = pooled_ws_size(pix, n_q, k1, nullptr);
+  w.pooled_bytes = pooled_ws_size(pix, n_q, k1, nullptr, true);
   off = align_up(off + w.pooled_bytes, 1024);
   w.s1_scores = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 4, 256);

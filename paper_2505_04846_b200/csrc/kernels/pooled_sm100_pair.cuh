@@ -57,7 +57,11 @@ __device__ __forceinline__ float pooled_thr_score(uint64_t thr) {
 // DBG (ablation builds only, HIPER_DEBUG_MODE): 1 = the epilogue only waits/releases the
 // accumulator (no TMEM reads, no top-k); 2 = additionally no TMA after the first stage fill;
 // 3 = the epilogue reads TMEM but does no arithmetic; 4 = arithmetic without TMEM reads.
-template <int MODE, int KP, int DBG = 0>
+// CL = CTAs per cluster.  CL == 2: one CTA pair per cluster.  CL == 4: two pairs that score two
+// query tiles (2qq, 2qq + 1) against the same chunk tiles; each chunk-tile K-block half (128 rows)
+// needed by CTA r of both pairs is loaded once, half by each of them, and TMA-multicast to both, so
+// the chunk operand costs half the L2 reads.  tmap_c then has a 64-row box.
+template <int MODE, int KP, int DBG = 0, int CL = 2>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     pooled_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_c, const PooledArgs args) {
@@ -65,9 +69,14 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   using namespace ptx;
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
-  const uint32_t pair = cluster_id_x();
-  const uint32_t n_pairs = nclusters_x();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u;      // CTA within its pair (0 = pair leader)
+  const uint32_t lead = crank & ~1u;     // cluster rank of this pair's leader
+  const uint32_t p2 = crank >> 1;        // pair within the cluster
+  const uint32_t pair = cluster_id_x() * (CL / 2) + p2;
+  const uint32_t n_pairs = nclusters_x() * (CL / 2);
+  const uint16_t pair_mask = (uint16_t)(3u << lead);
+  const uint16_t all_mask = (uint16_t)((1u << CL) - 1u);
 
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t sStage = base;  // n_stages x {A 16 KiB | B 16 KiB}
@@ -84,7 +93,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(bar_full(s), 1);
-      mbar_init(bar_empty(s), 1);
+      mbar_init(bar_empty(s), CL / 2);  // every pair whose operands this stage (also) holds
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_tfull(b), 1);
@@ -101,10 +110,15 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr_generic);
 
-  const int32_t n_units = args.n_qtiles * args.n_parts;
+  // units: (query tile, partition) for CL == 2; (query-tile pair, partition) for CL == 4, the two
+  // pairs of a cluster taking query tiles 2qq and 2qq + 1 of the same unit
+  const int32_t n_qu = args.n_qtiles / (CL / 2);
+  const int32_t n_units = n_qu * args.n_parts;
+  const uint32_t ustride = n_pairs / (CL / 2);  // clusters
+  const uint32_t ufirst = pair / (CL / 2);
   auto decode = [&](int32_t u, int32_t& qt, int32_t& p, int32_t& t0, int32_t& t1) {
-    p = u / args.n_qtiles;
-    qt = u - p * args.n_qtiles;
+    p = u / n_qu;
+    qt = (u - p * n_qu) * (CL / 2) + (int32_t)p2;
     t0 = (int32_t)((int64_t)p * args.n_ctiles / args.n_parts);
     t1 = (int32_t)((int64_t)(p + 1) * args.n_ctiles / args.n_parts);
   };
@@ -115,7 +129,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       prefetch_tmap(&tmap_c);
       int s = 0;
       uint32_t ph = 0, it = 0, streamed = 0;  // streamed: chunk tiles of this pair's finished units
-      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
+      for (int32_t u = (int32_t)ufirst; u < n_units; u += (int32_t)ustride, ++it) {
         int32_t qt, p, t0, t1;
         decode(u, qt, p, t0, t1);
         for (int32_t ct = t0; ct < t1; ++ct) {
@@ -132,10 +146,16 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               continue;
             }
             if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
-            const uint32_t full_leader = mapa_shared(bar_full(s), 0);
+            const uint32_t full_leader = mapa_shared(bar_full(s), lead);
             const uint32_t st = sStage + s * args.stage_bytes;
             tma_load_2d_pair(st, &tmap_q, full_leader, kb * 64, qt * 256 + (int32_t)rank * 128);
-            tma_load_2d_pair(st + 16384u, &tmap_c, full_leader, kb * 64, ct * 256 + (int32_t)rank * 128);
+            if constexpr (CL == 2) {
+              tma_load_2d_pair(st + 16384u, &tmap_c, full_leader, kb * 64, ct * 256 + (int32_t)rank * 128);
+            } else {  // my 64-row half of the 128 chunk rows CTA `rank` of both pairs needs
+              tma_load_2d_pair_mc(st + 16384u + p2 * 8192u, &tmap_c, full_leader, kb * 64,
+                                  ct * 256 + (int32_t)rank * 128 + (int32_t)p2 * 64,
+                                  (uint16_t)((1u << rank) | (1u << (2u + rank))));
+            }
             if (++s == S) { s = 0; ph ^= 1u; }
           }
         }
@@ -150,7 +170,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       uint32_t ph = 0, t = 0;
       long long st_acc = 0, st_full = 0;
       const long long st_t0 = clock64();
-      for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
+      for (int32_t u = (int32_t)ufirst; u < n_units; u += (int32_t)ustride) {
         int32_t qt, p, t0, t1;
         decode(u, qt, p, t0, t1);
         for (int32_t ct = t0; ct < t1; ++ct, ++t) {
@@ -171,10 +191,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               mma_bf16_ss_pair(d_tmem, umma_desc_sw128(st + kk * 32),
                                umma_desc_sw128(st + 16384u + kk * 32), idesc,
                                (kb | kk) != 0 ? 1u : 0u);
-            mma_commit_pair_mc(bar_empty(s), 0x3);
+            mma_commit_pair_mc(bar_empty(s), all_mask);  // every CTA that wrote into this stage
             if (++s == S) { s = 0; ph ^= 1u; }
           }
-          mma_commit_pair_mc(bar_tfull(acc), 0x3);
+          mma_commit_pair_mc(bar_tfull(acc), pair_mask);
         }
       }
       if (args.stats) {
@@ -187,11 +207,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     const uint32_t qslot = warp & 3u;
     const uint32_t grp = warp >> 2;
     const uint32_t taddr_base = tmem_base + ((qslot * 32u) << 16) + grp * kAccStride;
-    const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), 0);
+    const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), lead);
     const int32_t k = args.k;
     uint32_t t = 0, mine = 0;
     long long st_drain = 0, st_ewait = 0, st_tiles = 0, st_any = 0, st_ins = 0;
-    for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
+    for (int32_t u = (int32_t)ufirst; u < n_units; u += (int32_t)ustride) {
       int32_t qt, p, t0, t1;
       decode(u, qt, p, t0, t1);
       const int32_t q = qt * 256 + (int32_t)rank * 128 + (int32_t)qslot * 32 + (int32_t)lane;
