@@ -252,15 +252,20 @@ HIPER_API hiper_status hiper_coltrast_scores_loss_grad(
  * token_idx, the token rows of the SAME chunks (same n and id_base), keeping the final top-k
  * (ColBERTv2's retrieve-then-rerank; SPEC.md:268-276 rerank; score desc, id asc).
  *   q_pooled device [n_q][pooled dim]; q_tokens device [n_q][q_max_len][token dim]; q_lens HOST.
- *   1 <= k <= k1 <= 16.  Single shard (comm not supported on this path yet). */
+ *   1 <= k <= k1 <= 16.
+ *   comm: NULL = this shard only.  With a communicator every rank passes the same queries and its
+ *   own shard (both indexes with the shard's id_base): stage 1 is the global pooled top-k1 (one
+ *   all-gather), each rank re-scores the candidates it owns, and one more all-gather + merge gives
+ *   every rank the identical global top-k -- bitwise the single-GPU result on the whole corpus. */
 HIPER_API size_t hiper_two_stage_workspace_size(const hiper_index* pooled_idx,
                                                 const hiper_index* token_idx, int32_t n_q,
-                                                int32_t k1);
+                                                int32_t k1, const hiper_comm* comm);
 HIPER_API hiper_status hiper_two_stage_topk(const hiper_index* pooled_idx,
                                             const hiper_index* token_idx, const void* q_pooled,
                                             const void* q_tokens, hiper_dtype dtype,
                                             const int32_t* q_lens, int32_t n_q, int32_t q_max_len,
-                                            int32_t k1, int32_t k, uint32_t flags, void* workspace,
+                                            int32_t k1, int32_t k, uint32_t flags,
+                                            const hiper_comm* comm, void* workspace,
                                             size_t workspace_bytes, float* out_scores,
                                             int64_t* out_ids, hiper_stream_t stream);
 

@@ -98,8 +98,8 @@ def lib():
         "hiper_profile_enable": ([i32], None),
         "hiper_coltrast_loss_workspace_size": ([i32, i32, i32, i32, i32, P], sz),
         "hiper_coltrast_grad_workspace_size": ([i32, i32, i32, i32], sz),
-        "hiper_two_stage_workspace_size": ([P, P, i32, i32], sz),
-        "hiper_two_stage_topk": ([P, P, P, P, i32, P, i32, i32, i32, i32, u32, P, sz, P, P, P], i32),
+        "hiper_two_stage_workspace_size": ([P, P, i32, i32, P], sz),
+        "hiper_two_stage_topk": ([P, P, P, P, i32, P, i32, i32, i32, i32, u32, P, P, sz, P, P, P], i32),
         "hiper_coltrast_scores_loss_grad": ([P, P, i32, i32, P, P, i32, i32, i32, i32, u32, P,
                                              ctypes.c_float, P, sz, P, P, P, P, P], i32),
         "hiper_coltrast_loss": ([P, P, i32, P, P, i32, i32, P, P, i32, i32, i32, u32, i32,
@@ -502,21 +502,23 @@ def hiper_coltrast_scores_loss_grad(q_tokens, q_lens, d_tokens, d_lens, *, pos_i
 
 
 def hiper_two_stage_topk(pooled_index: Index, token_index: Index, q_pooled, q_tokens, q_lens,
-                         k1: int, k: int, *, flags: int = 0, stream=None):
-    """NEXT N3: pooled top-k1 then exact MaxSim rerank -> (scores [n_q][k], ids [n_q][k])."""
+                         k1: int, k: int, *, flags: int = 0, comm: Comm | None = None, stream=None):
+    """NEXT N3: pooled top-k1 then exact MaxSim rerank -> (scores [n_q][k], ids [n_q][k]).
+    With comm, every rank passes its shard's two indexes and receives the global result."""
     torch = _torch()
     n_q, q_max_len, _ = q_tokens.shape
     qp = q_pooled.reshape(n_q, -1)
     if qp.dtype != q_tokens.dtype:
         raise HiperError(1, "pooled and token queries must share a dtype")
     ql = _host_i32(q_lens)
-    nb = lib().hiper_two_stage_workspace_size(pooled_index.handle, token_index.handle, n_q, k1)
+    ch = comm.handle if comm else None
+    nb = lib().hiper_two_stage_workspace_size(pooled_index.handle, token_index.handle, n_q, k1, ch)
     ws, wp, wn = _workspace(nb, q_tokens.device)
     s = torch.empty((n_q, k), dtype=torch.float32, device=q_tokens.device)
     i = torch.empty((n_q, k), dtype=torch.int64, device=q_tokens.device)
     _check(lib().hiper_two_stage_topk(pooled_index.handle, token_index.handle, _dev_ptr(qp.contiguous()),
                                       _dev_ptr(q_tokens), _dtype_code(q_tokens), _ptr(ql), n_q,
-                                      q_max_len, k1, k, flags, ctypes.c_void_p(wp), wn,
+                                      q_max_len, k1, k, flags, ch, ctypes.c_void_p(wp), wn,
                                       _dev_ptr(s), _dev_ptr(i), _stream_ptr(stream)))
     s._hiper_ws = ws
     return s, i

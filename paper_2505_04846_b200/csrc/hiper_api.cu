@@ -1820,13 +1820,13 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
 // per pair scoring the union of their candidates.
 struct TwoStageWs {
   size_t pooled = 0, pooled_bytes = 0, s1_scores = 0, s1_ids = 0, slots = 0, status = 0, qlens = 0,
-         qlayout = 0, S2 = 0, total = 0;
+         qlayout = 0, S2 = 0, local = 0, gathered = 0, total = 0;
 };
 static void two_stage_ws_layout(const hiper_index* pix, const hiper_index* tix, int32_t n_q,
-                                int32_t k1, TwoStageWs& w) {
+                                int32_t k1, const hiper_comm* comm, TwoStageWs& w) {
   size_t off = 0;
   w.pooled = off;
-  w.pooled_bytes = pooled_ws_size(pix, n_q, k1, nullptr, true);
+  w.pooled_bytes = pooled_ws_size(pix, n_q, k1, comm, true);
   off = align_up(off + w.pooled_bytes, 1024);
   w.s1_scores = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 4, 256);
@@ -1842,15 +1842,19 @@ static void two_stage_ws_layout(const hiper_index* pix, const hiper_index* tix, 
   off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * tix->dim * 2, 1024);
   w.S2 = off;
   off = align_up(off + (size_t)n_q_pad_of(n_q) * 8 * k1 * 4, 1024);
+  w.local = off;  // multi-rank: this rank's re-scored top-k keys, then every rank's
+  if (comm) off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 8, 256);
+  w.gathered = off;
+  if (comm) off = align_up(off + (size_t)comm->world * std::max(n_q, 1) * k1 * 8, 256);
   w.total = off;
 }
 
 extern "C" size_t hiper_two_stage_workspace_size(const hiper_index* pooled_idx,
                                                  const hiper_index* token_idx, int32_t n_q,
-                                                 int32_t k1) {
+                                                 int32_t k1, const hiper_comm* comm) {
   if (!pooled_idx || !token_idx || n_q < 0 || k1 < 1) return 0;
   TwoStageWs w;
-  two_stage_ws_layout(pooled_idx, token_idx, n_q, k1, w);
+  two_stage_ws_layout(pooled_idx, token_idx, n_q, k1, comm, w);
   return w.total;
 }
 
@@ -1858,9 +1862,9 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
                                              const void* q_pooled, const void* q_tokens,
                                              hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
                                              int32_t q_max_len, int32_t k1, int32_t k,
-                                             uint32_t flags, void* workspace, size_t workspace_bytes,
-                                             float* out_scores, int64_t* out_ids,
-                                             hiper_stream_t stream_) {
+                                             uint32_t flags, const hiper_comm* comm, void* workspace,
+                                             size_t workspace_bytes, float* out_scores,
+                                             int64_t* out_ids, hiper_stream_t stream_) {
   g_launches = 0;
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!pix || !tix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
@@ -1882,21 +1886,23 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   DevInfo di;
   TRY(device_info(di));
   TwoStageWs w;
-  two_stage_ws_layout(pix, tix, n_q, k1, w);
+  two_stage_ws_layout(pix, tix, n_q, k1, comm, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
+  const bool multi = comm != nullptr && comm->world > 1;
   uint8_t* ws = (uint8_t*)workspace;
   float* s1s = (float*)(ws + w.s1_scores);
   int64_t* s1i = (int64_t*)(ws + w.s1_ids);
   int32_t* slots = (int32_t*)(ws + w.slots);
   // stage 1: pooled top-k1 (pooled queries have one row each; lengths all 1)
   std::vector<int32_t> ones(n_q, 1);
-  TRY(pooled_search(pix, q_pooled, dtype, ones.data(), n_q, pix->dim, k1, flags, nullptr,
+  // (with comm: the GLOBAL pooled top-k1, identical on every rank)
+  TRY(pooled_search(pix, q_pooled, dtype, ones.data(), n_q, pix->dim, k1, flags, comm,
                     ws + w.pooled, w.pooled_bytes, s1s, s1i, nullptr, stream));
   int32_t launches = g_launches;
   // stage 2: slots, token query prep, MaxSim over each row group's candidate union
   const int32_t nqp = n_q_pad_of(n_q);
   ids_to_slots_kernel<<<(unsigned)(((int64_t)nqp * k1 + 255) / 256), 256, 0, stream>>>(
-      s1i, n_q, nqp, k1, pix->id_base, slots);
+      s1i, n_q, nqp, k1, pix->id_base, pix->n, slots);
   CUDA_TRY(cudaGetLastError());
   uint32_t* status = (uint32_t*)(ws + w.status);
   int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
@@ -1933,10 +1939,23 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   a.score_ld = n_slots;
   a.cand = slots;
   TRY(launch_maxsim(0, 1, kp, tq, tix->tmap_half, a, stream));
+  if (!multi) {
+    rerank_select_kernel<1><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, n_slots, slots, k1, n_q,
+                                                                tix->id_base, k, out_scores, out_ids);
+    CUDA_TRY(cudaGetLastError());
+    g_launches += launches + 2;
+    return HIPER_OK;
+  }
+  // multi-rank: this rank's re-scored candidates -> top-k keys; all-gather; the same merge on every
+  // rank (keys are unique and every candidate is scored by its owner: bitwise the 1-GPU answer)
+  uint64_t* local = (uint64_t*)(ws + w.local);
+  uint64_t* gathered = (uint64_t*)(ws + w.gathered);
   rerank_select_kernel<1><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, n_slots, slots, k1, n_q,
-                                                              tix->id_base, k, out_scores, out_ids);
+                                                              tix->id_base, k, nullptr, nullptr, local);
   CUDA_TRY(cudaGetLastError());
-  g_launches += launches + 2;
+  NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, comm->comm, stream));
+  TRY(launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream));
+  g_launches += launches + 2;  // + stage 1, ids_to_slots, rerank_select
   return HIPER_OK;
 }
 

@@ -342,33 +342,32 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
 #pragma unroll
           for (int g = 14; g >= 0; --g)
             m16[g] = ((gstart >> (g + 1)) & 1u) ? m16[g] : fmaxf(m16[g], m16[g + 1]);
-          // Pass 3: the masked sum over query tokens for every group (16 independent butterflies,
-          // the dense kernel's fixed order); only chunk-start groups are results.  Top-k: a score
+          // Pass 3: the masked sum over query tokens of each chunk (a butterfly in the dense kernel's
+          // fixed order, only for chunk-start groups: warp-uniform branches).  Top-k: a score
           // pre-filter against the list threshold, exact key test and insert for the rare rest.
           const uint32_t starts = gstart & (n_grp >= 16 ? 0xFFFFu : ((1u << n_grp) - 1u));
+          const uint32_t thr_hi = (uint32_t)(topk.thresh >> 32);
           float sums[16];
+          uint32_t cand = 0u;
 #pragma unroll
           for (int g = 0; g < 16; ++g) {
-            float sv = ((int32_t)lane < lq) ? m16[g] : 0.0f;
+            sums[g] = 0.0f;
+            if ((starts >> g) & 1u) {
+              float sv = ((int32_t)lane < lq) ? m16[g] : 0.0f;
 #pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-            sums[g] = sv + 0.0f;  // canonical +0
-          }
-          if constexpr (MODE == 0) {
-#pragma unroll
-            for (int g = 0; g < 16; ++g) {
-              if ((starts >> g) & 1u) {
+              for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+              sv += 0.0f;  // canonical +0
+              sums[g] = sv;
+              if constexpr (MODE == 0) {
                 const int e = __popc(gstart & ((1u << g) - 1u));
                 const int32_t chunk = (int32_t)__shfl_sync(0xffffffffu, rec, 16 + e);
-                if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk] = sums[g];
+                if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk] = sv;
+              } else {
+                cand |= (uint32_t)(float_orderable(sv) >= thr_hi) << g;
               }
             }
-          } else {
-            const uint32_t thr_hi = (uint32_t)(topk.thresh >> 32);
-            uint32_t cand = 0u;
-#pragma unroll
-            for (int g = 0; g < 16; ++g)
-              cand |= (uint32_t)(((starts >> g) & 1u) && float_orderable(sums[g]) >= thr_hi) << g;
+          }
+          if constexpr (MODE == 1) {
             while (cand != 0u) {
               const int g = __ffs(cand) - 1;
               cand &= cand - 1u;

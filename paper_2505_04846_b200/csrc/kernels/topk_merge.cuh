@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(256) rerank_select_kernel(const float* __restr
                                                             const int32_t* __restrict__ cand,
                                                             int32_t K1, int32_t n_q, int64_t id_base,
                                                             int32_t k, float* __restrict__ out_scores,
-                                                            int64_t* __restrict__ out_ids) {
+                                                            int64_t* __restrict__ out_ids,
+                                                            uint64_t* __restrict__ out_keys = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const int32_t q = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (q >= n_q) return;
@@ -106,20 +107,23 @@ __global__ void __launch_bounds__(256) rerank_select_kernel(const float* __restr
     const int i = r * 32 + (int)lane;
     if (i < k) {
       const uint64_t key = top.v[r];
-      out_scores[(int64_t)q * k + i] = key ? key_score(key) : -INFINITY;
-      out_ids[(int64_t)q * k + i] = key ? key_id(key) : -1;
+      if (out_keys) out_keys[(int64_t)q * k + i] = key;
+      if (out_scores) out_scores[(int64_t)q * k + i] = key ? key_score(key) : -INFINITY;
+      if (out_ids) out_ids[(int64_t)q * k + i] = key ? key_id(key) : -1;
     }
   }
 }
 
-// Stage-1 ids (int64 global, -1 = none) -> stage-2 slot table [n_q_pad][K1] of local chunk indices.
+// Stage-1 ids (int64 global, -1 = none) -> stage-2 slot table [n_q_pad][K1] of local chunk indices;
+// ids outside this shard [id_base, id_base + n) (re-scored by the rank that owns them) -> -1.
 __global__ void ids_to_slots_kernel(const int64_t* __restrict__ ids, int32_t n_q, int32_t n_q_pad,
-                                    int32_t K1, int64_t id_base, int32_t* __restrict__ slots) {
+                                    int32_t K1, int64_t id_base, int64_t n,
+                                    int32_t* __restrict__ slots) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)n_q_pad * K1) return;
   const int64_t q = e / K1;
   const int64_t id = q < n_q ? ids[e] : -1;
-  slots[e] = id >= 0 ? (int32_t)(id - id_base) : -1;
+  slots[e] = (id >= id_base && id < id_base + n) ? (int32_t)(id - id_base) : -1;
 }
 
 }  // namespace hiper

@@ -44,8 +44,8 @@ def main():
     md = [f"# Profiles and bench evidence, round {tag}\n",
           "All numbers below come from `tools/run_evidence.sh` on one B200 (gpurun). ncu runs used "
           "`--clock-control none`; a number measured under ncu is never a bench value.\n"]
-    for name in ("bench_final", "bench_ref", "bench_c3v", "bench_c3v_dense", "bench_c5", "bench_c2",
-                 "bench_c2_grad"):
+    for name in ("bench_final", "bench_ref", "bench_c3_q64", "bench_c3v", "bench_c3v_dense",
+                 "bench_c4v_n1", "bench_c5", "bench_c2", "bench_c2_grad"):
         d = jline(os.path.join(G, f"{name}.json"))
         if d is None:
             continue

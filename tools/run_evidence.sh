@@ -8,6 +8,8 @@ timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_fi
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 python bench.py --workload config3v > gpurun_out/bench_c3v.json 2> gpurun_out/bench_c3v.err
 timeout 900 python bench.py --workload config3v --no-pack --no-cpu-baseline > gpurun_out/bench_c3v_dense.json 2> gpurun_out/bench_c3v_dense.err
+timeout 900 python bench.py --queries 64 --no-cpu-baseline > gpurun_out/bench_c3_q64.json 2> gpurun_out/bench_c3_q64.err
+timeout 1200 python bench.py --workload config4v --queries 256 --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/bench_c4v_n1.json 2> gpurun_out/bench_c4v_n1.err
 timeout 900 python bench.py --workload config5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 timeout 900 python bench.py --workload config2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
 timeout 900 python bench.py --workload config2 --grad --no-cpu-baseline > gpurun_out/bench_c2_grad.json 2> gpurun_out/bench_c2_grad.err
