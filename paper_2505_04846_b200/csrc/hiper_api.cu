@@ -1693,7 +1693,7 @@ extern "C" hiper_status hiper_coltrast_loss(
 
 // ============================================================================ N1: L_LI backward
 struct GradWs {
-  size_t base = 0, amax = 0, G = 0, total = 0;
+  size_t base = 0, amax = 0, G = 0, sorted = 0, bucket = 0, total = 0;
   ColtrastWs cw;
 };
 static void grad_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim, GradWs& w) {
@@ -1703,6 +1703,10 @@ static void grad_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t 
   off = align_up(off + (size_t)std::max(n_q, 1) * std::max(n_d, 1) * 32, 1024);
   w.G = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * std::max(n_d, 1) * 4, 1024);
+  w.sorted = off;  // inverted argmax map per doc: [n_d][n_q * 32] u16 entries + [n_d][258] offsets
+  off = align_up(off + (size_t)std::max(n_q, 1) * 32 * std::max(n_d, 1) * 2, 1024);
+  w.bucket = off;
+  off = align_up(off + (size_t)std::max(n_d, 1) * 258 * 4, 1024);
   w.total = off;
 }
 
@@ -1795,10 +1799,18 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     CUDA_TRY(cudaGetLastError());
     auto gk = grad_d_kernel<VPL, Tin>;
     CUDA_TRY(set_max_smem((const void*)gk, (int)dsmem));
-    gk<<<n_d, 256, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
-                                          (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d);
+    uint16_t* srt = (uint16_t*)(ws + w.sorted);
+    int32_t* bkt = (int32_t*)(ws + w.bucket);
+    // sort-only pass (one block per doc), then one warp per output row for the gathers
+    gk<<<(unsigned)n_d, 256, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
+                                              (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d,
+                                              srt, bkt);
     CUDA_TRY(cudaGetLastError());
-    g_launches += 2;
+    const int64_t drows = (int64_t)n_d * d_max_len;
+    grad_d_gather_kernel<VPL, Tin><<<(unsigned)((drows + 7) / 8), 256, 0, stream>>>(
+        G, n_q, n_d, qlayout, srt, bkt, (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d);
+    CUDA_TRY(cudaGetLastError());
+    g_launches += 3;
     return HIPER_OK;
   };
   using I2 = std::integral_constant<int, 2>;

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) grad_q_kernel(const float* __restrict__ G
   float g[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) g[v] = 0.0f;
-#pragma unroll 4
+#pragma unroll 8
   for (int32_t j = 0; j < M; ++j) {
     const float gij = G[(int64_t)i * M + j];
     const int32_t u = amax[((int64_t)i * M + j) * 32 + t];
@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(256) grad_q_kernel(const float* __restrict__ G
 }
 
 // One block (8 warps) per doc j: invert the argmax map with a stable counting sort in SMEM, then
-// gather-sum each output row in (i, t) order.
+// gather-sum each output row in (i, t) order.  With sorted_out / base_out set the block only sorts
+// and stores the inverted map; grad_d_gather_kernel then runs one warp per output row.
 //  1. stage a(., ., j) (n_q x 32 bytes), G(., j) and q_lens in SMEM;
 //  2. warp w histograms its contiguous eighth of the entries (match_any per 32 entries);
 //  3. block-wide offsets: bucket u of warp w starts at base[u] + sum_{w' < w} hist[w'][u];
@@ -126,7 +127,9 @@ __global__ void __launch_bounds__(256) grad_d_kernel(const float* __restrict__ G
                                                      int32_t ld_pad, const Tin* __restrict__ xd,
                                                      int32_t d_max_len, const int32_t* __restrict__ d_lens,
                                                      uint32_t assume_normalized,
-                                                     float* __restrict__ grad_d) {
+                                                     float* __restrict__ grad_d,
+                                                     uint16_t* __restrict__ sorted_out = nullptr,
+                                                     int32_t* __restrict__ base_out = nullptr) {
   constexpr int D = VPL * 32;
   constexpr int NB = 257;  // 256 buckets + 1 for padding entries (t >= len_q)
   extern __shared__ uint8_t smem[];
@@ -193,6 +196,11 @@ __global__ void __launch_bounds__(256) grad_d_kernel(const float* __restrict__ G
   }
   __syncthreads();
   const int32_t lj = d_lens[j];
+  if (sorted_out != nullptr) {  // sort-only mode: hand the inverted map to grad_d_gather_kernel
+    for (int32_t x = threadIdx.x; x < E; x += blockDim.x) sorted_out[(int64_t)j * E + x] = sorted[x];
+    for (int32_t x = threadIdx.x; x <= NB; x += blockDim.x) base_out[(int64_t)j * (NB + 1) + x] = base[x];
+    return;
+  }
   for (int32_t u = warp; u < d_max_len; u += 8) {
     float* out = grad_d + ((int64_t)j * d_max_len + u) * D;
     if (u >= lj) {
@@ -231,6 +239,63 @@ __global__ void __launch_bounds__(256) grad_d_kernel(const float* __restrict__ G
     norm_backward_row<VPL, Tin>(xd + ((int64_t)j * d_max_len + u) * D, g, assume_normalized != 0,
                                 out, lane);
   }
+}
+
+// One warp per doc output row (j, u): gather-sum G_ij qn_{i,t} over the row's bucket of the inverted
+// argmax map (sorted (i, t) order from grad_d_kernel's sort-only mode: deterministic), 16 gathers in
+// flight, then NORM's Jacobian.  65,536 warps at B = 256 instead of 256 blocks.
+template <int VPL, typename Tin>
+__global__ void __launch_bounds__(256) grad_d_gather_kernel(const float* __restrict__ G, int32_t B,
+                                                            int32_t M, const __nv_bfloat16* __restrict__ qlay,
+                                                            const uint16_t* __restrict__ sorted,
+                                                            const int32_t* __restrict__ base,
+                                                            const Tin* __restrict__ xd, int32_t d_max_len,
+                                                            const int32_t* __restrict__ d_lens,
+                                                            uint32_t assume_normalized,
+                                                            float* __restrict__ grad_d) {
+  constexpr int D = VPL * 32;
+  constexpr int NB = 257;
+  const uint32_t lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= (int64_t)M * d_max_len) return;
+  const int32_t j = (int32_t)(row / d_max_len), u = (int32_t)(row % d_max_len);
+  float* out = grad_d + row * D;
+  if (u >= d_lens[j]) {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) out[lane * VPL + v] = 0.0f;
+    return;
+  }
+  const int32_t E = B * 32;
+  const uint16_t* srt = sorted + (int64_t)j * E;
+  const int32_t h0 = base[(int64_t)j * (NB + 1) + u], h1 = base[(int64_t)j * (NB + 1) + u + 1];
+  float g[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) g[v] = 0.0f;
+  int32_t h = h0;
+  for (; h + 16 <= h1; h += 16) {
+    float qv[16][VPL];
+    float gv[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int32_t e = srt[h + r];
+      gv[r] = G[(int64_t)(e >> 5) * M + j];
+      const __nv_bfloat16* qr = qlay + (int64_t)e * D + lane * VPL;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) qv[r][v] = __bfloat162float(qr[v]);
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) g[v] = fmaf(gv[r], qv[r][v], g[v]);
+  }
+  for (; h < h1; ++h) {
+    const int32_t e = srt[h];
+    const float gij = G[(int64_t)(e >> 5) * M + j];
+    const __nv_bfloat16* qr = qlay + (int64_t)e * D + lane * VPL;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) g[v] = fmaf(gij, __bfloat162float(qr[v]), g[v]);
+  }
+  norm_backward_row<VPL, Tin>(xd + row * D, g, assume_normalized != 0, out, lane);
 }
 
 }  // namespace hiper
