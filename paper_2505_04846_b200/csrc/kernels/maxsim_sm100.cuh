@@ -170,6 +170,24 @@ __device__ __forceinline__ void max64_masked(const uint32_t (&v)[64], float (&m)
     m[i & 3] = fmaxf(m[i & 3], x);
   }
 }
+// Running max and argmax (lowest column on exact ties) with one running pair per thread: the block
+// max costs 21 FMNMX3; only a block that raises the running max is scanned (downwards, == test) for
+// its lowest column attaining it.  The lowest match is always a real column: the block max is
+// attained by one, and padded columns (index >= rem) come after every real one.
+__device__ __forceinline__ void max64_arg1(const uint32_t (&v)[64], float& m, int& ix, int base,
+                                           int rem) {
+  float b[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  if (rem >= 64) max64(v, b);
+  else max64_masked(v, b, rem);
+  const float mb = fmaxf(fmaxf(b[0], b[1]), fmaxf(b[2], b[3]));
+  if (mb > m) {
+    int j = 63;
+#pragma unroll
+    for (int i = 63; i >= 0; --i) j = (__uint_as_float(v[i]) == mb) ? i : j;
+    m = mb;
+    ix = base + j;
+  }
+}
 
 template <int MODE, int KR>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           tmem_ld64_wait(taddr_base + (uint32_t)col, v);
           const int rem = ld - col;
           if constexpr (MODE == 2) {
-            max64_arg(v, m4, ix4, col, rem);
+            max64_arg1(v, m4[0], ix4[0], col, rem);  // chains 1..3 stay at -inf
           } else {
             if (rem >= 64) max64(v, m4);
             else max64_masked(v, m4, rem);
