@@ -1300,6 +1300,7 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
     a.partial = partial;
     a.progress = (kp.pair && getenv("HIPER_NO_LOCKSTEP") == nullptr) ? progress : nullptr;
     a.window = kLockstepWindow;
+    if (const char* e = getenv("HIPER_LOCKSTEP_WINDOW")) a.window = std::max(1, atoi(e));  // ablation
     TRY(launch_maxsim(1, k, kp, tq, kp.pair ? ix->tmap_half : ix->tmap, a, stream));
   }
   // partial lists [P][kEpiGroups][n_q_pad][k]: n_lists = P * kEpiGroups, each [n_q_pad][k]
