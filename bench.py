@@ -292,6 +292,8 @@ def run_ours(a, rank, local_rank, world):
         lens = all_lens[c0:c1].copy()
     else:
         lens = np.full(n_local, a.chunk_len, np.int32)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter()
     if a.gen_packed:  # N4 at paper scale: generate into the packed layout, NORM in place
         dst, n_rows = H.hiper_pack_dst_rows(lens)
         corpus = torch.empty((max(n_rows, 1), a.dim), dtype=torch.bfloat16, device="cuda")
@@ -306,6 +308,8 @@ def run_ours(a, rank, local_rank, world):
         torch.cuda.empty_cache()
     else:
         idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_BORROW_TOKENS)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build  # a1 (hiper_index_build; + generation for config4v)
     comm = H.Comm() if world > 1 else None
     q = torch.empty((a.queries, a.query_len, a.dim), dtype=torch.bfloat16, device="cuda")
     device.queries_(q, a.qseed, corpus_seed=a.seed, n_chunks=a.chunks, L=a.chunk_len,
@@ -415,7 +419,8 @@ def run_ours(a, rank, local_rank, world):
         "clocks": clk,
         "extra": {"chunk_pairs_per_s": value * a.chunks,
                   "tflops_step": fpp * a.queries * a.chunks * a.steps / (ms / 1e3) / 1e12,
-                  "top1_is_planted_target": top1, "launches_per_step": launches_per_step},
+                  "top1_is_planted_target": top1, "launches_per_step": launches_per_step,
+                  "index_build_s_rank0": build_s},
     }
     if a.packed:
         line["extra"]["packing"] = line_pack
@@ -440,6 +445,36 @@ _RESULT_FD = None
 def emit(line: dict):
     """Print the ONE JSON result line to the real stdout (library chatter goes to stderr)."""
     os.write(_RESULT_FD if _RESULT_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
+def coltrast_oracle_sample(a, seed, qseed):
+    """The CPU oracle on a bounded sample of the ColTrast step: NORM + MaxSim of the first n_s query
+    rows against all B docs + their InfoNCE rows, extrapolated linearly to the B x B step."""
+    import numpy as np
+
+    import oracle
+    from synth import gen
+    oracle.build()
+    B, L, Lq, d = a.queries, a.chunk_len, a.query_len, a.dim
+    cores = len(os.sched_getaffinity(0))
+    docs = gen.corpus(seed, 0, B, L, d)
+    qs = gen.queries(qseed, B, Lq, d, corpus_seed=seed, n_chunks=B, L=L, diagonal=True,
+                     sigma_q=gen.SIGMA_Q_HARD)
+    n_s = 2
+    while True:
+        t0 = time.perf_counter()
+        dn, qn = oracle.norm_rows(docs), oracle.norm_rows(qs[:n_s])
+        S = oracle.maxsim_matrix(qn, np.full(n_s, Lq, np.int32), dn, np.full(B, L, np.int32),
+                                 n_threads=cores)
+        oracle.infonce(S, pos=list(range(n_s)), tau=1.0)
+        dt = time.perf_counter() - t0
+        if dt > 3.0 or n_s >= B:
+            break
+        n_s = min(B, n_s * 4)
+    step_s = dt * B / n_s
+    return {"value": 1.0 / step_s, "unit": "steps/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n_s} of {B} query rows x {B} docs ({dt:.1f} s: NORM + MaxSim + InfoNCE rows), "
+                      f"extrapolated linearly to the {B}x{B} step; float64 C oracle, OpenMP"}
 
 
 def run_coltrast(a, rank, local_rank, world):
@@ -562,6 +597,8 @@ def run_coltrast(a, rank, local_rank, world):
         "gpu_launches": launches * steps, "clocks": clk,
         "extra": {"loss": float(out[1].item()), "tflops_step": flops * world * steps / (ms / 1e3) / 1e12},
     }
+    if world == 1 and not a.no_cpu_baseline and not a.grad:
+        line["cpu_baseline"] = coltrast_oracle_sample(a, seed, qseed)
     emit(line)
     if dist is not None:
         dist.barrier()
