@@ -131,19 +131,6 @@ __device__ __forceinline__ void max64(const uint32_t (&v)[64], float (&m)[4]) {
       m[c] = fmaxf(fmaxf(m[c], __uint_as_float(v[i + 2 * c])), __uint_as_float(v[i + 2 * c + 1]));
   }
 }
-// Running max AND argmax over 64 columns (MODE 2, for the backward pass): 4 chains over columns
-// c = i mod 4, ascending, strict '>' -> each chain keeps its lowest index on exact ties.
-__device__ __forceinline__ void max64_arg(const uint32_t (&v)[64], float (&m)[4], int (&ix)[4],
-                                          int base, int rem) {
-#pragma unroll
-  for (int i = 0; i < 64; ++i) {
-    const float x = (i < rem) ? __uint_as_float(v[i]) : -INFINITY;
-    if (x > m[i & 3]) {
-      m[i & 3] = x;
-      ix[i & 3] = base + i;
-    }
-  }
-}
 // Running max over N (16 or 32) columns, all real / only the first `rem` real (reading R2).
 template <int N>
 __device__ __forceinline__ void maxN(const uint32_t (&v)[N], float (&m)[4]) {
