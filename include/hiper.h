@@ -80,11 +80,13 @@ enum {
   /* hiper_index_build only (NEXT N4, variable-length chunks from semantic chunking):
    * length-bucketed packed layout.  Chunk c occupies roundup(lens[c], 16) rows of a tile of <= 256
    * rows (hiper_pack_plan); the MaxSim kernel's MMA N is the tile's row count, so padded token
-   * columns are neither stored nor multiplied.  Results are those of the dense layout.  Not accepted
+   * columns are neither stored nor multiplied.  The rows past a chunk's length inside its 16-row slot
+   * are written as copies of its last real row, so the kernel needs no column masking (a repeated
+   * column cannot change a maximum).  Results are those of the dense layout.  Not accepted
    * by hiper_two_stage_topk.  With HIPER_BORROW_TOKENS as well, `tokens` is the caller's bf16 buffer
    * ALREADY in the packed layout ([n_rows][dim], chunk c's token j at row row0(tile) + col + j as
    * hiper_pack_plan(lens) places it; rows past a chunk's length inside its 16-row slot are ignored
-   * and zeroed), NORM'd in place: no second copy of the corpus (the paper-scale 16.4M-chunk corpus,
+   * and overwritten as above), NORM'd in place: no second copy of the corpus (the paper-scale 16.4M-chunk corpus,
    * PAPER.md:564, at 110 GB per GPU on 4 GPUs).  The buffer must hold n_rows rows and outlive the
    * index. */
   HIPER_PACKED = 16u

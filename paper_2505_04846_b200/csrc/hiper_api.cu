@@ -278,34 +278,22 @@ static hiper_status pack_plan(const int32_t* lens, int64_t n, std::vector<int4>&
 // Kernel-side tile records (not part of hiper_pack_plan's ABI): one 128-B record per tile, so the
 // kernel reads everything it needs about a tile with ONE coalesced warp load (lane i <- word i):
 //   w0 = n_rows | n_ent << 16, w1 = start mask (bit g: a chunk begins at column group g; also set
-//   for every group past n_rows, so no chunk's suffix max reaches them),
-//   w2/w3 = 4 bits per column group of 16 = real columns - 1, w4 = row0, w5 = tail mask (groups with
-//   padding columns), w16 + e = chunk of slot e.
+//   for every group past n_rows, so no chunk's suffix max reaches them), w4 = row0,
+//   w16 + e = chunk of slot e.  (No per-group valid-column counts: the padding rows of a chunk's
+//   last group repeat its last real row, pack_pad_replicate_kernel.)
 static constexpr int kTileRecWords = 32;
 static std::vector<uint32_t> tile_records(const std::vector<int4>& tiles, const std::vector<int2>& ents) {
   std::vector<uint32_t> rec(tiles.size() * kTileRecWords, 0u);
   for (size_t t = 0; t < tiles.size(); ++t) {
     uint32_t* r = rec.data() + t * kTileRecWords;
-    uint64_t vcw = 0;
-    uint32_t start = 0, tail = 0;
+    uint32_t start = 0;
     for (int32_t e = tiles[t].z; e < tiles[t].w; ++e) {
-      const int32_t col = ents[e].y >> 16, len = ents[e].y & 0xFFFF;
-      const int32_t g0 = col / 16, ng = (len + 15) / 16;
-      start |= 1u << g0;
-      for (int32_t j = 0; j < ng; ++j) {
-        const int32_t vc = (j == ng - 1) ? len - 16 * j : 16;
-        vcw |= (uint64_t)(vc - 1) << (4 * (g0 + j));
-        if (vc < 16) tail |= 1u << (g0 + j);
-      }
+      start |= 1u << ((ents[e].y >> 16) / 16);
       r[16 + (e - tiles[t].z)] = (uint32_t)ents[e].x;
     }
     r[0] = (uint32_t)tiles[t].y | ((uint32_t)(tiles[t].w - tiles[t].z) << 16);
     r[1] = start | (0xFFFFu & ~((1u << (tiles[t].y / 16)) - 1u));  // groups past n_rows: own "chunks"
-
-    r[2] = (uint32_t)vcw;
-    r[3] = (uint32_t)(vcw >> 32);
     r[4] = (uint32_t)tiles[t].x;
-    r[5] = tail;
   }
   return rec;
 }
@@ -534,6 +522,13 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     st = launch_norm(tokens, dtype, n, max_len, ix->lens, n, ld_pad, dim,
                      flags | HIPER_CHECK_FINITE, ix->tok, status, stream, dst_dev);
     if (st != HIPER_OK) break;
+    if (packed && n > 0) {  // padding rows repeat each chunk's last row (unmasked packed epilogue)
+      const int64_t threads = (int64_t)n * (dim / 8);
+      pack_pad_replicate_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
+          ix->tok, dst_dev, ix->lens, n, dim);
+      if (cudaGetLastError() != cudaSuccess) { st = fail(HIPER_ERR_CUDA, "pad replicate launch"); break; }
+      ++g_launches;
+    }
     if (cudaMemcpyAsync(&hstat, status, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
         cudaStreamSynchronize(stream) != cudaSuccess) {
       st = fail(HIPER_ERR_CUDA, "build sync: %s", cudaGetErrorString(cudaGetLastError()));

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       t += (uint32_t)(c1 - c0);
       if constexpr (PACKED) {
         // Tile columns = 16 groups of 16, each inside one chunk.  Pass 1 reads the tile with the
-        // same x64 TMEM loads as the dense kernel and keeps one masked max per group; pass 2 turns
+        // same x64 TMEM loads as the dense kernel and keeps one max per group; pass 2 turns
         // them into per-chunk maxima (suffix max inside each chunk); pass 3 finishes each chunk.
         // The tile's 128-B record is one coalesced warp load (lane i <- word i), issued two of this
         // group's tiles (four MMA periods) ahead, so its DRAM latency never reaches the drain.
@@ -287,19 +287,17 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           rec_n2 = load_rec(c + 4);
           const uint32_t w0 = __shfl_sync(0xffffffffu, rec, 0);
           const uint32_t gstart = __shfl_sync(0xffffffffu, rec, 1);
-          const uint64_t vcw = ((uint64_t)__shfl_sync(0xffffffffu, rec, 3) << 32) |
-                               __shfl_sync(0xffffffffu, rec, 2);
           const int32_t n_grp = (int32_t)(w0 & 0xFFFFu) >> 4;  // column groups in use
-          const uint32_t tailmask = __shfl_sync(0xffffffffu, rec, 5);  // groups with padding columns
           long long e0 = args.stats ? clock64() : 0;
           mbar_wait(bar_tfull(grp), mine & 1u);
           long long e1 = args.stats ? clock64() : 0;
           if (args.stats) st_ewait_g += e1 - e0;
           tc_fence_after();
           // Pass 1: one running max per column group of 16 -- 4 independent FMNMX3 chains per
-          // 64-column TMEM load, the dense kernel's instruction mix -- then the few tail groups
-          // (a chunk's last group, when its length is not a multiple of 16) are re-read with one
-          // x16 load each and reduced over their real columns only (reading R2).
+          // 64-column TMEM load, the dense kernel's instruction mix.  No column is masked: the
+          // padding rows of a chunk's last 16-row group repeat its last real row (the packed layout
+          // build, pack_pad_replicate_kernel), and a repeated column cannot change a maximum, so the
+          // group max is the max over the chunk's real columns (reading R2) with no tail re-reads.
           float m16[16];
 #pragma unroll
           for (int blk = 0; blk < 4; ++blk) {
@@ -318,17 +316,6 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
 #pragma unroll
               for (int gg = 0; gg < 4; ++gg) m16[blk * 4 + gg] = -INFINITY;
             }
-          }
-          for (uint32_t tails = tailmask; tails != 0u; tails &= tails - 1u) {
-            const int g = __ffs(tails) - 1;
-            const int vc = (int)((vcw >> (4 * g)) & 15u) + 1;
-            uint32_t v[16];
-            tmem_ld16_wait(taddr_base + (uint32_t)(g * 16), v);
-            float a0 = -INFINITY;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) a0 = fmaxf(a0, i < vc ? __uint_as_float(v[i]) : -INFINITY);
-#pragma unroll
-            for (int gg = 0; gg < 16; ++gg) m16[gg] = (gg == g) ? a0 : m16[gg];
           }
           tc_fence_before();
           __syncwarp();

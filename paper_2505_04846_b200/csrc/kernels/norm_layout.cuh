@@ -45,7 +45,8 @@ __device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, flo
 // d % 8 == 0 and 16-B aligned rows.  In-place (in == out) is allowed when Tin == bf16 and
 // in_rows == out_rows: every thread reads and writes only its own row.
 // dst_row (packed layout, N4; nullptr = dense): item i's rows go to packed rows dst_row[i] + j for
-// j < roundup(len, 16) only (the padding rows of its 16-row slot are zeroed); out_rows is then just
+// j < roundup(len, 16) only (the padding rows of its 16-row slot are zeroed here, then replaced by
+// copies of its last real row by pack_pad_replicate_kernel); out_rows is then just
 // the per-item thread range (>= roundup(max_len, 16)).
 template <typename Tin>
 __device__ __forceinline__ void norm_row(int64_t row, const Tin* in, int64_t n_src, int32_t in_rows,
@@ -222,6 +223,27 @@ __global__ void __launch_bounds__(256) norm_layout_tpr_kernel(const Tin* in, int
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   norm_row_group<Tin, TPR>(tid / TPR, (uint32_t)(tid % TPR), in, n_src, in_rows, lens, n_items, out_rows,
                            d, assume_normalized, check_finite, out, status, dst_row);
+}
+
+// Packed layout (N4): the padding rows of chunk c's last 16-row group (rows len .. roundup(len,16)-1
+// of its slot) become copies of its last real row.  The MaxSim kernel's packed epilogue then takes
+// an unmasked max over every 16-column group: a repeated column cannot change a maximum, so the
+// result is the max over the chunk's real columns exactly (reading R2), with no per-tail masking.
+// Runs after the NORM launch (stream order), so it copies the final bf16 row.  One thread per
+// (chunk, 16-byte word of a row).
+__global__ void __launch_bounds__(256) pack_pad_replicate_kernel(__nv_bfloat16* tok,
+                                                                 const int64_t* __restrict__ dst_row,
+                                                                 const int32_t* __restrict__ lens,
+                                                                 int64_t n, int32_t d) {
+  const int32_t wpr = d / 8;  // uint4 words per row
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = tid / wpr;
+  if (c >= n) return;
+  const int32_t len = lens[c], end = (len + 15) & ~15;
+  if (len == end) return;
+  uint4* base = reinterpret_cast<uint4*>(tok + dst_row[c] * (int64_t)d) + (tid - c * wpr);
+  const uint4 v = base[(int64_t)(len - 1) * wpr];
+  for (int32_t j = len; j < end; ++j) base[(int64_t)j * wpr] = v;
 }
 
 // Two layouts in one launch (the ColTrast step: queries and documents): blocks [0, blocks_a) lay out

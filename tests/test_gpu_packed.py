@@ -2,7 +2,7 @@
 
 The packed layout changes where rows live and the MMA N per tile; it must not change any result:
 * layout: every chunk's packed rows are bitwise the oracle's NORM of its raw rows, padding rows of its
-  16-row slot are zero (R1, R2);
+  16-row slot repeat its last real row (R1, R2: a repeated column cannot change the max);
 * scores / top-k: within the R8 tolerance of the float64 oracle on the same bf16 operands, on
   semantic-chunk, tiny-chunk (16 per tile), full-length and mixed corpora;
 * packed == dense index bitwise (scores and top-k): per (query, chunk) the same K order and epilogue.
@@ -58,7 +58,8 @@ def unpack(H, idx, clen, rows_out):
             r0, ln = t0 + (cl >> 16), cl & 0xFFFF
             dense[c, :ln] = lay[r0:r0 + ln]
             w = (ln + 15) // 16 * 16
-            pad_ok &= not lay[r0 + ln:r0 + w].any()
+            # padding rows of the chunk's last 16-row group repeat its last real row
+            pad_ok &= bool((lay[r0 + ln:r0 + w] == lay[r0 + ln - 1]).all())
     return dense, pad_ok
 
 
