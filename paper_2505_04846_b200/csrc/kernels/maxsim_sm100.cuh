@@ -56,9 +56,8 @@ struct MaxsimArgs {
   // packed layout (N4, PACKED kernels): slot c of the kernel is tile c of a length-bucketed packed
   // corpus, described by a 128-B record recs[c][0..32): w0 = n_rows | n_ent << 16 (n_rows a multiple
   // of 16, <= 256; n_ent <= 16 chunks), w1 = start mask (bit g: a chunk begins at column group g of
-  // 16), w2/w3 = 4 bits per column group = real columns - 1, w4 = first packed row, w5 = tail mask
-  // (groups holding padding columns), w16 + e = chunk
-  // index of slot e (slots in column order).
+  // 16), w4 = first packed row, w16 + e = chunk index of slot e (slots in column order).  The
+  // padding rows of a chunk's last 16-row group repeat its last real row (no column masking).
   const uint32_t* recs;
   unsigned long long* stats;  // HIPER_PIPE_STATS diagnostics (see pooled_sm100_pair.cuh), or nullptr
 };

@@ -24,7 +24,9 @@ namespace hiper {
 
 // DBG (ablation builds only, selected by HIPER_DEBUG_MODE): 0 = production; 1 = epilogue skips the
 // TMEM reads and reductions (measures the TMA + MMA pipeline alone); 2 = additionally no chunk TMA
-// after the first stage fill (measures MMA issue alone).  DBG != 0 results are meaningless.
+// after the first stage fill (measures MMA issue alone); 3 = no chunk TMA after the first stage fill
+// but the full epilogue (measures MMA + epilogue without the L2 feed).  DBG != 0 results are
+// meaningless.
 // warps 0-7: epilogue groups 0/1; 8: TMEM allocator; 9: spare; 10: TMA producer; 11: MMA issuer
 constexpr uint32_t kPairAllocWarp = 8, kPairProducerWarp = 10, kPairMmaWarp = 11;
 
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           // one stage = this CTA's half of one whole chunk (all dim/64 K-blocks)
           mbar_wait(bar_empty(s), ph ^ 1u);
           if constexpr (PACKED) st_shared_u32(sMeta + 4u * s, nrows);  // MMA N of this stage
-          if (DBG == 2 && (c > c0 || it > 0)) {
+          if ((DBG == 2 || DBG == 3) && (c > c0 || it > 0)) {
             if (rank == 0) mbar_arrive(bar_full(s));
           } else {
             if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         tc_fence_after();
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         int ix4[4] = {0, 0, 0, 0};
-        for (int32_t col = 0; col < (DBG ? 0 : ld); col += 64) {
+        for (int32_t col = 0; col < ((DBG == 1 || DBG == 2) ? 0 : ld); col += 64) {
           uint32_t v[64];
           tmem_ld64_wait(taddr_base + (uint32_t)col, v);
           const int rem = ld - col;
