@@ -82,8 +82,9 @@ enum {
    * rows (hiper_pack_plan); the MaxSim kernel's MMA N is the tile's row count, so padded token
    * columns are neither stored nor multiplied.  The rows past a chunk's length inside its 16-row slot
    * are written as copies of its last real row, so the kernel needs no column masking (a repeated
-   * column cannot change a maximum).  Results are those of the dense layout.  Not accepted
-   * by hiper_two_stage_topk.  With HIPER_BORROW_TOKENS as well, `tokens` is the caller's bf16 buffer
+   * column cannot change a maximum).  Results are those of the dense layout, also as the token
+   * index of hiper_two_stage_topk (which reads chunks by id through a per-chunk row table the
+   * index keeps, 8 B per chunk).  With HIPER_BORROW_TOKENS as well, `tokens` is the caller's bf16 buffer
    * ALREADY in the packed layout ([n_rows][dim], chunk c's token j at row row0(tile) + col + j as
    * hiper_pack_plan(lens) places it; rows past a chunk's length inside its 16-row slot are ignored
    * and overwritten as above), NORM'd in place: no second copy of the corpus (the paper-scale 16.4M-chunk corpus,
@@ -251,7 +252,8 @@ HIPER_API hiper_status hiper_coltrast_scores_loss_grad(
 /* ------------------------------------------------------------------ NEXT N3: two-stage retrieval
  * Stage 1: pooled-cosine top-k1 over pooled_idx (built with max_len 1: the paper's deployed
  * retrieval); stage 2: exact MaxSim re-scoring of those k1 candidates over
- * token_idx, the token rows of the SAME chunks (same n and id_base), keeping the final top-k
+ * token_idx, the token rows of the SAME chunks (same n and id_base; dense or HIPER_PACKED), keeping
+ * the final top-k
  * (ColBERTv2's retrieve-then-rerank; SPEC.md:268-276 rerank; score desc, id asc).
  *   q_pooled device [n_q][pooled dim]; q_tokens device [n_q][q_max_len][token dim]; q_lens HOST.
  *   1 <= k <= k1 <= 16.

@@ -231,6 +231,7 @@ struct hiper_index_s {
   int4* tiles = nullptr;     // device [n_tiles]: the plan's tiles (hiper_pack_plan layout)
   uint32_t* recs = nullptr;  // device [n_tiles][32]: kernel tile records (tile_records)
   int2* ents = nullptr;   // device [n]
+  int64_t* row_of = nullptr;  // device [n]: first packed row of chunk c (two-stage rerank by id)
 };
 
 // ---------------------------------------------------------------------------- N4 packing plan
@@ -471,6 +472,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     if (ix->recs) cudaFree(ix->recs);
     if (ix->ents) cudaFree(ix->ents);
     if (dst_dev) cudaFree(dst_dev);
+    ix->row_of = nullptr;
     delete ix;
     return s;
   };
@@ -548,10 +550,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   } while (0);
   cudaFree(status);
   if (st != HIPER_OK) return cleanup(st);
-  if (dst_dev) {
-    cudaFree(dst_dev);  // the stream was synchronised above
-    dst_dev = nullptr;
-  }
+  ix->row_of = dst_dev;  // kept: stage 2 of hiper_two_stage_topk reads packed chunks by id
   *out = ix;
   return HIPER_OK;
 }
@@ -563,6 +562,7 @@ extern "C" hiper_status hiper_index_destroy(hiper_index* ix) {
   if (ix->tiles) cudaFree(ix->tiles);
   if (ix->recs) cudaFree(ix->recs);
   if (ix->ents) cudaFree(ix->ents);
+  if (ix->row_of) cudaFree(ix->row_of);
   delete ix;
   return HIPER_OK;
 }
@@ -826,6 +826,11 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
     unsigned long long* st = nullptr;
     MaxsimArgs b = a;
+    // wait policy: the MMA thread busy-waits (its barrier wake-up latency is on the tensor pipe's
+    // critical path; measured -7% MMA-thread cycles), every other role suspends in try_wait so it
+    // does not take issue slots from the epilogue.  HIPER_SPIN overrides (ablation).
+    static const uint32_t spin = getenv("HIPER_SPIN") ? (uint32_t)atoi(getenv("HIPER_SPIN")) : 1u;
+    b.spin = spin;
     if (stats_on) {
       CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
       CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
@@ -1098,6 +1103,8 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
   unsigned long long* st = nullptr;
   PooledArgs b = a;
+  static const uint32_t spin = getenv("HIPER_SPIN") ? (uint32_t)atoi(getenv("HIPER_SPIN")) : 1u;
+  b.spin = spin;  // the MaxSim kernel's wait policy (MMA thread busy-waits)
   if (stats_on) {
     CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
@@ -1888,8 +1895,7 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   if (!pix || !tix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
   if (pix->ld_pad != 1) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (max_len 1)");
   if (tix->ld_pad == 1) return fail(HIPER_ERR_INVALID_ARG, "stage-2 index must hold token rows");
-  if (tix->packed || pix->packed)
-    return fail(HIPER_ERR_UNSUPPORTED, "two-stage retrieval reads chunks by id: build the indexes without HIPER_PACKED");
+  if (pix->packed) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (not HIPER_PACKED)");
   if (pix->n != tix->n || pix->id_base != tix->id_base)
     return fail(HIPER_ERR_INVALID_ARG, "the two indexes must cover the same chunks (n, id_base)");
   if (k1 < 1 || k < 1 || k > k1) return fail(HIPER_ERR_INVALID_ARG, "need 1 <= k <= k1");
@@ -1933,7 +1939,11 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
   KernelPlan kp;
   const int32_t n_slots = 8 * k1;
-  TRY(plan_kernel(di, n_q, n_slots, tix->ld_pad, tix->dim, kp));
+  // a packed token index (N4) is read chunk by chunk through its row table: the kernel loads a
+  // 256-row window from the chunk's first packed row and the epilogue reads only its len real
+  // columns (the rows after them belong to other chunks and are never part of a max)
+  const int32_t ldp = tix->packed ? kTileRows : tix->ld_pad;
+  TRY(plan_kernel(di, n_q, n_slots, ldp, tix->dim, kp));
   if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "rerank needs the CTA-pair kernel");
   kp.n_parts = 1;  // a unit = one row group and its own candidate list
   kp.grid = (int)std::min<int64_t>(kp.n_groups, di.num_sms / 2) * 2;
@@ -1943,7 +1953,8 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   a.n_q = n_q;
   a.n_groups = kp.n_groups;
   a.n_parts = 1;
-  a.ld_pad = tix->ld_pad;
+  a.ld_pad = ldp;
+  a.row_of = tix->packed ? tix->row_of : nullptr;
   a.num_kb = tix->dim / 64;
   a.k = 1;
   a.n_stages = kp.n_stages;

@@ -53,6 +53,8 @@ struct MaxsimArgs {
   const int32_t* cand;    // rerank (N3): [G][n_chunks] chunk index per slot of each row group
                           // (-1 = empty slot), or nullptr = the corpus itself
   int32_t window;         // chunks a pair may run ahead of the slowest pair (lockstep window)
+  const int64_t* row_of;  // rerank over a packed index: first packed row of each chunk (its rows are
+                          // row_of[c] + j); nullptr = dense layout, chunk c at row c * ld_pad
   // packed layout (N4, PACKED kernels): slot c of the kernel is tile c of a length-bucketed packed
   // corpus, described by a 128-B record recs[c][0..32): w0 = n_rows | n_ent << 16 (n_rows a multiple
   // of 16, <= 256; n_ent <= 16 chunks), w1 = start mask (bit g: a chunk begins at column group g of
@@ -60,6 +62,8 @@ struct MaxsimArgs {
   // padding rows of a chunk's last 16-row group repeat its last real row (no column masking).
   const uint32_t* recs;
   unsigned long long* stats;  // HIPER_PIPE_STATS diagnostics (see pooled_sm100_pair.cuh), or nullptr
+  uint32_t spin;              // pair kernel wait policy: bit 0 = the MMA thread busy-waits (test_wait)
+                              // instead of suspending (default); bit 1 = the epilogue; bit 2 = producer
 };
 
 // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare; warps 4-7 = epilogue warpgroup 0 (accumulator 0, even

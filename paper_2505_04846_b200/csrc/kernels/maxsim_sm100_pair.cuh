@@ -176,7 +176,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           nrows = ld_shared_u32(e) & 0xFFFFu;
           brow = (int32_t)ld_shared_u32(e + 4u) + (int32_t)rank * (int32_t)(nrows >> 1);
         } else {
-          brow = (int32_t)(slot_chunk(args, g, c) * args.ld_pad + (int64_t)rank * half_rows);
+          const int64_t ch = slot_chunk(args, g, c);
+          const int64_t r0 = args.row_of != nullptr ? __ldg(args.row_of + ch) : ch * args.ld_pad;
+          brow = (int32_t)(r0 + (int64_t)rank * half_rows);
         }
         if (lane == 0) {
           if (args.progress != nullptr && rank == 0 && ((c - c0) & 15) == 0) {
@@ -185,7 +187,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
           }
           // one stage = this CTA's half of one whole chunk (all dim/64 K-blocks)
-          mbar_wait(bar_empty(s), ph ^ 1u);
+          if (args.spin & 4u) mbar_wait_spin(bar_empty(s), ph ^ 1u);
+          else mbar_wait(bar_empty(s), ph ^ 1u);
           if constexpr (PACKED) st_shared_u32(sMeta + 4u * s, nrows);  // MMA N of this stage
           if ((DBG == 2 || DBG == 3) && (c > c0 || it > 0)) {
             if (rank == 0) mbar_arrive(bar_full(s));
@@ -223,14 +226,16 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         for (int64_t c = c0; c < c1; ++c, ++t) {
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
           long long w0 = args.stats ? clock64() : 0;
-          mbar_wait(bar_tempty(acc), tph ^ 1u);
+          if (args.spin & 1u) mbar_wait_spin(bar_tempty(acc), tph ^ 1u);
+          else mbar_wait(bar_tempty(acc), tph ^ 1u);
           if (args.stats) {
             st_acc += clock64() - w0;
             w0 = clock64();
           }
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
-          mbar_wait(bar_full(s), ph);
+          if (args.spin & 1u) mbar_wait_spin(bar_full(s), ph);
+          else mbar_wait(bar_full(s), ph);
           if (args.stats) st_full += clock64() - w0;
           tc_fence_after();
           uint32_t idesc_c = idesc;
@@ -291,7 +296,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           const uint32_t gstart = __shfl_sync(0xffffffffu, rec, 1);
           const int32_t n_grp = (int32_t)(w0 & 0xFFFFu) >> 4;  // column groups in use
           long long e0 = args.stats ? clock64() : 0;
-          mbar_wait(bar_tfull(grp), mine & 1u);
+          if (args.spin & 2u) mbar_wait_spin(bar_tfull(grp), mine & 1u);
+        else mbar_wait(bar_tfull(grp), mine & 1u);
           long long e1 = args.stats ? clock64() : 0;
           if (args.stats) st_ewait_g += e1 - e0;
           tc_fence_after();
@@ -376,7 +382,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         const int32_t ld = ld_next;
         if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk(args, g, c + 2));
         long long e0 = args.stats ? clock64() : 0;
-        mbar_wait(bar_tfull(grp), mine & 1u);
+        if (args.spin & 2u) mbar_wait_spin(bar_tfull(grp), mine & 1u);
+        else mbar_wait(bar_tfull(grp), mine & 1u);
         long long e1 = args.stats ? clock64() : 0;
         if (args.stats) st_ewait_g += e1 - e0;
         tc_fence_after();

@@ -62,3 +62,24 @@ def test_two_stage_matches_oracle(H, C, n_q, k1, k):
         assert (i[r, m:] == -1).all()
         checked += 1
     assert checked >= max(1, int(0.8 * n_q))
+
+
+def test_two_stage_packed_token_index_bitwise(H):
+    """Stage 2 over a HIPER_PACKED token index (chunks read by id through the index's row table)
+    gives bitwise the result over the dense token index, on semantic-chunking lengths."""
+    C, n_q, k1, k, L, Lq, d, dp = 1200, 21, 16, 10, 256, 32, 128, 768
+    tok = gen.corpus(91, 0, C, L, d)
+    tl = gen.lengths(91, C, L, True)   # variable lengths 1..L
+    pooled = gen.corpus(92, 0, C, 1, dp)
+    qt = gen.queries(93, n_q, Lq, d, corpus_seed=91, n_chunks=C, L=L, chunk_lens_fn=lambda c: tl[c])
+    ql = gen.lengths(93, n_q, Lq, True, stream=gen.QLEN)
+    qp = gen.queries(93, n_q, 1, dp, corpus_seed=92, n_chunks=C, L=1, sigma_q=np.float32(8.0))
+    pidx = H.hiper_index_build(to_dev(pooled), np.ones(C, np.int32), id_base=7)
+    dense = H.hiper_index_build(to_dev(tok), tl, id_base=7)
+    packed = H.hiper_index_build(to_dev(tok), tl, id_base=7, flags=H.HIPER_PACKED)
+    assert packed.packed
+    s0, i0 = [t.cpu().numpy() for t in H.hiper_two_stage_topk(pidx, dense, to_dev(qp), to_dev(qt), ql, k1, k)]
+    s1, i1 = [t.cpu().numpy() for t in H.hiper_two_stage_topk(pidx, packed, to_dev(qp), to_dev(qt), ql, k1, k)]
+    assert np.array_equal(i1, i0)
+    assert np.array_equal(s1.view(np.uint32), s0.view(np.uint32))
+    assert (i0[:, 0] >= 7).all()
