@@ -806,6 +806,7 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1>;
     if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2>;
     if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 3) kern = maxsim_sm100_pair_kernel<MODE, KR, 3>;
+    if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 4) kern = maxsim_sm100_pair_kernel<MODE, KR, 4>;
     CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)kp.grid);

@@ -25,8 +25,9 @@ namespace hiper {
 // DBG (ablation builds only, selected by HIPER_DEBUG_MODE): 0 = production; 1 = epilogue skips the
 // TMEM reads and reductions (measures the TMA + MMA pipeline alone); 2 = additionally no chunk TMA
 // after the first stage fill (measures MMA issue alone); 3 = no chunk TMA after the first stage fill
-// but the full epilogue (measures MMA + epilogue without the L2 feed).  DBG != 0 results are
-// meaningless.
+// but the full epilogue (measures MMA + epilogue without the L2 feed); 4 = mode 2 with every
+// chunk's K loop issued twice into its accumulator (per-chunk fixed costs vs MMA time).  DBG != 0
+// results are meaningless.
 // warps 0-7: epilogue groups 0/1; 8: TMEM allocator; 9: spare; 10: TMA producer; 11: MMA issuer
 constexpr uint32_t kPairAllocWarp = 8, kPairProducerWarp = 10, kPairMmaWarp = 11;
 
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           if (args.spin & 4u) mbar_wait_spin(bar_empty(s), ph ^ 1u);
           else mbar_wait(bar_empty(s), ph ^ 1u);
           if constexpr (PACKED) st_shared_u32(sMeta + 4u * s, nrows);  // MMA N of this stage
-          if ((DBG == 2 || DBG == 3) && (c > c0 || it > 0)) {
+          if ((DBG == 2 || DBG == 3 || DBG == 4) && (c > c0 || it > 0)) {
             if (rank == 0) mbar_arrive(bar_full(s));
           } else {
             if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
@@ -242,13 +243,14 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           if constexpr (PACKED)  // MMA N = this tile's packed rows (written by the producer)
             idesc_c = idesc_bf16_f32(256, ld_shared_u32(sMeta + 4u * s));
           const uint32_t b_st = sB + s * args.stage_bytes;
+          for (int rep = 0; rep < (DBG == 4 ? 2 : 1); ++rep)  // DBG 4: each chunk's K loop twice
           for (int kb = 0; kb < args.num_kb; ++kb) {
             const uint32_t a_kb = a_tile + kb * 16384u;
             const uint32_t b_kb = b_st + kb * half_tile;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               mma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_kb + kk * 32),
-                               umma_desc_sw128(b_kb + kk * 32), idesc_c, (kb | kk) != 0 ? 1u : 0u);
+                               umma_desc_sw128(b_kb + kk * 32), idesc_c, (rep | kb | kk) != 0 ? 1u : 0u);
           }
           mma_commit_pair_mc(bar_empty(s), 0x3);  // both CTAs' stage s free again
           if (++s == S) { s = 0; ph ^= 1u; }
@@ -389,7 +391,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         tc_fence_after();
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         int ix4[4] = {0, 0, 0, 0};
-        for (int32_t col = 0; col < ((DBG == 1 || DBG == 2) ? 0 : ld); col += 64) {
+        for (int32_t col = 0; col < ((DBG == 1 || DBG == 2 || DBG == 4) ? 0 : ld); col += 64) {
           uint32_t v[64];
           tmem_ld64_wait(taddr_base + (uint32_t)col, v);
           const int rem = ld - col;
