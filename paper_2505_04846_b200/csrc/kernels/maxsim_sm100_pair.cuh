@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
           long long w0 = args.stats ? clock64() : 0;
           if (args.spin & 1u) mbar_wait_spin(bar_tempty(acc), tph ^ 1u);
+          else if (args.spin & 32u) mbar_wait_nohint(bar_tempty(acc), tph ^ 1u);
           else mbar_wait(bar_tempty(acc), tph ^ 1u);
           if (args.stats) {
             st_acc += clock64() - w0;
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
           if (args.spin & 1u) mbar_wait_spin(bar_full(s), ph);
+          else if (args.spin & 32u) mbar_wait_nohint(bar_full(s), ph);
           else mbar_wait(bar_full(s), ph);
           if (args.stats) st_full += clock64() - w0;
           tc_fence_after();
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           const int32_t n_grp = (int32_t)(w0 & 0xFFFFu) >> 4;  // column groups in use
           long long e0 = args.stats ? clock64() : 0;
           if (args.spin & 2u) mbar_wait_spin(bar_tfull(grp), mine & 1u);
+        else if (args.spin & 16u) mbar_wait_nohint(bar_tfull(grp), mine & 1u);
         else mbar_wait(bar_tfull(grp), mine & 1u);
           long long e1 = args.stats ? clock64() : 0;
           if (args.stats) st_ewait_g += e1 - e0;
@@ -385,6 +388,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk(args, g, c + 2));
         long long e0 = args.stats ? clock64() : 0;
         if (args.spin & 2u) mbar_wait_spin(bar_tfull(grp), mine & 1u);
+        else if (args.spin & 16u) mbar_wait_nohint(bar_tfull(grp), mine & 1u);
         else mbar_wait(bar_tfull(grp), mine & 1u);
         long long e1 = args.stats ? clock64() : 0;
         if (args.stats) st_ewait_g += e1 - e0;

@@ -103,6 +103,30 @@ __device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
   }
 }
 
+// try_wait without a suspend-time hint: the hardware's own (short) default wait window.
+__device__ __forceinline__ bool mbar_try_wait_nohint(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_nohint(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait_nohint(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_nohint(bar, parity)) {
+    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) {
+      printf("hiper: mbarrier watchdog (nohint) block %d thread %d bar 0x%x parity %u\n", blockIdx.x,
+             threadIdx.x, bar, parity);
+      __trap();
+    }
+  }
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
