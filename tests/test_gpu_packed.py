@@ -193,3 +193,35 @@ def test_packed_borrow_in_place(H):
     s1, i1 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(idx, to_dev(q), qlen, 10)]
     s0, i0 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(ref, to_dev(q), qlen, 10)]
     assert np.array_equal(i1, i0) and np.array_equal(s1.view(np.uint32), s0.view(np.uint32))
+
+
+def test_packed_masking_adversary(H):
+    """P10 on the packed layout: every real doc token has a negative dot with the query token, and no
+    length is a multiple of 16, so a zero padding row would win the max.  The padding rows repeat
+    each chunk's last real row, so the packed scores equal the oracle's (negative) masked scores and
+    the dense index's bitwise, through both the dense-score and the top-k epilogues."""
+    d = 128
+    qv = np.zeros((4, 32, d), np.float32)
+    qv[:, 0, 0] = 1.0
+    qlen = np.ones(4, np.int32)
+    rng = np.random.default_rng(5)
+    C, L = 40, 64
+    docs = np.zeros((C, L, d), np.float32)
+    docs[:, :, 0] = -np.abs(rng.standard_normal((C, L))) - 0.1
+    docs[:, :, 1:] = rng.standard_normal((C, L, d - 1)) * 0.1
+    clen = np.array([(1 + 3 * c) % 63 + 1 for c in range(C)], np.int32)
+    clen[clen % 16 == 0] += 1
+    idx = packed_index(H, docs, clen)
+    S = H.hiper_maxsim_scores(idx, to_dev(qv), qlen).cpu().numpy()
+    ql = query_layout(H, qv, qlen)
+    lay = expected_layout(docs, clen, L)
+    S_o = oracle.maxsim_matrix(ql[:len(qlen)], qlen, lay, clen)
+    assert (S_o < 0).all() and (S < 0).all()
+    assert_scores_close(S, S_o, qlen, d, "packed masking")
+    dense = H.hiper_index_build(to_dev(docs), clen)
+    S_d = H.hiper_maxsim_scores(dense, to_dev(qv), qlen).cpu().numpy()
+    assert np.array_equal(S.view(np.uint32), S_d.view(np.uint32))
+    s, i = [t.cpu().numpy() for t in H.hiper_maxsim_topk(idx, to_dev(qv), qlen, 5)]
+    s_d, i_d = [t.cpu().numpy() for t in H.hiper_maxsim_topk(dense, to_dev(qv), qlen, 5)]
+    assert np.array_equal(i, i_d) and np.array_equal(s.view(np.uint32), s_d.view(np.uint32))
+    assert (s < 0).all()
