@@ -827,11 +827,6 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
     unsigned long long* st = nullptr;
     MaxsimArgs b = a;
-    // wait policy: the MMA thread busy-waits (its barrier wake-up latency is on the tensor pipe's
-    // critical path; measured -7% MMA-thread cycles), every other role suspends in try_wait so it
-    // does not take issue slots from the epilogue.  HIPER_SPIN overrides (ablation).
-    static const uint32_t spin = getenv("HIPER_SPIN") ? (uint32_t)atoi(getenv("HIPER_SPIN")) : 1u;
-    b.spin = spin;
     if (stats_on) {
       CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
       CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
@@ -1104,8 +1099,6 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
   unsigned long long* st = nullptr;
   PooledArgs b = a;
-  static const uint32_t spin = getenv("HIPER_SPIN") ? (uint32_t)atoi(getenv("HIPER_SPIN")) : 1u;
-  b.spin = spin;  // the MaxSim kernel's wait policy (MMA thread busy-waits)
   if (stats_on) {
     CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));

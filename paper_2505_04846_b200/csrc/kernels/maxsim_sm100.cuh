@@ -62,9 +62,6 @@ struct MaxsimArgs {
   // padding rows of a chunk's last 16-row group repeat its last real row (no column masking).
   const uint32_t* recs;
   unsigned long long* stats;  // HIPER_PIPE_STATS diagnostics (see pooled_sm100_pair.cuh), or nullptr
-  uint32_t spin;              // pair kernel wait policy: bit 0 = the MMA thread busy-waits (test_wait)
-                              // instead of suspending (default); bit 1 = the epilogue; bit 2 = producer;
-                              // bits 4 / 5: epilogue / MMA thread use try_wait without a suspend hint
 };
 
 // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare; warps 4-7 = epilogue warpgroup 0 (accumulator 0, even

@@ -50,10 +50,7 @@ __device__ __forceinline__ void lockstep_wait(const uint32_t* progress, uint32_t
       mn = min(mn, *reinterpret_cast<const volatile uint32_t*>(progress + j));
     if ((uint64_t)pos <= (uint64_t)mn + window) return;
     __nanosleep(200);
-    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) {
-      printf("hiper: lockstep watchdog pair %u pos 0x%x min 0x%x\n", 0u, pos, mn);
-      __trap();
-    }
+    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) ptx::hiper_watchdog_fail("lockstep", pos, mn);
   }
 }
 
@@ -188,8 +185,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
           }
           // one stage = this CTA's half of one whole chunk (all dim/64 K-blocks)
-          if (args.spin & 4u) mbar_wait_spin(bar_empty(s), ph ^ 1u);
-          else mbar_wait(bar_empty(s), ph ^ 1u);
+          mbar_wait(bar_empty(s), ph ^ 1u);
           if constexpr (PACKED) st_shared_u32(sMeta + 4u * s, nrows);  // MMA N of this stage
           if ((DBG == 2 || DBG == 3 || DBG == 4) && (c > c0 || it > 0)) {
             if (rank == 0) mbar_arrive(bar_full(s));
@@ -227,18 +223,14 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         for (int64_t c = c0; c < c1; ++c, ++t) {
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
           long long w0 = args.stats ? clock64() : 0;
-          if (args.spin & 1u) mbar_wait_spin(bar_tempty(acc), tph ^ 1u);
-          else if (args.spin & 32u) mbar_wait_nohint(bar_tempty(acc), tph ^ 1u);
-          else mbar_wait(bar_tempty(acc), tph ^ 1u);
+          mbar_wait(bar_tempty(acc), tph ^ 1u);
           if (args.stats) {
             st_acc += clock64() - w0;
             w0 = clock64();
           }
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
-          if (args.spin & 1u) mbar_wait_spin(bar_full(s), ph);
-          else if (args.spin & 32u) mbar_wait_nohint(bar_full(s), ph);
-          else mbar_wait(bar_full(s), ph);
+          mbar_wait(bar_full(s), ph);
           if (args.stats) st_full += clock64() - w0;
           tc_fence_after();
           uint32_t idesc_c = idesc;
@@ -300,9 +292,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           const uint32_t gstart = __shfl_sync(0xffffffffu, rec, 1);
           const int32_t n_grp = (int32_t)(w0 & 0xFFFFu) >> 4;  // column groups in use
           long long e0 = args.stats ? clock64() : 0;
-          if (args.spin & 2u) mbar_wait_spin(bar_tfull(grp), mine & 1u);
-        else if (args.spin & 16u) mbar_wait_nohint(bar_tfull(grp), mine & 1u);
-        else mbar_wait(bar_tfull(grp), mine & 1u);
+          mbar_wait(bar_tfull(grp), mine & 1u);
           long long e1 = args.stats ? clock64() : 0;
           if (args.stats) st_ewait_g += e1 - e0;
           tc_fence_after();
@@ -387,9 +377,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         const int32_t ld = ld_next;
         if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk(args, g, c + 2));
         long long e0 = args.stats ? clock64() : 0;
-        if (args.spin & 2u) mbar_wait_spin(bar_tfull(grp), mine & 1u);
-        else if (args.spin & 16u) mbar_wait_nohint(bar_tfull(grp), mine & 1u);
-        else mbar_wait(bar_tfull(grp), mine & 1u);
+        mbar_wait(bar_tfull(grp), mine & 1u);
         long long e1 = args.stats ? clock64() : 0;
         if (args.stats) st_ewait_g += e1 - e0;
         tc_fence_after();

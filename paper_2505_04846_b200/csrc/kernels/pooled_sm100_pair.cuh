@@ -42,7 +42,6 @@ struct PooledArgs {
   unsigned long long* stats;  // pipeline statistics (HIPER_PIPE_STATS), or nullptr: [0] MMA cycles
                               // waiting for a free accumulator, [1] for a full stage, [2] MMA
                               // thread total, [3] epilogue drain cycles, [4] epilogue wait, [5] tiles
-  uint32_t spin;              // bit 0: the MMA thread busy-waits (as in the MaxSim pair kernel)
 };
 
 // Per-thread register top-k: the epilogue thread of query q keeps KP sortable keys in registers.
@@ -177,15 +176,13 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         for (int32_t ct = t0; ct < t1; ++ct, ++t) {
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
           long long w0 = args.stats ? clock64() : 0;
-          if (args.spin & 1u) mbar_wait_spin(bar_tempty(acc), tph ^ 1u);
-          else mbar_wait(bar_tempty(acc), tph ^ 1u);
+          mbar_wait(bar_tempty(acc), tph ^ 1u);
           if (args.stats) st_acc += clock64() - w0;
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
           for (int kb = 0; kb < args.num_kb; ++kb) {
             if (args.stats) w0 = clock64();
-            if (args.spin & 1u) mbar_wait_spin(bar_full(s), ph);
-            else mbar_wait(bar_full(s), ph);
+            mbar_wait(bar_full(s), ph);
             if (args.stats) st_full += clock64() - w0;
             tc_fence_after();
             const uint32_t st = sStage + s * args.stage_bytes;

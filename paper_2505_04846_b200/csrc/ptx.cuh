@@ -64,6 +64,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Watchdog report, out of line: every inlined wait site carries only a call, not the printf argument
+// set-up (the fused kernels' hot loops share the instruction cache; code size is measurable there).
+__device__ __noinline__ void hiper_watchdog_fail(const char* what, uint32_t a, uint32_t b) {
+  printf("hiper: %s watchdog block %d thread %d 0x%x 0x%x\n", what, blockIdx.x, threadIdx.x, a, b);
+  __trap();
+}
 // Wait until the phase with the given parity has completed.  try_wait suspends the thread in hardware
 // until the phase completes or the (10 ms) time hint expires, so waiting warps do not spin on issue
 // slots shared with the epilogue's arithmetic.
@@ -71,59 +77,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) {
-      printf("hiper: mbarrier watchdog block %d thread %d bar 0x%x parity %u\n", blockIdx.x,
-             threadIdx.x, bar, parity);
-      __trap();
-    }
-  }
-}
-
-// Busy-wait variant (no suspend): mbarrier.test_wait polls the phase without parking the thread.
-__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
-  if (mbar_test_wait(bar, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_test_wait(bar, parity)) {
-    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) {
-      printf("hiper: mbarrier watchdog (spin) block %d thread %d bar 0x%x parity %u\n", blockIdx.x,
-             threadIdx.x, bar, parity);
-      __trap();
-    }
-  }
-}
-
-// try_wait without a suspend-time hint: the hardware's own (short) default wait window.
-__device__ __forceinline__ bool mbar_try_wait_nohint(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_nohint(uint32_t bar, uint32_t parity) {
-  if (mbar_try_wait_nohint(bar, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_try_wait_nohint(bar, parity)) {
-    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) {
-      printf("hiper: mbarrier watchdog (nohint) block %d thread %d bar 0x%x parity %u\n", blockIdx.x,
-             threadIdx.x, bar, parity);
-      __trap();
-    }
+    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) hiper_watchdog_fail("mbarrier", bar, parity);
   }
 }
 
