@@ -802,11 +802,17 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   bool rec = false;
   if (kp.pair) {
-    auto kern = maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED>;
-    if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1>;
-    if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2>;
-    if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 3) kern = maxsim_sm100_pair_kernel<MODE, KR, 3>;
-    if (!PACKED && MODE == 1 && KR == 1 && debug_mode() == 4) kern = maxsim_sm100_pair_kernel<MODE, KR, 4>;
+    static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
+    // production: no instrumentation compiled in; HIPER_PIPE_STATS / HIPER_DEBUG_MODE select the
+    // instrumented (STATS) instantiations
+    auto kern = stats_on ? maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED, true>
+                         : maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED, false>;
+    if constexpr (!PACKED && MODE == 1 && KR == 1) {
+      if (debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1, false, true>;
+      if (debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2, false, true>;
+      if (debug_mode() == 3) kern = maxsim_sm100_pair_kernel<MODE, KR, 3, false, true>;
+      if (debug_mode() == 4) kern = maxsim_sm100_pair_kernel<MODE, KR, 4, false, true>;
+    }
     CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)kp.grid);
@@ -824,7 +830,6 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
     unsigned long long* st = nullptr;
     MaxsimArgs b = a;
     if (stats_on) {

@@ -66,7 +66,9 @@ __device__ __forceinline__ bool slot_valid(const MaxsimArgs& a, int32_t g, int64
 
 // PACKED (N4): the slots are the tiles of a length-bucketed packed corpus (MaxsimArgs::tiles/ents):
 // the MMA N is the tile's n_rows, and the epilogue reduces each chunk over its own column segment.
-template <int MODE, int KR, int DBG = 0, bool PACKED = false>
+// STATS: HIPER_PIPE_STATS instrumentation compiled in (diagnostics builds only; the production
+// instantiation carries none of it -- the kernel's hot loops are instruction-cache sensitive).
+template <int MODE, int KR, int DBG = 0, bool PACKED = false, bool STATS = false>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_d, const MaxsimArgs args) {
@@ -222,16 +224,16 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         const uint32_t a_tile = sA + ab * args.a_bytes;
         for (int64_t c = c0; c < c1; ++c, ++t) {
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
-          long long w0 = args.stats ? clock64() : 0;
+          long long w0 = (STATS && args.stats) ? clock64() : 0;
           mbar_wait(bar_tempty(acc), tph ^ 1u);
-          if (args.stats) {
+          if (STATS && args.stats) {
             st_acc += clock64() - w0;
             w0 = clock64();
           }
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
           mbar_wait(bar_full(s), ph);
-          if (args.stats) st_full += clock64() - w0;
+          if (STATS && args.stats) st_full += clock64() - w0;
           tc_fence_after();
           uint32_t idesc_c = idesc;
           if constexpr (PACKED)  // MMA N = this tile's packed rows (written by the producer)
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         }
         mma_commit_pair_mc(bar_aempty(ab), 0x3);
       }
-      if (args.stats) {
+      if (STATS && args.stats) {
         atomicAdd(args.stats + 0, (unsigned long long)st_acc);
         atomicAdd(args.stats + 1, (unsigned long long)st_full);
         atomicAdd(args.stats + 2, (unsigned long long)(clock64() - st_t0));
@@ -291,10 +293,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           const uint32_t w0 = __shfl_sync(0xffffffffu, rec, 0);
           const uint32_t gstart = __shfl_sync(0xffffffffu, rec, 1);
           const int32_t n_grp = (int32_t)(w0 & 0xFFFFu) >> 4;  // column groups in use
-          long long e0 = args.stats ? clock64() : 0;
+          long long e0 = (STATS && args.stats) ? clock64() : 0;
           mbar_wait(bar_tfull(grp), mine & 1u);
-          long long e1 = args.stats ? clock64() : 0;
-          if (args.stats) st_ewait_g += e1 - e0;
+          long long e1 = (STATS && args.stats) ? clock64() : 0;
+          if (STATS && args.stats) st_ewait_g += e1 - e0;
           tc_fence_after();
           // Pass 1: one running max per column group of 16 -- 4 independent FMNMX3 chains per
           // 64-column TMEM load, the dense kernel's instruction mix.  No column is masked: the
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty_leader);  // TMEM drained: release the accumulator
-          if (args.stats) {
+          if (STATS && args.stats) {
             st_drain_g += clock64() - e1;
             ++st_tiles_g;
           }
@@ -376,10 +378,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       for (int64_t c = first; c < c1; c += 2, ++mine) {
         const int32_t ld = ld_next;
         if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk(args, g, c + 2));
-        long long e0 = args.stats ? clock64() : 0;
+        long long e0 = (STATS && args.stats) ? clock64() : 0;
         mbar_wait(bar_tfull(grp), mine & 1u);
-        long long e1 = args.stats ? clock64() : 0;
-        if (args.stats) st_ewait_g += e1 - e0;
+        long long e1 = (STATS && args.stats) ? clock64() : 0;
+        if (STATS && args.stats) st_ewait_g += e1 - e0;
         tc_fence_after();
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         int ix4[4] = {0, 0, 0, 0};
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader);
-        if (args.stats) {
+        if (STATS && args.stats) {
           st_drain_g += clock64() - e1;
           ++st_tiles_g;
         }
@@ -437,7 +439,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     }
   }
 
-  if (warp < 8 && args.stats && lane == 0) {
+  if (STATS && warp < 8 && args.stats && lane == 0) {
     atomicAdd(args.stats + 3, (unsigned long long)st_drain_g);
     atomicAdd(args.stats + 4, (unsigned long long)st_ewait_g);
     atomicAdd(args.stats + 5, (unsigned long long)st_tiles_g);
