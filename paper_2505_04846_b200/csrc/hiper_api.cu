@@ -1079,12 +1079,14 @@ template <int MODE>
 static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, const CUtensorMap& tc,
                                   const PooledArgs& a, cudaStream_t stream) {
   if (pp.grid == 0 || pp.n_parts == 0) return HIPER_OK;
+  static const bool pstats_on = getenv("HIPER_PIPE_STATS") != nullptr;
   auto kern = pp.cl == 4 ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 4>
-                         : pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
-  if (MODE == 1 && debug_mode() == 1) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 1>;
-  if (MODE == 1 && debug_mode() == 2) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 2>;
-  if (MODE == 1 && debug_mode() == 3) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 3>;
-  if (MODE == 1 && debug_mode() == 4) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 4>;
+              : pstats_on ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 2, true>
+                          : pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
+  if (MODE == 1 && debug_mode() == 1) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 1, 2, true>;
+  if (MODE == 1 && debug_mode() == 2) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 2, 2, true>;
+  if (MODE == 1 && debug_mode() == 3) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 3, 2, true>;
+  if (MODE == 1 && debug_mode() == 4) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 4, 2, true>;
   CUDA_TRY(set_max_smem((const void*)kern, (int)pp.smem_bytes));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)pp.grid);

@@ -55,13 +55,17 @@ __device__ __forceinline__ void lockstep_wait(const uint32_t* progress, uint32_t
 }
 
 // Chunk scored in slot c of row group g: the corpus itself, or (rerank, N3) a per-group candidate list.
+// BY_ID: the instantiation can see a candidate table / row table (MODE 0 only: the rerank of N3);
+// the top-k and argmax instantiations compile these look-ups out.
+template <bool BY_ID>
 __device__ __forceinline__ int64_t slot_chunk(const MaxsimArgs& a, int32_t g, int64_t c) {
-  if (a.cand == nullptr) return c;
+  if (!BY_ID || a.cand == nullptr) return c;
   const int32_t id = __ldg(a.cand + (int64_t)g * a.n_chunks + c);
   return id < 0 ? 0 : id;
 }
+template <bool BY_ID>
 __device__ __forceinline__ bool slot_valid(const MaxsimArgs& a, int32_t g, int64_t c) {
-  return a.cand == nullptr || __ldg(a.cand + (int64_t)g * a.n_chunks + c) >= 0;
+  return !BY_ID || a.cand == nullptr || __ldg(a.cand + (int64_t)g * a.n_chunks + c) >= 0;
 }
 
 // PACKED (N4): the slots are the tiles of a length-bucketed packed corpus (MaxsimArgs::tiles/ents):
@@ -176,8 +180,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           nrows = ld_shared_u32(e) & 0xFFFFu;
           brow = (int32_t)ld_shared_u32(e + 4u) + (int32_t)rank * (int32_t)(nrows >> 1);
         } else {
-          const int64_t ch = slot_chunk(args, g, c);
-          const int64_t r0 = args.row_of != nullptr ? __ldg(args.row_of + ch) : ch * args.ld_pad;
+          const int64_t ch = slot_chunk<MODE == 0>(args, g, c);
+          const int64_t r0 = (MODE == 0 && args.row_of != nullptr) ? __ldg(args.row_of + ch) : ch * args.ld_pad;
           brow = (int32_t)(r0 + (int64_t)rank * half_rows);
         }
         if (lane == 0) {
@@ -374,10 +378,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           }
         }
       } else {
-      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + slot_chunk(args, g, first)) : 0;
+      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + slot_chunk<MODE == 0>(args, g, first)) : 0;
       for (int64_t c = first; c < c1; c += 2, ++mine) {
         const int32_t ld = ld_next;
-        if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk(args, g, c + 2));
+        if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk<MODE == 0>(args, g, c + 2));
         long long e0 = (STATS && args.stats) ? clock64() : 0;
         mbar_wait(bar_tfull(grp), mine & 1u);
         long long e1 = (STATS && args.stats) ? clock64() : 0;
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         sv += 0.0f;  // canonical +0
         if constexpr (MODE == 0 || MODE == 2) {
           if (lane == 0 && q < args.n_q)
-            args.scores[(int64_t)q * args.score_ld + c] = slot_valid(args, g, c) ? sv : -INFINITY;
+            args.scores[(int64_t)q * args.score_ld + c] = slot_valid<MODE == 0>(args, g, c) ? sv : -INFINITY;
         } else {
           const uint64_t key = make_key(sv, args.id_base + c);
           if (key > topk.thresh) topk.insert(key, args.k, lane);

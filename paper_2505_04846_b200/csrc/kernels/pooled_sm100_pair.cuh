@@ -61,7 +61,8 @@ __device__ __forceinline__ float pooled_thr_score(uint64_t thr) {
 // query tiles (2qq, 2qq + 1) against the same chunk tiles; each chunk-tile K-block half (128 rows)
 // needed by CTA r of both pairs is loaded once, half by each of them, and TMA-multicast to both, so
 // the chunk operand costs half the L2 reads.  tmap_c then has a 64-row box.
-template <int MODE, int KP, int DBG = 0, int CL = 2>
+// STATS: HIPER_PIPE_STATS instrumentation compiled in (diagnostics only; see the MaxSim pair kernel).
+template <int MODE, int KP, int DBG = 0, int CL = 2, bool STATS = false>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     pooled_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_c, const PooledArgs args) {
@@ -175,15 +176,15 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         decode(u, qt, p, t0, t1);
         for (int32_t ct = t0; ct < t1; ++ct, ++t) {
           const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
-          long long w0 = args.stats ? clock64() : 0;
+          long long w0 = (STATS && args.stats) ? clock64() : 0;
           mbar_wait(bar_tempty(acc), tph ^ 1u);
-          if (args.stats) st_acc += clock64() - w0;
+          if (STATS && args.stats) st_acc += clock64() - w0;
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccStride;
           for (int kb = 0; kb < args.num_kb; ++kb) {
-            if (args.stats) w0 = clock64();
+            if (STATS && args.stats) w0 = clock64();
             mbar_wait(bar_full(s), ph);
-            if (args.stats) st_full += clock64() - w0;
+            if (STATS && args.stats) st_full += clock64() - w0;
             tc_fence_after();
             const uint32_t st = sStage + s * args.stage_bytes;
 #pragma unroll
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           mma_commit_pair_mc(bar_tfull(acc), pair_mask);
         }
       }
-      if (args.stats) {
+      if (STATS && args.stats) {
         atomicAdd(args.stats + 0, (unsigned long long)st_acc);
         atomicAdd(args.stats + 1, (unsigned long long)st_full);
         atomicAdd(args.stats + 2, (unsigned long long)(clock64() - st_t0));
@@ -227,10 +228,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       const int32_t first = t0 + (int32_t)((grp - (t & 1u)) & 1u);
       t += (uint32_t)(t1 - t0);
       for (int32_t ct = first; ct < t1; ct += 2, ++mine) {
-        long long e0 = args.stats ? clock64() : 0;
+        long long e0 = (STATS && args.stats) ? clock64() : 0;
         mbar_wait(bar_tfull(grp), mine & 1u);
-        long long e1 = args.stats ? clock64() : 0;
-        if (args.stats) st_ewait += e1 - e0;
+        long long e1 = (STATS && args.stats) ? clock64() : 0;
+        if (STATS && args.stats) st_ewait += e1 - e0;
         tc_fence_after();
         const int64_t cbase = (int64_t)ct * 256;
         const int64_t left = args.n_chunks - cbase;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             }
             uint64_t hits = 0ull;
             if (any) {
-              if (args.stats) ++st_any;
+              if (STATS && args.stats) ++st_any;
 #pragma unroll
               for (int j = 0; j < 64; ++j)
                 hits |= (uint64_t)(__uint_as_float(r[j]) >= thr_f && j < nj) << j;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                 hits &= hits - 1;
                 uint64_t key = make_key(xs[j], args.id_base + cbase + col + j);
                 if (key > lim) {
-                  if (args.stats) ++st_ins;
+                  if (STATS && args.stats) ++st_ins;
 #pragma unroll
                   for (int m = 0; m < KP; ++m) {
                     const uint64_t hi = v[m] > key ? v[m] : key;
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader);
-        if (args.stats) {
+        if (STATS && args.stats) {
           st_drain += clock64() - e1;
           ++st_tiles;
         }
@@ -332,12 +333,12 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         }
       }
     }
-    if (args.stats && lane == 0) {
+    if (STATS && args.stats && lane == 0) {
       atomicAdd(args.stats + 3, (unsigned long long)st_drain);
       atomicAdd(args.stats + 4, (unsigned long long)st_ewait);
       atomicAdd(args.stats + 5, (unsigned long long)st_tiles);
     }
-    if (args.stats) {
+    if (STATS && args.stats) {
       atomicAdd(args.stats + 6, (unsigned long long)st_any);
       atomicAdd(args.stats + 7, (unsigned long long)st_ins);
     }
