@@ -338,41 +338,46 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
 #pragma unroll
           for (int g = 14; g >= 0; --g)
             m16[g] = ((gstart >> (g + 1)) & 1u) ? m16[g] : fmaxf(m16[g], m16[g + 1]);
-          // Pass 3: the masked sum over query tokens of each chunk (a butterfly in the dense kernel's
-          // fixed order, only for chunk-start groups: warp-uniform branches).  Top-k: a score
-          // pre-filter against the list threshold, exact key test and insert for the rare rest.
-          const uint32_t starts = gstart & (n_grp >= 16 ? 0xFFFFu : ((1u << n_grp) - 1u));
-          const uint32_t thr_hi = (uint32_t)(topk.thresh >> 32);
-          float sums[16];
-          uint32_t cand = 0u;
+          // Pass 3: the masked sum over query tokens of all 16 groups at once, by a transposed
+          // butterfly (a reduce-scatter by shuffles): each round halves the groups a lane carries, and
+          // lane l ends with the sum of group l >> 1.  Every group's sum is built from exactly the
+          // dense kernel's butterfly pairings (xor 16, 8, 4, 2, 1; fp add is commutative), so the
+          // scores are bitwise those of the dense layout -- in straight-line code instead of 16
+          // branch-guarded butterflies (the kernel's hot loops are instruction-cache sensitive).
+          float x[16];
 #pragma unroll
-          for (int g = 0; g < 16; ++g) {
-            sums[g] = 0.0f;
-            if ((starts >> g) & 1u) {
-              float sv = ((int32_t)lane < lq) ? m16[g] : 0.0f;
+          for (int g = 0; g < 16; ++g) x[g] = ((int32_t)lane < lq) ? m16[g] : 0.0f;
 #pragma unroll
-              for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-              sv += 0.0f;  // canonical +0
-              sums[g] = sv;
-              if constexpr (MODE == 0) {
-                const int e = __popc(gstart & ((1u << g) - 1u));
-                const int32_t chunk = (int32_t)__shfl_sync(0xffffffffu, rec, 16 + e);
-                if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk] = sv;
-              } else {
-                cand |= (uint32_t)(float_orderable(sv) >= thr_hi) << g;
-              }
+          for (int w = 8; w >= 1; w >>= 1) {  // keep w groups; partner = lane ^ 2w
+            const bool hi = (lane & (2u * (uint32_t)w)) != 0u;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+              const float keep = hi ? x[i + w] : x[i];
+              const float send = hi ? x[i] : x[i + w];
+              x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * w);
             }
           }
-          if constexpr (MODE == 1) {
+          float sv = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
+          sv += 0.0f;  // canonical +0
+          // lane pair (2g, 2g + 1) holds group g; its even lane speaks for it when a chunk starts there
+          // (start bits are also set past n_rows, so mask them to the groups in use)
+          const uint32_t starts = gstart & (n_grp >= 16 ? 0xFFFFu : ((1u << n_grp) - 1u));
+          const uint32_t gl = (lane >> 1) & 15u;
+          const bool speaker = ((starts >> gl) & 1u) != 0u && (lane & 1u) == 0u;
+          const int32_t chunk_l = (int32_t)__shfl_sync(0xffffffffu, rec, 16 + __popc(gstart & ((1u << gl) - 1u)));
+          if constexpr (MODE == 0) {
+            if (speaker && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk_l] = sv;
+          } else {
+            // top-k: a score pre-filter against the list threshold, exact key test and insert for
+            // the rare rest (ascending group order)
+            const uint32_t thr_hi = (uint32_t)(topk.thresh >> 32);
+            uint32_t cand = __ballot_sync(0xffffffffu, speaker && float_orderable(sv) >= thr_hi);
             while (cand != 0u) {
-              const int g = __ffs(cand) - 1;
+              const int src = __ffs(cand) - 1;
               cand &= cand - 1u;
-              const int e = __popc(gstart & ((1u << g) - 1u));
-              const int32_t chunk = (int32_t)__shfl_sync(0xffffffffu, rec, 16 + e);
-              float sv = sums[0];
-#pragma unroll
-              for (int gg = 1; gg < 16; ++gg) sv = (gg == g) ? sums[gg] : sv;
-              const uint64_t key = make_key(sv, args.id_base + chunk);
+              const float s_src = __shfl_sync(0xffffffffu, sv, src);
+              const int32_t c_src = __shfl_sync(0xffffffffu, chunk_l, src);
+              const uint64_t key = make_key(s_src, args.id_base + c_src);
               if (key > topk.thresh) topk.insert(key, args.k, lane);
             }
           }
