@@ -175,6 +175,31 @@ HIPER_API hiper_status hiper_maxsim_topk(const hiper_index* idx, const void* q_t
                                size_t workspace_bytes, float* out_scores, int64_t* out_ids,
                                hiper_stream_t stream);
 
+/* ------------------------------------------------------------------ step a8, in two halves
+ * The cross-GPU merge of hiper_maxsim_topk(comm != NULL) is: every rank's local top-k as sortable
+ * 64-bit keys -> one ncclAllGather into [world][n_q][k] -> the same merge + decode on every rank.  The
+ * two halves are exported so the merge can be driven (and tested against the oracle) without NCCL:
+ * nearest neighbours over the whole store (§2.3) from per-shard lists (north star:
+ * "merged with one NCCL all-gather").
+ * Key format: (orderable(score) << 32) | (~(uint32)global_id), orderable(f) = bits(f) ^ (f < 0 ?
+ * 0xFFFFFFFF : 0x80000000); a larger key = a higher score, then a lower id (R6); key 0 = empty slot.
+ *
+ * hiper_maxsim_topk_keys: as hiper_maxsim_topk with comm == NULL, but writes this shard's top-k as keys,
+ *   out_keys device uint64 [n_q][k] (descending; 0-padded when k > n).  Workspace: as
+ *   hiper_maxsim_topk_workspace_size(idx, n_q, k, NULL).
+ * hiper_topk_merge_keys: lists device uint64 [n_lists][n_q][k] (each [n_q][k] block sorted descending,
+ *   as written by hiper_maxsim_topk_keys or gathered by ncclAllGather) -> the top-k of their union,
+ *   decoded: out_scores device float [n_q][k], out_ids device int64 [n_q][k] (padding -inf / -1).
+ *   1 <= k <= 128; n_lists >= 0 (0 gives all padding).  Bitwise independent of the list order. */
+HIPER_API hiper_status hiper_maxsim_topk_keys(const hiper_index* idx, const void* q_tokens,
+                                    hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
+                                    int32_t q_max_len, int32_t dim, int32_t k, uint32_t flags,
+                                    void* workspace, size_t workspace_bytes, uint64_t* out_keys,
+                                    hiper_stream_t stream);
+HIPER_API hiper_status hiper_topk_merge_keys(const uint64_t* lists, int32_t n_lists, int32_t n_q,
+                                   int32_t k, float* out_scores, int64_t* out_ids,
+                                   hiper_stream_t stream);
+
 /* ------------------------------------------------------------------ dense scores (test support + a10)
  * out_scores device float [n_q][n] = S(q, c) for every query and every chunk of the index. */
 HIPER_API size_t hiper_maxsim_scores_workspace_size(const hiper_index* idx, int32_t n_q);

@@ -49,7 +49,7 @@ EXPORTS = [
     "hiper_profile_enable", "hiper_profile_read", "hiper_coltrast_loss_workspace_size",
     "hiper_coltrast_loss", "hiper_coltrast_grad_workspace_size", "hiper_coltrast_scores_loss_grad",
     "hiper_two_stage_workspace_size", "hiper_two_stage_topk", "hiper_pack_plan",
-    "hiper_index_pack_info",
+    "hiper_index_pack_info", "hiper_maxsim_topk_keys", "hiper_topk_merge_keys",
 ]
 
 
@@ -107,6 +107,8 @@ def lib():
         "hiper_profile_read": ([P, P], i32),
         "hiper_pack_plan": ([P, i64, P, P, P, P], i32),
         "hiper_index_pack_info": ([P, P, P, P, P, P], i32),
+        "hiper_maxsim_topk_keys": ([P, P, i32, P, i32, i32, i32, i32, u32, P, sz, P, P], i32),
+        "hiper_topk_merge_keys": ([P, i32, i32, i32, P, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -151,6 +153,13 @@ def _stream_ptr(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _keep(buf, stream):
+    """The library enqueues on `stream`; a temporary torch allocation (workspace, contiguous copy)
+    used by that work must not be recycled by the caching allocator before `stream` reaches it."""
+    if buf is not None:
+        buf.record_stream(stream if stream is not None else _torch().cuda.current_stream())
 
 
 def _workspace(nbytes: int, device):
@@ -283,6 +292,14 @@ def hiper_index_build(tokens, lens, *, id_base: int = 0, flags: int = 0, max_len
             raise HiperError(1, "a 2-D token buffer needs HIPER_PACKED | HIPER_BORROW_TOKENS")
         n, dim = ln.shape[0], tokens.shape[1]
         max_len = max_len or 256
+        torch = _torch()
+        if tokens.dtype != torch.bfloat16:
+            raise HiperError(1, "a borrowed packed buffer must be bfloat16")
+        # the library NORMs the buffer in place and writes padding rows up to the plan's n_rows:
+        # it cannot see the buffer's size, so check it here
+        _, n_rows = hiper_pack_dst_rows(ln) if n else (None, 0)
+        if tokens.shape[0] < n_rows:
+            raise HiperError(1, f"packed buffer has {tokens.shape[0]} rows < the plan's {n_rows}")
     else:
         n, max_len, dim = tokens.shape
     if ln.shape != (n,):
@@ -353,6 +370,7 @@ def hiper_maxsim_topk(index: Index, q_tokens, q_lens, k: int, *, flags: int = 0,
     ql = _host_i32(q_lens)
     if workspace is None:
         workspace = TopkWorkspace(index, n_q, k, comm, q_tokens.device)
+        _keep(workspace.buf, stream)
     if out is None:
         out = (torch.empty((n_q, k), dtype=torch.float32, device=q_tokens.device),
                torch.empty((n_q, k), dtype=torch.int64, device=q_tokens.device))
@@ -364,6 +382,40 @@ def hiper_maxsim_topk(index: Index, q_tokens, q_lens, k: int, *, flags: int = 0,
     return out
 
 
+def hiper_maxsim_topk_keys(index: Index, q_tokens, q_lens, k: int, *, flags: int = 0,
+                           workspace: TopkWorkspace | None = None, out=None, stream=None):
+    """a8, first half: this shard's top-k as sortable keys (the all-gather payload), returned as a
+    torch int64 tensor [n_q][k] holding the uint64 key bits (include/hiper.h key format)."""
+    torch = _torch()
+    n_q, q_max_len, dim = q_tokens.shape
+    ql = _host_i32(q_lens)
+    if workspace is None:
+        workspace = TopkWorkspace(index, n_q, k, None, q_tokens.device)
+        _keep(workspace.buf, stream)
+    if out is None:
+        out = torch.empty((n_q, k), dtype=torch.int64, device=q_tokens.device)
+    _check(lib().hiper_maxsim_topk_keys(index.handle, _dev_ptr(q_tokens), _dtype_code(q_tokens),
+                                        _ptr(ql), n_q, q_max_len, dim, k, flags,
+                                        ctypes.c_void_p(workspace.ptr), workspace.nbytes,
+                                        _dev_ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def hiper_topk_merge_keys(lists, k: int, *, out=None, stream=None):
+    """a8, second half: lists = int64 tensor [n_lists][n_q][k] of uint64 key bits (e.g. the
+    all-gathered per-shard keys) -> (scores float32 [n_q][k], ids int64 [n_q][k])."""
+    torch = _torch()
+    n_lists, n_q, kk = lists.shape
+    if kk != k:
+        raise HiperError(1, f"lists last dim {kk} != k {k}")
+    if out is None:
+        out = (torch.empty((n_q, k), dtype=torch.float32, device=lists.device),
+               torch.empty((n_q, k), dtype=torch.int64, device=lists.device))
+    _check(lib().hiper_topk_merge_keys(_dev_ptr(lists) if lists.numel() else None, n_lists, n_q, k,
+                                       _dev_ptr(out[0]), _dev_ptr(out[1]), _stream_ptr(stream)))
+    return out
+
+
 def hiper_maxsim_scores(index: Index, q_tokens, q_lens, *, flags: int = 0, out=None, stream=None):
     """Dense S [n_q][n] (test support; same kernel mainloop as the top-k path)."""
     torch = _torch()
@@ -371,6 +423,7 @@ def hiper_maxsim_scores(index: Index, q_tokens, q_lens, *, flags: int = 0, out=N
     ql = _host_i32(q_lens)
     nb = lib().hiper_maxsim_scores_workspace_size(index.handle, n_q)
     ws, wp, wn = _workspace(nb, q_tokens.device)
+    _keep(ws, stream)
     if out is None:
         out = torch.empty((n_q, index.n), dtype=torch.float32, device=q_tokens.device)
     _check(lib().hiper_maxsim_scores(index.handle, _dev_ptr(q_tokens), _dtype_code(q_tokens),
@@ -401,6 +454,7 @@ def hiper_coltrast_scores_loss(q_tokens, q_lens, d_tokens, d_lens, *, pos_idx=No
     pos = None if pos_idx is None else _host_i32(pos_idx)
     if workspace is None:
         workspace = ColtrastWorkspace(n_q, n_d, d_max_len, dim, q_tokens.device)
+        _keep(workspace.buf, stream)
     if out is None:
         S = (torch.empty((n_q, n_d), dtype=torch.float32, device=q_tokens.device)
              if want_scores else None)
@@ -421,6 +475,7 @@ def hiper_infonce_loss(scores, *, pos_idx=None, temperature: float = 1.0, stream
     n_q, n_d = scores.shape
     pos = None if pos_idx is None else _host_i32(pos_idx)
     ws, wp, wn = _workspace(max(1024, (n_q * 4 + 1023) // 1024 * 1024), scores.device)
+    _keep(ws, stream)
     loss = torch.empty(1, dtype=torch.float32, device=scores.device)
     _check(lib().hiper_infonce_loss(_dev_ptr(scores), n_q, n_d,
                                     _ptr(pos) if pos is not None else None, float(temperature),
@@ -465,6 +520,7 @@ def hiper_coltrast_loss(q_tokens, q_lens, d_tokens, d_lens, q_pooled, d_pooled, 
     nb = lib().hiper_coltrast_loss_workspace_size(b, d_max_len, dim, dp, n_max,
                                                   comm.handle if comm else None)
     ws, wp, wn = _workspace(nb, q_tokens.device)
+    _keep(ws, stream)
     losses = torch.empty(3, dtype=torch.float32, device=q_tokens.device)
     S = torch.empty((b, m), dtype=torch.float32, device=q_tokens.device) if want_scores else None
     mo = ctypes.c_int32()
@@ -487,6 +543,7 @@ def hiper_coltrast_scores_loss_grad(q_tokens, q_lens, d_tokens, d_lens, *, pos_i
     pos = None if pos_idx is None else _host_i32(pos_idx)
     nb = lib().hiper_coltrast_grad_workspace_size(n_q, n_d, d_max_len, dim)
     ws, wp, wn = _workspace(nb, q_tokens.device)
+    _keep(ws, stream)
     dev = q_tokens.device
     S = torch.empty((n_q, n_d), dtype=torch.float32, device=dev)
     loss = torch.empty(1, dtype=torch.float32, device=dev)
@@ -514,9 +571,12 @@ def hiper_two_stage_topk(pooled_index: Index, token_index: Index, q_pooled, q_to
     ch = comm.handle if comm else None
     nb = lib().hiper_two_stage_workspace_size(pooled_index.handle, token_index.handle, n_q, k1, ch)
     ws, wp, wn = _workspace(nb, q_tokens.device)
+    _keep(ws, stream)
+    qp = qp.contiguous()
+    _keep(qp, stream)
     s = torch.empty((n_q, k), dtype=torch.float32, device=q_tokens.device)
     i = torch.empty((n_q, k), dtype=torch.int64, device=q_tokens.device)
-    _check(lib().hiper_two_stage_topk(pooled_index.handle, token_index.handle, _dev_ptr(qp.contiguous()),
+    _check(lib().hiper_two_stage_topk(pooled_index.handle, token_index.handle, _dev_ptr(qp),
                                       _dev_ptr(q_tokens), _dtype_code(q_tokens), _ptr(ql), n_q,
                                       q_max_len, k1, k, flags, ch, ctypes.c_void_p(wp), wn,
                                       _dev_ptr(s), _dev_ptr(i), _stream_ptr(stream)))

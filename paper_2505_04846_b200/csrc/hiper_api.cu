@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -78,6 +79,17 @@ extern "C" const char* hiper_status_string(hiper_status s) {
   }
   return "HIPER_ERR_UNKNOWN";
 }
+// NVTX range around every ABI entry point (header-only NVTX3: a no-op unless a profiler such as
+// nsys / ncu --nvtx is attached), so a timeline shows which library call each kernel belongs to.
+struct HiperRange {
+  explicit HiperRange(const char* name) { nvtxRangePushA(name); }
+  ~HiperRange() { nvtxRangePop(); }
+  HiperRange(const HiperRange&) = delete;
+  HiperRange& operator=(const HiperRange&) = delete;
+};
+
+static constexpr int32_t kMaxK = 128;  // top-k capacity of every list (register / warp lists)
+
 extern "C" const char* hiper_last_error(void) { return g_last_error.c_str(); }
 extern "C" int32_t hiper_version(void) { return 100; }
 extern "C" int32_t hiper_last_launch_count(void) { return g_launches; }
@@ -419,6 +431,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
                                           int64_t n, int32_t max_len, int32_t dim, int64_t id_base,
                                           uint32_t flags, hiper_stream_t stream_, hiper_index** out) {
   g_launches = 0;
+  HiperRange nv("hiper_index_build");
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!out) return fail(HIPER_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
@@ -644,6 +657,7 @@ extern "C" hiper_status hiper_prepare_queries(const void* q_tokens, hiper_dtype 
                                               int32_t dim, uint32_t flags, void* out_layout,
                                               uint32_t* status, hiper_stream_t stream_) {
   g_launches = 0;
+  HiperRange nv("hiper_prepare_queries");
   cudaStream_t stream = (cudaStream_t)stream_;
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
   if (!out_layout || !is_device_ptr(out_layout)) return fail(HIPER_ERR_INVALID_ARG, "out_layout must be device memory");
@@ -913,6 +927,22 @@ struct hiper_comm_s {
       return fail(HIPER_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(_r), __FILE__, __LINE__); \
   } while (0)
 
+// A collective's enqueue can succeed while the communicator has already failed asynchronously (a
+// peer died, a network error): ncclCommGetAsyncError is non-blocking and reports it.
+static hiper_status nccl_async_check(const hiper_comm_s* c, const char* what) {
+  ncclResult_t ar = ncclSuccess;
+  NCCL_TRY(ncclCommGetAsyncError(c->comm, &ar));
+  if (ar != ncclSuccess && ar != ncclInProgress)
+    return fail(HIPER_ERR_NCCL, "%s: communicator async error: %s", what, ncclGetErrorString(ar));
+  return HIPER_OK;
+}
+
+// a8: every rank's local [n_q][k] key list -> [world][n_q][k] on every rank (one ncclAllGather on
+// `stream`, no host round trip), then the same deterministic merge + decode (a7/a9 kernel).
+static hiper_status gather_merge(const hiper_comm_s* c, const uint64_t* local, uint64_t* gathered,
+                                 int32_t n_q, int32_t k, float* out_scores, int64_t* out_ids,
+                                 cudaStream_t stream);
+
 extern "C" hiper_status hiper_comm_unique_id(uint8_t id[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   if (!id) return fail(HIPER_ERR_INVALID_ARG, "id is NULL");
@@ -956,6 +986,32 @@ extern "C" hiper_status hiper_comm_info(const hiper_comm* c, int32_t* world, int
   if (world) *world = c->world;
   if (rank) *rank = c->rank;
   return HIPER_OK;
+}
+
+static hiper_status gather_merge(const hiper_comm_s* c, const uint64_t* local, uint64_t* gathered,
+                                 int32_t n_q, int32_t k, float* out_scores, int64_t* out_ids,
+                                 cudaStream_t stream) {
+  NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, c->comm, stream));
+  TRY(nccl_async_check(c, "ncclAllGather of top-k keys"));
+  return launch_merge(gathered, c->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids,
+                      stream);
+}
+
+extern "C" hiper_status hiper_topk_merge_keys(const uint64_t* lists, int32_t n_lists, int32_t n_q,
+                                              int32_t k, float* out_scores, int64_t* out_ids,
+                                              hiper_stream_t stream_) {
+  g_launches = 0;
+  HiperRange nv("hiper_topk_merge_keys");
+  if (n_lists < 0 || n_q < 0) return fail(HIPER_ERR_INVALID_ARG, "n_lists / n_q < 0");
+  if (k < 1) return fail(HIPER_ERR_INVALID_ARG, "k must be >= 1");
+  if (k > kMaxK) return fail(HIPER_ERR_UNSUPPORTED, "k %d > %d", k, kMaxK);
+  if (n_q == 0) return HIPER_OK;
+  if (!out_scores || !out_ids || !is_device_ptr(out_scores) || !is_device_ptr(out_ids))
+    return fail(HIPER_ERR_INVALID_ARG, "outputs must be device memory");
+  if (n_lists > 0 && (!lists || !is_device_ptr(lists)))
+    return fail(HIPER_ERR_INVALID_ARG, "lists must be device memory");
+  return launch_merge(lists, n_lists, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids,
+                      (cudaStream_t)stream_);
 }
 
 // ============================================================================ workspace layouts
@@ -1160,7 +1216,8 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
                                   const int32_t* q_lens, int32_t n_q, int32_t dim, int32_t k,
                                   uint32_t flags, const hiper_comm* comm, void* workspace,
                                   size_t workspace_bytes, float* out_scores, int64_t* out_ids,
-                                  float* dense_scores, cudaStream_t stream) {
+                                  float* dense_scores, cudaStream_t stream,
+                                  uint64_t* out_keys = nullptr) {
   if (!dense_scores && k > kPooledKP)
     return fail(HIPER_ERR_UNSUPPORTED, "pooled top-k supports k <= %d (got %d)", kPooledKP, k);
   DevInfo di;
@@ -1216,13 +1273,14 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   }
   const int32_t n_lists = ix->n > 0 ? pp.n_parts * kEpiGroups : 0;
   const int64_t list_stride = (int64_t)pp.q_pad * k;
+  if (out_keys)  // this shard's top-k keys (a8's all-gather payload)
+    return launch_merge(partial, n_lists, list_stride, n_q, k, k, out_keys, nullptr, nullptr, stream);
   if (!comm || comm->world == 1)
     return launch_merge(partial, n_lists, list_stride, n_q, k, k, nullptr, out_scores, out_ids, stream);
   uint64_t* local = (uint64_t*)(ws + w.local);
   uint64_t* gathered = (uint64_t*)(ws + w.gathered);
   TRY(launch_merge(partial, n_lists, list_stride, n_q, k, k, local, nullptr, nullptr, stream));
-  NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, comm->comm, stream));
-  return launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream);
+  return gather_merge(comm, local, gathered, n_q, k, out_scores, out_ids, stream);
 }
 
 static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, const hiper_comm* comm,
@@ -1241,25 +1299,25 @@ static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, cons
   return w.total;
 }
 
-extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_tokens,
-                                          hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
-                                          int32_t q_max_len, int32_t dim, int32_t k, uint32_t flags,
-                                          const hiper_comm* comm, void* workspace,
-                                          size_t workspace_bytes, float* out_scores,
-                                          int64_t* out_ids, hiper_stream_t stream_) {
-  g_launches = 0;
-  cudaStream_t stream = (cudaStream_t)stream_;
+// Steps a2-a9.  out_keys != NULL (comm == NULL): stop after the intra-GPU merge and write this shard's
+// top-k as sortable keys (a8's all-gather payload, hiper_maxsim_topk_keys) instead of decoding.
+static hiper_status topk_search(const hiper_index* ix, const void* q_tokens, hiper_dtype dtype,
+                                const int32_t* q_lens, int32_t n_q, int32_t q_max_len, int32_t dim,
+                                int32_t k, uint32_t flags, const hiper_comm* comm, void* workspace,
+                                size_t workspace_bytes, float* out_scores, int64_t* out_ids,
+                                uint64_t* out_keys, cudaStream_t stream) {
   if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
   if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
   if (k < 1) return fail(HIPER_ERR_INVALID_ARG, "k must be >= 1");
-  if (k > 128) return fail(HIPER_ERR_UNSUPPORTED, "k %d > 128", k);
+  if (k > kMaxK) return fail(HIPER_ERR_UNSUPPORTED, "k %d > %d", k, kMaxK);
   const bool pooled = ix->ld_pad == 1;
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, pooled));
   if (n_q == 0) return HIPER_OK;
-  if (!out_scores || !out_ids) return fail(HIPER_ERR_INVALID_ARG, "outputs are NULL");
+  if (out_keys ? !is_device_ptr(out_keys) : (!out_scores || !out_ids))
+    return fail(HIPER_ERR_INVALID_ARG, "outputs are NULL");
   if (pooled)
     return pooled_search(ix, q_tokens, dtype, q_lens, n_q, dim, k, flags, comm, workspace,
-                         workspace_bytes, out_scores, out_ids, nullptr, stream);
+                         workspace_bytes, out_scores, out_ids, nullptr, stream, out_keys);
   DevInfo di;
   TRY(device_info(di));
   if (di.device != ix->device) return fail(HIPER_ERR_INVALID_ARG, "index lives on device %d, current is %d", ix->device, di.device);
@@ -1318,17 +1376,40 @@ extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_t
   }
   // partial lists [P][kEpiGroups][n_q_pad][k]: n_lists = P * kEpiGroups, each [n_q_pad][k]
   const int64_t q_stride = k, list_stride = (int64_t)n_q_pad_of(n_q) * k;
-  const int32_t n_lists = kp.n_parts * kEpiGroups;
-  if (!comm || comm->world == 1) {
-    TRY(launch_merge(partial, n_lists, list_stride, n_q, q_stride, k, nullptr, out_scores, out_ids, stream));
-    return HIPER_OK;
-  }
+  const int32_t n_lists = kp.grid > 0 ? kp.n_parts * kEpiGroups : 0;
+  if (out_keys)
+    return launch_merge(partial, n_lists, list_stride, n_q, q_stride, k, out_keys, nullptr, nullptr, stream);
+  if (!comm || comm->world == 1)
+    return launch_merge(partial, n_lists, list_stride, n_q, q_stride, k, nullptr, out_scores, out_ids, stream);
   uint64_t* local = (uint64_t*)(ws + w.local);
   uint64_t* gathered = (uint64_t*)(ws + w.gathered);
   TRY(launch_merge(partial, n_lists, list_stride, n_q, q_stride, k, local, nullptr, nullptr, stream));
-  NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, comm->comm, stream));
-  TRY(launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream));
-  return HIPER_OK;
+  return gather_merge(comm, local, gathered, n_q, k, out_scores, out_ids, stream);
+}
+
+extern "C" hiper_status hiper_maxsim_topk(const hiper_index* ix, const void* q_tokens,
+                                          hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
+                                          int32_t q_max_len, int32_t dim, int32_t k, uint32_t flags,
+                                          const hiper_comm* comm, void* workspace,
+                                          size_t workspace_bytes, float* out_scores,
+                                          int64_t* out_ids, hiper_stream_t stream_) {
+  g_launches = 0;
+  HiperRange nv("hiper_maxsim_topk");
+  return topk_search(ix, q_tokens, dtype, q_lens, n_q, q_max_len, dim, k, flags, comm, workspace,
+                     workspace_bytes, out_scores, out_ids, nullptr, (cudaStream_t)stream_);
+}
+
+extern "C" hiper_status hiper_maxsim_topk_keys(const hiper_index* ix, const void* q_tokens,
+                                               hiper_dtype dtype, const int32_t* q_lens, int32_t n_q,
+                                               int32_t q_max_len, int32_t dim, int32_t k,
+                                               uint32_t flags, void* workspace,
+                                               size_t workspace_bytes, uint64_t* out_keys,
+                                               hiper_stream_t stream_) {
+  g_launches = 0;
+  HiperRange nv("hiper_maxsim_topk_keys");
+  if (!out_keys && n_q > 0) return fail(HIPER_ERR_INVALID_ARG, "out_keys is NULL");
+  return topk_search(ix, q_tokens, dtype, q_lens, n_q, q_max_len, dim, k, flags, nullptr, workspace,
+                     workspace_bytes, nullptr, nullptr, out_keys, (cudaStream_t)stream_);
 }
 
 // ============================================================================ dense scores
@@ -1360,6 +1441,7 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
                                             void* workspace, size_t workspace_bytes,
                                             float* out_scores, hiper_stream_t stream_) {
   g_launches = 0;
+  HiperRange nv("hiper_maxsim_scores");
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
   if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
@@ -1505,6 +1587,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
                                                    void* workspace, size_t workspace_bytes,
                                                    float* out_scores, float* out_loss, hiper_stream_t stream_) {
   g_launches = 0;
+  HiperRange nv("hiper_coltrast_scores_loss");
   cudaStream_t stream = (cudaStream_t)stream_;
   TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
@@ -1638,6 +1721,7 @@ extern "C" hiper_status hiper_coltrast_loss(
     float tau_li, float tau_c, const hiper_comm* comm, void* workspace, size_t workspace_bytes,
     float* out_losses, float* out_scores_c, int32_t* out_m, hiper_stream_t stream_) {
   g_launches = 0;
+  HiperRange nv("hiper_coltrast_loss");
   cudaStream_t stream = (cudaStream_t)stream_;
   if (b == 0) return fail(HIPER_ERR_EMPTY_BATCH, "empty batch");
   if (b < 0) return fail(HIPER_ERR_INVALID_ARG, "b < 0");
@@ -1681,6 +1765,7 @@ extern "C" hiper_status hiper_coltrast_loss(
   const size_t row_bytes = (size_t)dp * 2;
   if (world > 1) {
     NCCL_TRY(ncclAllGather(dpp, gathered, (size_t)b * dp, ncclBfloat16, comm->comm, stream));
+    TRY(nccl_async_check(comm, "ncclAllGather of pooled passages"));
     CUDA_TRY(cudaMemcpyAsync(cand, gathered + (size_t)rank * b * dp, (size_t)b * row_bytes,
                              cudaMemcpyDeviceToDevice, stream));
     int64_t filled = b;
@@ -1739,6 +1824,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     size_t workspace_bytes, float* out_scores, float* out_loss, float* grad_q, float* grad_d,
     hiper_stream_t stream_) {
   g_launches = 0;
+  HiperRange nv("hiper_coltrast_scores_loss_grad");
   cudaStream_t stream = (cudaStream_t)stream_;
   TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
@@ -1892,6 +1978,7 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
                                              size_t workspace_bytes, float* out_scores,
                                              int64_t* out_ids, hiper_stream_t stream_) {
   g_launches = 0;
+  HiperRange nv("hiper_two_stage_topk");
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!pix || !tix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
   if (pix->ld_pad != 1) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (max_len 1)");
@@ -1968,7 +2055,9 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   a.scores = S2;
   a.score_ld = n_slots;
   a.cand = slots;
-  TRY(launch_maxsim(0, 1, kp, tq, tix->tmap_half, a, stream));
+  // an empty shard has no tensor map and no candidates (every slot is -1, so rerank_select never
+  // reads S2): skip the scoring launch, but still take part in the all-gather below
+  if (tix->n > 0) TRY(launch_maxsim(0, 1, kp, tq, tix->tmap_half, a, stream));
   if (!multi) {
     rerank_select_kernel<1><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, n_slots, slots, k1, n_q,
                                                                 tix->id_base, k, out_scores, out_ids);
@@ -1983,8 +2072,7 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   rerank_select_kernel<1><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, n_slots, slots, k1, n_q,
                                                               tix->id_base, k, nullptr, nullptr, local);
   CUDA_TRY(cudaGetLastError());
-  NCCL_TRY(ncclAllGather(local, gathered, (size_t)n_q * k, ncclUint64, comm->comm, stream));
-  TRY(launch_merge(gathered, comm->world, (int64_t)n_q * k, n_q, k, k, nullptr, out_scores, out_ids, stream));
+  TRY(gather_merge(comm, local, gathered, n_q, k, out_scores, out_ids, stream));
   g_launches += launches + 2;  // + stage 1, ids_to_slots, rerank_select
   return HIPER_OK;
 }
@@ -1993,6 +2081,7 @@ extern "C" hiper_status hiper_infonce_loss(const float* scores, int32_t n_q, int
                                            const int32_t* pos_idx, float temperature, void* workspace,
                                            size_t workspace_bytes, float* out_loss, hiper_stream_t stream_) {
   g_launches = 0;
+  HiperRange nv("hiper_infonce_loss");
   cudaStream_t stream = (cudaStream_t)stream_;
   TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
   if (!scores || !out_loss) return fail(HIPER_ERR_INVALID_ARG, "NULL pointer");

@@ -16,6 +16,38 @@ import paper_2505_04846_b200 as H
 from synth import device, gen
 
 
+def oracle_check(s, i, full, lens, q, qlen, k, what):
+    """The sharded, all-gathered answer vs the ORACLE's exact top-k over the whole corpus, for
+    sampled queries.  The oracle scores the bf16 operands of a dense layout of the full corpus,
+    after sampled rows of it are checked bitwise against the oracle's own NORM of the raw inputs."""
+    import oracle
+    from tests._compare import assert_topk_ok
+    C, L, d = full.shape
+    bits = lambda t: t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    didx = H.hiper_index_build(full, lens)                 # dense layout (NORM'd in a copy)
+    lay = bits(didx.layout())
+    rows = [0, 1, C // 2, C - 1]
+    raw = gen.corpus_tokens_f32(5, np.array(rows), L, d)
+    for j, c in enumerate(rows):
+        n = int(lens[c])
+        assert np.array_equal(lay[c, :n], oracle.norm_rows(gen.f32_to_bf16_bits(raw[j, :n]))), c
+    qlay, _ = H.hiper_prepare_queries(q, qlen)
+    qlay = bits(qlay)
+    sample = [0, len(qlen) - 1]
+    S_o = oracle.maxsim_matrix(qlay[sample], qlen[sample], lay, lens)
+    ids = np.arange(C, dtype=np.int64)
+    s, i = s.cpu().numpy(), i.cpu().numpy()
+    try:
+        for r, qq in enumerate(sample):
+            assert_topk_ok(s[qq], i[qq], S_o[r], ids, k, qlen[qq], d, f"{what} query {qq}")
+    except AssertionError as e:
+        print(f"{what}: ORACLE MISMATCH {e}", flush=True)
+        return False
+    print(f"{what}: sharded top-{k} == oracle top-{k} over all {C} chunks (queries {sample})",
+          flush=True)
+    return True
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -55,6 +87,7 @@ def main():
                 print(f"k={k} packed={packed} rank{r}: ids equal {same_i}, scores bitwise {same_s}",
                       flush=True)
                 ok &= same_i and same_s
+            ok &= oracle_check(gs[0], gi[0], full, lens_use, q, qlen, k, f"k={k} packed={packed}")
             del full, fidx
         del shard, idx
     # ---- NEXT N3 across ranks: global pooled top-k1, owner re-scoring, one more all-gather

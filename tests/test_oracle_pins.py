@@ -387,3 +387,41 @@ def test_li_grad_matches_loss_and_structure():
     assert (am < dl[None, :, None]).all()
     L1, g1, g2, _, _, _ = oracle.li_loss_grad(xq[:1], ql[:1], xd[:1], dl[:1])
     assert L1 == 0.0 and np.abs(g1).max() == 0.0 and np.abs(g2).max() == 0.0
+
+
+def _fixed_point_rows(rng, shape, d):
+    """Rows of exactly unit norm whose entries are 0 or +-1/8 (64 nonzeros, d >= 64): NORM maps them to
+    themselves bit for bit (acc = 64 * 2^-6 = 1 exactly, inv = 1), and so does x / ||x|| in float64."""
+    out = np.zeros(shape + (d,), np.float64)
+    for idx in np.ndindex(*shape):
+        nz = rng.choice(d, 64, replace=False)
+        out[idx + (nz,)] = rng.choice([-0.125, 0.125], 64)
+    return out
+
+
+@pytest.mark.parametrize("scale", [1.0, 4.0])
+def test_li_grad_straight_through_branch_on_norm_fixed_points(scale):
+    """Reading R19: with exact_norm = 0 the oracle takes the forward, the argmax and the
+    G.d sums on the bf16 NORM'd operands (the GPU's), but the Jacobian of the normalisation on the
+    float64 x/||x|| (a straight-through view of the bf16 rounding).  On NORM fixed points the two
+    operand sets coincide exactly, so this branch must equal the finite-difference-pinned
+    exact_norm = 1 branch to rounding (a power-of-two scale keeps both exact and exercises 1/||x||)."""
+    rng = np.random.default_rng(33)
+    B, Lq, M, Ld, d = 3, 5, 4, 7, 128
+    xq = _fixed_point_rows(rng, (B, Lq), d) * scale
+    xd = _fixed_point_rows(rng, (M, Ld), d) * scale
+    ql = np.array([5, 2, 4], np.int32)
+    dl = np.array([7, 1, 3, 6], np.int32)
+    ex = oracle.li_loss_grad(xq, ql, xd, dl, tau=0.5, exact_norm=True)
+    st = oracle.li_loss_grad(xq, ql, xd, dl, tau=0.5, exact_norm=False)
+    assert abs(ex[0] - st[0]) <= 1e-12 * max(1.0, abs(ex[0]))
+    assert np.array_equal(ex[3], st[3])                    # same argmax (same tie rule, same values)
+    for a, b in ((ex[1], st[1]), (ex[2], st[2])):
+        assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(a).max())
+    assert np.abs(ex[1]).max() > 0 and np.abs(ex[2]).max() > 0
+    # and away from fixed points the branches differ by the bf16 rounding only (~2^-8 relative)
+    xq2 = rng.standard_normal((B, Lq, d))
+    xd2 = rng.standard_normal((M, Ld, d))
+    e2 = oracle.li_loss_grad(xq2, ql, xd2, dl, tau=0.5, exact_norm=True)
+    s2 = oracle.li_loss_grad(xq2, ql, xd2, dl, tau=0.5, exact_norm=False)
+    assert abs(e2[0] - s2[0]) <= 2e-2 * abs(e2[0])
