@@ -307,7 +307,8 @@ def run_ours(a, rank, local_rank, world):
         del corpus
         torch.cuda.empty_cache()
     else:
-        idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_BORROW_TOKENS)
+        idx = H.hiper_index_build(corpus, lens, id_base=c0, flags=H.HIPER_BORROW_TOKENS |
+                                  (H.HIPER_POOLED if a.chunk_len == 1 else 0))
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t_build  # a1 (hiper_index_build; + generation for config4v)
     comm = H.Comm() if world > 1 else None

@@ -21,9 +21,11 @@
  *  - Token tensors are row-major [n][max_len][dim] (dim contiguous), float32 or bfloat16.  Rows
  *    j >= len of an item are ignored (never read as zero vectors into a max, reading R2/R3).
  *  - Scores are computed with bf16 operands and fp32 accumulation (tcgen05 tensor cores, sm_100a).
- *  - Supported shapes (round 1): dim in {64, 128}; q_max_len <= 32; chunk max_len <= 256;
- *    1 <= k <= 128; global ids < 2^32 - 1; n * roundup(max_len,16) < 2^31 per index.
- *    Anything else returns HIPER_ERR_UNSUPPORTED.
+ *  - Supported shapes: token dim % 16 == 0 and <= 256 (pooled: <= 4096); q_max_len <= 128;
+ *    chunk max_len <= 512 (HIPER_PACKED: <= 256); 1 <= k <= 128; global ids < 2^32 - 1;
+ *    n * roundup(max_len,16) < 2^31 per index.  Anything else returns HIPER_ERR_UNSUPPORTED.
+ *    (Narrower: the N1 backward takes q_max_len <= 32, d_max_len <= 256, dim 64 or 128; the N3
+ *    rerank takes token dim <= 128, q_max_len <= 32, max_len <= 256.)
  *  - No CPU fallback exists: without an sm_100 device every compute call returns HIPER_ERR_UNSUPPORTED
  *    or HIPER_ERR_CUDA.
  */
@@ -90,7 +92,12 @@ enum {
    * and overwritten as above), NORM'd in place: no second copy of the corpus (the paper-scale 16.4M-chunk corpus,
    * PAPER.md:564, at 110 GB per GPU on 4 GPUs).  The buffer must hold n_rows rows and outlive the
    * index. */
-  HIPER_PACKED = 16u
+  HIPER_PACKED = 16u,
+  /* hiper_index_build only: a POOLED index (the a12 limit case; "cosine similarity on
+   * the pooled embeddings"): one vector per item (max_len must be 1), scored by the pooled GEMM kernel,
+   * queried with q_max_len 1.  dim % 16 == 0, <= 4096.  Without this flag a max_len-1 index is a token
+   * index like any other (any query length scores against its single row). */
+  HIPER_POOLED = 32u
 };
 
 typedef struct hiper_index_s hiper_index; /* opaque; immutable after build; shareable by readers */
@@ -148,8 +155,9 @@ HIPER_API hiper_status hiper_index_pack_info(const hiper_index* idx, int32_t* pa
                                    int64_t* n_rows, const void** tiles_dev, const void** ents_dev);
 
 /* ------------------------------------------------------------------ step a2: query preparation
- * NORM every real query row into the kernel's query layout: out device bf16 [n_q_pad][32][dim] with
- * n_q_pad = roundup(n_q, 8); rows i >= q_lens[q] and queries q >= n_q are zero.  status: device
+ * NORM every real query row into the kernel's query layout: out device bf16 [n_q_pad][QS][dim] with
+ * QS = 32 / 64 / 128 for q_max_len <= 32 / 64 / 128 (one, two or four warps of TMEM lanes per query)
+ * and n_q_pad = roundup(n_q, 256 / QS); rows i >= q_lens[q] and queries q >= n_q are zero.  status: device
  * uint32 (bit 0: zero row, bit 1: non-finite row), OR-ed, may be NULL.  Exposed so the layout can be
  * checked bitwise against the oracle's NORM; the search/loss entry points call it internally. */
 HIPER_API hiper_status hiper_prepare_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
@@ -281,7 +289,8 @@ HIPER_API hiper_status hiper_coltrast_scores_loss_grad(
  * the final top-k
  * (ColBERTv2's retrieve-then-rerank; SPEC.md:268-276 rerank; score desc, id asc).
  *   q_pooled device [n_q][pooled dim]; q_tokens device [n_q][q_max_len][token dim]; q_lens HOST.
- *   1 <= k <= k1 <= 16.
+ *   1 <= k <= k1 <= 128.  Stage 2 computes each query's own k1 candidates exactly once (a gather of
+ *   their token rows, HBM-bound); token dim <= 128, q_max_len <= 32, max_len <= 256.
  *   comm: NULL = this shard only.  With a communicator every rank passes the same queries and its
  *   own shard (both indexes with the shard's id_base): stage 1 is the global pooled top-k1 (one
  *   all-gather), each rank re-scores the candidates it owns, and one more all-gather + merge gives

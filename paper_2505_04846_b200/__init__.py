@@ -29,6 +29,7 @@ HIPER_CHECK_FINITE = 2
 HIPER_BORROW_TOKENS = 4
 HIPER_VALIDATE_SYNC = 8
 HIPER_PACKED = 16
+HIPER_POOLED = 32
 
 STATUS = {
     0: "HIPER_OK", 1: "HIPER_ERR_INVALID_ARG", 2: "HIPER_ERR_DIM_MISMATCH",
@@ -343,8 +344,10 @@ def hiper_prepare_queries(q_tokens, q_lens, *, flags: int = 0, stream=None):
     torch = _torch()
     n_q, q_max_len, dim = q_tokens.shape
     ql = _host_i32(q_lens)
-    n_pad = max(8, (n_q + 7) // 8 * 8)
-    out = torch.empty((n_pad, 32, dim), dtype=torch.bfloat16, device=q_tokens.device)
+    qs = 32 if q_max_len <= 32 else (64 if q_max_len <= 64 else 128)   # query slot rows
+    per = 256 // qs
+    n_pad = max(per, (n_q + per - 1) // per * per)
+    out = torch.empty((n_pad, qs, dim), dtype=torch.bfloat16, device=q_tokens.device)
     status = torch.zeros(1, dtype=torch.int32, device=q_tokens.device)
     _check(lib().hiper_prepare_queries(_dev_ptr(q_tokens), _dtype_code(q_tokens), _ptr(ql), n_q,
                                        q_max_len, dim, flags, _dev_ptr(out), _dev_ptr(status),

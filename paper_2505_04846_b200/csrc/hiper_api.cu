@@ -23,10 +23,10 @@
 
 #include "../../include/hiper.h"
 #include "kernels/infonce.cuh"
-#include "kernels/maxsim_sm100.cuh"
 #include "kernels/maxsim_backward.cuh"
 #include "kernels/maxsim_sm100_pair.cuh"
 #include "kernels/pooled_sm100_pair.cuh"
+#include "kernels/rerank_gather.cuh"
 #include "kernels/norm_layout.cuh"
 #include "kernels/topk_merge.cuh"
 
@@ -88,7 +88,9 @@ struct HiperRange {
   HiperRange& operator=(const HiperRange&) = delete;
 };
 
-static constexpr int32_t kMaxK = 128;  // top-k capacity of every list (register / warp lists)
+static constexpr int32_t kMaxK = 128;         // top-k capacity of every list (register / warp lists)
+static constexpr int32_t kMaxChunkLen = 512;  // chunk tokens (> 256: two MMA halves per chunk)
+static constexpr int32_t kMaxQueryLen = 128;  // query tokens (query slots of 32, 64 or 128 rows)
 
 extern "C" const char* hiper_last_error(void) { return g_last_error.c_str(); }
 extern "C" int32_t hiper_version(void) { return 100; }
@@ -224,7 +226,6 @@ static cudaError_t set_max_smem(const void* fn, int bytes) {
 }
 static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-static bool use_pair_kernel();
 
 // ============================================================================ the index
 struct hiper_index_s {
@@ -235,8 +236,9 @@ struct hiper_index_s {
   __nv_bfloat16* tok = nullptr;  // [n][ld_pad][dim]
   bool owns_tok = false;
   int32_t* lens = nullptr;  // device [n]
-  alignas(64) CUtensorMap tmap;       // box = 64 dims x ld_pad rows   (single-CTA kernel)
-  alignas(64) CUtensorMap tmap_half;  // box = 64 dims x ld_pad/2 rows (CTA-pair kernel)
+  bool pooled = false;                // HIPER_POOLED: one vector per item (a12)
+  alignas(64) CUtensorMap tmap;       // pooled: box = 64 dims x 128 rows
+  alignas(64) CUtensorMap tmap_half;  // tokens: box = 64 dims x (ld_pad/2 | 128) rows (CTA pair)
   // packed layout (HIPER_PACKED, N4): tok is bf16 [n_rows][dim]; tiles/ents as in MaxsimArgs
   bool packed = false;
   int64_t n_tiles = 0, n_rows = 0;
@@ -330,19 +332,18 @@ extern "C" hiper_status hiper_pack_plan(const int32_t* lens, int64_t n, int32_t*
   return HIPER_OK;
 }
 
-// Token path (max_len > 1): dim in {64, 128}.  Pooled path (one row per item, a12): dim % 64 == 0,
-// 64 <= dim <= 4096.
+// dim % 16 == 0 (one MMA K step; the TMA boxes are 64 wide and zero-fill the columns past dim).
+// Token path: dim <= 256.  Pooled path (HIPER_POOLED, one row per item, a12): dim <= 4096.
+static constexpr int32_t kMaxTokenDim = 256, kMaxPooledDim = 4096;
 static hiper_status check_dims(int32_t dim, bool pooled = false) {
   if (dim <= 0) return fail(HIPER_ERR_INVALID_ARG, "dim must be positive (got %d)", dim);
-  if (pooled) {
-    if (dim % 64 != 0 || dim > 4096)
-      return fail(HIPER_ERR_UNSUPPORTED, "pooled dim %d unsupported (multiple of 64, <= 4096)", dim);
-    return HIPER_OK;
-  }
-  if (dim != 64 && dim != 128)
-    return fail(HIPER_ERR_UNSUPPORTED, "dim %d unsupported for token rows (64 or 128)", dim);
+  const int32_t mx = pooled ? kMaxPooledDim : kMaxTokenDim;
+  if (dim % 16 != 0 || dim > mx)
+    return fail(HIPER_ERR_UNSUPPORTED, "%s dim %d unsupported (multiple of 16, <= %d)",
+                pooled ? "pooled" : "token", dim, mx);
   return HIPER_OK;
 }
+static inline int32_t num_kb_of(int32_t dim) { return (dim + 63) / 64; }
 
 static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src, int32_t in_rows,
                                 const int32_t* lens_dev, int64_t n_items, int32_t out_rows,
@@ -353,7 +354,7 @@ static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src
   const int threads = 256;
   const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
   const uint32_t cf = (flags & HIPER_CHECK_FINITE) ? 1u : 0u;
-  if (dim == 64 || dim == 128) {  // d/16 threads per row: coalesced, same fma order (bit-identical)
+  if (dim == 64 || dim == 128 || dim == 256) {  // d/16 threads per row: coalesced, same fma order
     const int tpr = dim / 16;
     const int64_t blocks = (rows * tpr + threads - 1) / threads;
     if (blocks > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
@@ -361,15 +362,17 @@ static hiper_status launch_norm(const void* in, hiper_dtype dtype, int64_t n_src
   norm_layout_tpr_kernel<T, TPR><<<(unsigned)blocks, threads, 0, stream>>>(                          \
       (const T*)in, n_src, in_rows, lens_dev, n_items, out_rows, dim, an, cf, out, status, dst_row)
     if (dtype == HIPER_F32) {
-      if (tpr == 4) HIPER_NORM_TPR(float, 4); else HIPER_NORM_TPR(float, 8);
+      if (tpr == 4) HIPER_NORM_TPR(float, 4); else if (tpr == 8) HIPER_NORM_TPR(float, 8); else HIPER_NORM_TPR(float, 16);
     } else {
-      if (tpr == 4) HIPER_NORM_TPR(__nv_bfloat16, 4); else HIPER_NORM_TPR(__nv_bfloat16, 8);
+      if (tpr == 4) HIPER_NORM_TPR(__nv_bfloat16, 4); else if (tpr == 8) HIPER_NORM_TPR(__nv_bfloat16, 8); else HIPER_NORM_TPR(__nv_bfloat16, 16);
     }
 #undef HIPER_NORM_TPR
     CUDA_TRY(cudaGetLastError());
     ++g_launches;
     return HIPER_OK;
   }
+  if (dst_row != nullptr && in == (const void*)out)
+    return fail(HIPER_ERR_UNSUPPORTED, "in-place packed layout needs dim 64, 128 or 256");
   const int64_t blocks = (rows + threads - 1) / threads;
   if (blocks > 0x7FFFFFFF) return fail(HIPER_ERR_UNSUPPORTED, "too many rows");
   if (dtype == HIPER_F32)
@@ -393,7 +396,10 @@ static hiper_status launch_norm2(const void* in_a, int64_t n_a, int32_t in_rows_
                                  hiper_dtype dtype, int32_t dim, uint32_t flags, uint32_t* status,
                                  cudaStream_t stream) {
   const int threads = 256;
-  if (dim != 64 && dim != 128) return fail(HIPER_ERR_UNSUPPORTED, "token dim %d", dim);
+  if (dim != 64 && dim != 128 && dim != 256) {  // other dims: the one-thread-per-row kernel, twice
+    TRY(launch_norm(in_a, dtype, n_a, in_rows_a, lens_a, items_a, out_rows_a, dim, flags, out_a, status, stream));
+    return launch_norm(in_b, dtype, n_b, in_rows_b, lens_b, items_b, out_rows_b, dim, flags, out_b, status, stream);
+  }
   const int tpr = dim / 16;
   const int64_t ba = (items_a * out_rows_a * tpr + threads - 1) / threads;
   const int64_t bb = (items_b * out_rows_b * tpr + threads - 1) / threads;
@@ -406,9 +412,9 @@ static hiper_status launch_norm2(const void* in_a, int64_t n_a, int32_t in_rows_
 #define HIPER_NORM2(T, TPR) \
   norm_layout2_kernel<T, TPR><<<(unsigned)(ba + bb), threads, 0, stream>>>(a, b, ba, dim, an, cf, status)
   if (dtype == HIPER_F32) {
-    if (tpr == 4) HIPER_NORM2(float, 4); else HIPER_NORM2(float, 8);
+    if (tpr == 4) HIPER_NORM2(float, 4); else if (tpr == 8) HIPER_NORM2(float, 8); else HIPER_NORM2(float, 16);
   } else {
-    if (tpr == 4) HIPER_NORM2(__nv_bfloat16, 4); else HIPER_NORM2(__nv_bfloat16, 8);
+    if (tpr == 4) HIPER_NORM2(__nv_bfloat16, 4); else if (tpr == 8) HIPER_NORM2(__nv_bfloat16, 8); else HIPER_NORM2(__nv_bfloat16, 16);
   }
 #undef HIPER_NORM2
   CUDA_TRY(cudaGetLastError());
@@ -437,11 +443,14 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   *out = nullptr;
   if (n < 0) return fail(HIPER_ERR_INVALID_ARG, "n < 0");
   if (dtype != HIPER_F32 && dtype != HIPER_BF16) return fail(HIPER_ERR_INVALID_ARG, "bad dtype");
-  if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_BORROW_TOKENS | HIPER_PACKED))
+  if (flags & ~(uint32_t)(HIPER_ASSUME_NORMALIZED | HIPER_CHECK_FINITE | HIPER_BORROW_TOKENS |
+                          HIPER_PACKED | HIPER_POOLED))
     return fail(HIPER_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   if (max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "max_len must be >= 1");
-  if (max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "max_len %d > 256", max_len);
-  const bool pooled = (max_len == 1) && !(flags & HIPER_PACKED);  // the pooled limit case (a12)
+  if (max_len > kMaxChunkLen) return fail(HIPER_ERR_UNSUPPORTED, "max_len %d > %d", max_len, kMaxChunkLen);
+  const bool pooled = (flags & HIPER_POOLED) != 0;  // the pooled limit case (a12)
+  if (pooled && (max_len != 1 || (flags & HIPER_PACKED)))
+    return fail(HIPER_ERR_INVALID_ARG, "HIPER_POOLED takes one vector per item (max_len 1, not packed)");
   TRY(check_dims(dim, pooled));
   if (id_base < 0 || id_base + n >= 0xFFFFFFFFll)
     return fail(HIPER_ERR_UNSUPPORTED, "global ids must be < 2^32-1");
@@ -451,10 +460,10 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
     return fail(HIPER_ERR_UNSUPPORTED, "n * ld_pad >= 2^31 rows for one index; shard the corpus");
   TRY(check_lens(lens, n, max_len, "chunk"));
   const bool borrow = (flags & HIPER_BORROW_TOKENS) != 0;
-  if (packed && borrow && (dtype != HIPER_BF16 || (dim != 64 && dim != 128)))
+  if (packed && borrow && dtype != HIPER_BF16)
     return fail(HIPER_ERR_INVALID_ARG, "HIPER_PACKED | HIPER_BORROW_TOKENS needs bf16 packed tokens");
-  if (packed && !use_pair_kernel())
-    return fail(HIPER_ERR_UNSUPPORTED, "HIPER_PACKED needs the CTA-pair kernel (HIPER_MAXSIM_CTA=1 set)");
+  if (packed && borrow && dim != 64 && dim != 128 && dim != 256)
+    return fail(HIPER_ERR_UNSUPPORTED, "in-place packed layout needs dim 64, 128 or 256");
   std::vector<int4> p_tiles;
   std::vector<int2> p_ents;
   std::vector<int64_t> p_dst;
@@ -477,6 +486,7 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
   ix->dim = dim;
   ix->id_base = id_base;
   ix->device = di.device;
+  ix->pooled = pooled;
   int64_t* dst_dev = nullptr;
   auto cleanup = [&](hiper_status s) {
     if (ix->owns_tok && ix->tok) cudaFree(ix->tok);
@@ -557,8 +567,8 @@ extern "C" hiper_status hiper_index_build(const void* tokens, hiper_dtype dtype,
       // half a full tile per CTA; a shorter tile's MMA reads only its first n_rows/2 rows
       st = make_tmap(&ix->tmap_half, ix->tok, p_rows, dim, kTileRows / 2);
     } else if (n > 0) {
-      st = make_tmap(&ix->tmap, ix->tok, n * (int64_t)ld_pad, dim, ld_pad);
-      if (st == HIPER_OK) st = make_tmap(&ix->tmap_half, ix->tok, n * (int64_t)ld_pad, dim, ld_pad / 2);
+      // this CTA's rows of a chunk: ld_pad / 2, or 128 of each 256-row half when ld_pad > 256
+      st = make_tmap(&ix->tmap_half, ix->tok, n * (int64_t)ld_pad, dim, ld_pad > 256 ? 128 : ld_pad / 2);
     }
   } while (0);
   cudaFree(status);
@@ -607,10 +617,18 @@ extern "C" hiper_status hiper_index_pack_info(const hiper_index* ix, int32_t* pa
 }
 
 // ============================================================================ query preparation
-static constexpr int32_t kQSlot = 32;  // padded query-token rows per query (one warp of TMEM lanes)
-
-// Queries are padded to a multiple of 8: one CTA pair's M = 256 rows = 8 queries x 32 token rows.
-static int32_t n_q_pad_of(int32_t n_q) { return (int32_t)round_up(std::max(n_q, 1), 8); }
+// A query occupies QS = 32, 64 or 128 padded token rows (q_max_len <= 32 / 64 / 128): one, two or
+// four warps of TMEM lanes.  Queries are padded to fill whole CTA pairs: M = 256 rows = 256 / QS.
+static int32_t qs_of(int32_t q_max_len) { return q_max_len <= 32 ? 32 : (q_max_len <= 64 ? 64 : 128); }
+static int32_t n_q_pad_of(int32_t n_q, int32_t qs = 32) {
+  return (int32_t)round_up(std::max(n_q, 1), 256 / qs);
+}
+// Query layout bytes for any q_max_len (the workspace-size entry points do not take q_max_len).
+static size_t q_layout_bytes_max(int32_t n_q, int32_t dim) {
+  size_t m = 0;
+  for (int32_t qs = 32; qs <= 128; qs *= 2) m = std::max(m, (size_t)n_q_pad_of(n_q, qs) * qs * dim * 2);
+  return m;
+}
 
 static hiper_status validate_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
                                      int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags,
@@ -621,9 +639,9 @@ static hiper_status validate_queries(const void* q_tokens, hiper_dtype dtype, co
     return fail(HIPER_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   TRY(check_dims(dim, pooled));
   if (pooled && q_max_len != 1)
-    return fail(HIPER_ERR_UNSUPPORTED, "a pooled index (max_len 1) takes pooled queries (q_max_len 1)");
+    return fail(HIPER_ERR_UNSUPPORTED, "a pooled index (HIPER_POOLED) takes pooled queries (q_max_len 1)");
   if (q_max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "q_max_len must be >= 1");
-  if (q_max_len > kQSlot) return fail(HIPER_ERR_UNSUPPORTED, "q_max_len %d > 32", q_max_len);
+  if (q_max_len > kMaxQueryLen) return fail(HIPER_ERR_UNSUPPORTED, "q_max_len %d > %d", q_max_len, kMaxQueryLen);
   TRY(check_lens(q_lens, n_q, q_max_len, "query"));
   if (n_q > 0) {
     if (!q_tokens) return fail(HIPER_ERR_INVALID_ARG, "q_tokens is NULL");
@@ -633,13 +651,14 @@ static hiper_status validate_queries(const void* q_tokens, hiper_dtype dtype, co
   return HIPER_OK;
 }
 
-// Device-side query prep: q_lens HOST -> lens_dev (staged), NORM into layout [n_q_pad][32][dim].
+// Device-side query prep: q_lens HOST -> lens_dev (staged), NORM into layout [n_q_pad][QS][dim].
 static hiper_status prep_queries(const void* q_tokens, hiper_dtype dtype, const int32_t* q_lens,
                                  int32_t n_q, int32_t q_max_len, int32_t dim, uint32_t flags,
                                  int32_t* lens_dev, __nv_bfloat16* layout, uint32_t* status,
                                  cudaStream_t stream) {
   TRY(stage_h2d(lens_dev, q_lens, (size_t)n_q * sizeof(int32_t), stream));
-  return launch_norm(q_tokens, dtype, n_q, q_max_len, lens_dev, n_q_pad_of(n_q), kQSlot, dim, flags,
+  const int32_t qs = qs_of(q_max_len);
+  return launch_norm(q_tokens, dtype, n_q, q_max_len, lens_dev, n_q_pad_of(n_q, qs), qs, dim, flags,
                      layout, status, stream);
 }
 
@@ -705,46 +724,67 @@ static int32_t choose_parts_topk(int32_t n_groups, int64_t n_slots, int num_slot
   return (int32_t)std::max<int64_t>(1, std::min<int64_t>(p, n_slots));
 }
 
-// Kernel shape: the CTA-pair kernel (cta_group::2, M = 256) is the production path; the
-// single-CTA kernel (M = 128) is kept for ablation only (HIPER_MAXSIM_CTA=1).
-static bool use_pair_kernel() {
-  static const bool pair = [] {
-    const char* e = getenv("HIPER_MAXSIM_CTA");
-    return !(e && e[0] == '1');
-  }();
-  return pair;
-}
-
+// The MaxSim kernel is the CTA-pair kernel (cta_group::2, M = 256 query-token rows per pair).
 struct KernelPlan {
-  bool pair = true;
-  int32_t qpg = 8;  // queries per row group (8 for a CTA pair, 4 for one CTA)
-  int32_t n_groups = 0, n_parts = 0, n_stages = 0;
-  uint32_t a_bytes = 0, stage_bytes = 0, smem_bytes = 0;
+  int32_t qs = 32, qw = 1, h = 1;  // query slot rows, warps per query, MMA halves per chunk
+  int32_t qpg = 8;                 // queries per row group (256 / qs)
+  int32_t n_q_pad = 0, n_groups = 0, n_parts = 0, n_stages = 0, a_bufs = 2;
+  uint32_t a_bytes = 0, stage_bytes = 0, box_rows = 0, smem_bytes = 0;
   int grid = 0;
 };
 
-static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int64_t n_chunks, int32_t ld_pad,
-                                int32_t dim, KernelPlan& kp, int32_t topk_k = 0) {
-  kp.pair = use_pair_kernel();
-  kp.qpg = kp.pair ? 8 : 4;
-  const int slots = kp.pair ? di.num_sms / 2 : di.num_sms;  // CTA pairs or CTAs
-  kp.n_groups = n_q_pad_of(n_q) / kp.qpg;
-  kp.n_parts = topk_k > 0 ? choose_parts_topk(kp.n_groups, n_chunks, slots, (int64_t)ld_pad * dim * 2,
-                                              n_q_pad_of(n_q), topk_k)
-                          : choose_parts(kp.n_groups, n_chunks, slots);
-  kp.a_bytes = (uint32_t)(dim / 64) * 16384u;
-  // pair kernel: one stage = this CTA's half of a whole chunk (all K-blocks); single-CTA kernel:
-  // one stage = one 64-dim K-block of a whole chunk
-  kp.stage_bytes = kp.pair ? (uint32_t)(ld_pad / 2) * 128u * (uint32_t)(dim / 64)
-                           : (uint32_t)ld_pad * 128u;
-  const uint32_t fixed = 1024u /*align slack*/ + 2u * kp.a_bytes + 1024u /*barriers, meta, ring*/;
-  const uint32_t avail = (uint32_t)di.max_smem > fixed ? (uint32_t)di.max_smem - fixed : 0u;
-  kp.n_stages = (int32_t)std::min<uint32_t>(kp.pair ? 12u : 8u, avail / kp.stage_bytes);
+// slot_rows: token rows per kernel slot (a chunk's ld_pad, or 256 for a packed tile).
+static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int32_t q_max_len, int64_t n_slots,
+                                int32_t slot_rows, int32_t dim, KernelPlan& kp, int32_t topk_k = 0) {
+  kp.qs = qs_of(q_max_len);
+  kp.qw = kp.qs / 32;
+  kp.qpg = 256 / kp.qs;
+  kp.h = slot_rows > 256 ? 2 : 1;
+  const int slots = di.num_sms / 2;  // CTA pairs
+  kp.n_q_pad = n_q_pad_of(n_q, kp.qs);
+  kp.n_groups = kp.n_q_pad / kp.qpg;
+  kp.n_parts = topk_k > 0 ? choose_parts_topk(kp.n_groups, n_slots, slots, (int64_t)slot_rows * dim * 2,
+                                              kp.n_q_pad, topk_k)
+                          : choose_parts(kp.n_groups, n_slots, slots);
+  const uint32_t nkb = (uint32_t)num_kb_of(dim);
+  kp.a_bytes = nkb * 16384u;
+  // one stage = this CTA's rows of one chunk (half): ld_pad / 2, or 128 of a 256-row half
+  kp.box_rows = kp.h == 2 ? 128u : (uint32_t)slot_rows / 2;
+  kp.stage_bytes = kp.box_rows * 128u * nkb;
+  // A double-buffered across units when two stages still fit, else single-buffered (large dims)
+  for (kp.a_bufs = 2; kp.a_bufs >= 1; --kp.a_bufs) {
+    const uint32_t fixed = 1024u /*align slack*/ + kp.a_bufs * kp.a_bytes + 2048u /*barriers, ring, sums*/;
+    const uint32_t avail = (uint32_t)di.max_smem > fixed ? (uint32_t)di.max_smem - fixed : 0u;
+    kp.n_stages = (int32_t)std::min<uint32_t>(12u, avail / kp.stage_bytes);
+    kp.smem_bytes = fixed + kp.n_stages * kp.stage_bytes;
+    if (kp.n_stages >= 2) break;
+  }
   if (kp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory for 2 stages");
-  kp.smem_bytes = fixed + kp.n_stages * kp.stage_bytes;
   const int64_t units = (int64_t)kp.n_groups * kp.n_parts;
-  kp.grid = (int)std::min<int64_t>(units, slots) * (kp.pair ? 2 : 1);
+  kp.grid = (int)std::min<int64_t>(units, slots) * 2;
   return HIPER_OK;
+}
+
+// The kernel arguments every MaxSim launch shares (plan + query side + the index's slots).
+static MaxsimArgs maxsim_args(const KernelPlan& kp, int32_t n_q, int64_t n_slots, int32_t ld_pad,
+                              int32_t dim, const int32_t* qlens_dev, const int32_t* dlens_dev) {
+  MaxsimArgs a{};
+  a.n_q = n_q;
+  a.n_groups = kp.n_groups;
+  a.n_parts = kp.n_parts;
+  a.ld_pad = ld_pad;
+  a.num_kb = num_kb_of(dim);
+  a.k = 1;
+  a.n_stages = kp.n_stages;
+  a.a_bytes = kp.a_bytes;
+  a.stage_bytes = kp.stage_bytes;
+  a.box_rows = kp.box_rows;
+  a.a_bufs = kp.a_bufs;
+  a.q_pad = kp.n_q_pad;
+  a.n_chunks = n_slots;
+  a.q_lens = qlens_dev;
+  a.d_lens = dlens_dev;
+  return a;
 }
 
 // ---------------------------------------------------------------------------- live kernel timing
@@ -810,65 +850,58 @@ static int debug_mode() {
   return m;
 }
 
-template <int MODE, int KR, bool PACKED = false>
+template <int MODE, int KR, bool PACKED, int QW, int H>
 static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
                                     const MaxsimArgs& a, cudaStream_t stream) {
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   bool rec = false;
-  if (kp.pair) {
-    static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
-    // production: no instrumentation compiled in; HIPER_PIPE_STATS / HIPER_DEBUG_MODE select the
-    // instrumented (STATS) instantiations
-    auto kern = stats_on ? maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED, true>
-                         : maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED, false>;
-    if constexpr (!PACKED && MODE == 1 && KR == 1) {
-      if (debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1, false, true>;
-      if (debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2, false, true>;
-      if (debug_mode() == 3) kern = maxsim_sm100_pair_kernel<MODE, KR, 3, false, true>;
-      if (debug_mode() == 4) kern = maxsim_sm100_pair_kernel<MODE, KR, 4, false, true>;
-    }
-    CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)kp.grid);
-    cfg.blockDim = dim3(kMaxsimThreads);
-    cfg.dynamicSmemBytes = kp.smem_bytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    // programmatic dependent launch: the kernel's set-up (barriers, TMEM, tensor-map prefetch)
-    // overlaps the previous kernel's tail; it waits (griddepcontrol.wait) before reading its inputs
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    unsigned long long* st = nullptr;
-    MaxsimArgs b = a;
-    if (stats_on) {
-      CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
-      CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
-      b.stats = st;
-    }
-    TRY(profile_begin(stream, &ev, &rec));
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, td, b));
-    if (st) {
-      unsigned long long h[8];
-      CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, stream));
-      CUDA_TRY(cudaStreamSynchronize(stream));
-      cudaFree(st);
-      const double pairs = kp.grid / 2.0, ep = 8.0 * kp.grid;
-      fprintf(stderr, "[hiper pipe] maxsim%s: MMA thread %.0f cyc avg; waits acc %.1f%% full %.1f%%; "
-              "epilogue drain %.0f cyc/tile, wait %.0f cyc/tile, tiles/warp %.0f\n",
-              PACKED ? " (packed)" : "", h[2] / pairs, 100.0 * h[0] / h[2], 100.0 * h[1] / h[2],
-              (double)h[3] / h[5], (double)h[4] / h[5], h[5] / ep);
-    }
-  } else {
-    auto kern = maxsim_sm100_kernel<MODE, KR>;
-    CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
-    TRY(profile_begin(stream, &ev, &rec));
-    kern<<<kp.grid, kMaxsimThreads, kp.smem_bytes, stream>>>(tq, td, a);
+  static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
+  // production: no instrumentation compiled in; HIPER_PIPE_STATS / HIPER_DEBUG_MODE select the
+  // instrumented (STATS) instantiations
+  auto kern = stats_on ? maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED, true, QW, H>
+                       : maxsim_sm100_pair_kernel<MODE, KR, 0, PACKED, false, QW, H>;
+  if constexpr (!PACKED && MODE == 1 && KR == 1 && QW == 1 && H == 1) {
+    if (debug_mode() == 1) kern = maxsim_sm100_pair_kernel<MODE, KR, 1, false, true>;
+    if (debug_mode() == 2) kern = maxsim_sm100_pair_kernel<MODE, KR, 2, false, true>;
+    if (debug_mode() == 3) kern = maxsim_sm100_pair_kernel<MODE, KR, 3, false, true>;
+    if (debug_mode() == 4) kern = maxsim_sm100_pair_kernel<MODE, KR, 4, false, true>;
+  }
+  CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)kp.grid);
+  cfg.blockDim = dim3(kMaxsimThreads);
+  cfg.dynamicSmemBytes = kp.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch: the kernel's set-up (barriers, TMEM, tensor-map prefetch)
+  // overlaps the previous kernel's tail; it waits (griddepcontrol.wait) before reading its inputs
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  unsigned long long* st = nullptr;
+  MaxsimArgs b = a;
+  if (stats_on) {
+    CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
+    b.stats = st;
+  }
+  TRY(profile_begin(stream, &ev, &rec));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, td, b));
+  if (st) {
+    unsigned long long h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    cudaFree(st);
+    const double pairs = kp.grid / 2.0, ep = 8.0 * kp.grid;
+    fprintf(stderr, "[hiper pipe] maxsim%s: MMA thread %.0f cyc avg; waits acc %.1f%% full %.1f%%; "
+            "epilogue drain %.0f cyc/tile, wait %.0f cyc/tile, tiles/warp %.0f\n",
+            PACKED ? " (packed)" : "", h[2] / pairs, 100.0 * h[0] / h[2], 100.0 * h[1] / h[2],
+            (double)h[3] / h[5], (double)h[4] / h[5], h[5] / ep);
   }
   CUDA_TRY(cudaGetLastError());
   TRY(profile_end(stream, ev, rec));
@@ -876,25 +909,46 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
   return HIPER_OK;
 }
 
+// MODE 0 dense scores, 1 top-k (KR = ceil(k / 32) register ranks per lane), 2 scores + argmax;
+// packed (a.recs) or dense; QW = kp.qw warps per query; H = kp.h MMA halves per chunk.
+template <int MODE, int KR, bool PACKED>
+static hiper_status launch_maxsim_qh(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
+                                     const MaxsimArgs& a, cudaStream_t stream) {
+  if constexpr (PACKED) {
+    if (kp.h != 1) return fail(HIPER_ERR_UNSUPPORTED, "packed tiles hold <= 256 rows");
+    if (kp.qw == 1) return launch_maxsim_t<MODE, KR, true, 1, 1>(kp, tq, td, a, stream);
+    if (kp.qw == 2) return launch_maxsim_t<MODE, KR, true, 2, 1>(kp, tq, td, a, stream);
+    return launch_maxsim_t<MODE, KR, true, 4, 1>(kp, tq, td, a, stream);
+  } else {
+    if (kp.h == 1) {
+      if (kp.qw == 1) return launch_maxsim_t<MODE, KR, false, 1, 1>(kp, tq, td, a, stream);
+      if (kp.qw == 2) return launch_maxsim_t<MODE, KR, false, 2, 1>(kp, tq, td, a, stream);
+      return launch_maxsim_t<MODE, KR, false, 4, 1>(kp, tq, td, a, stream);
+    }
+    if (kp.qw == 1) return launch_maxsim_t<MODE, KR, false, 1, 2>(kp, tq, td, a, stream);
+    if (kp.qw == 2) return launch_maxsim_t<MODE, KR, false, 2, 2>(kp, tq, td, a, stream);
+    return launch_maxsim_t<MODE, KR, false, 4, 2>(kp, tq, td, a, stream);
+  }
+}
+
 static hiper_status launch_maxsim(int mode, int k, const KernelPlan& kp, const CUtensorMap& tq,
                                   const CUtensorMap& td, const MaxsimArgs& a, cudaStream_t stream) {
   if (kp.grid == 0) return HIPER_OK;
-  if (a.recs != nullptr) {  // packed corpus (N4)
-    if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "a packed index needs the CTA-pair kernel");
-    if (mode == 0) return launch_maxsim_t<0, 1, true>(kp, tq, td, a, stream);
-    if (mode != 1) return fail(HIPER_ERR_UNSUPPORTED, "argmax capture on a packed index");
-    if (k <= 32) return launch_maxsim_t<1, 1, true>(kp, tq, td, a, stream);
-    if (k <= 64) return launch_maxsim_t<1, 2, true>(kp, tq, td, a, stream);
-    return launch_maxsim_t<1, 4, true>(kp, tq, td, a, stream);
-  }
-  if (mode == 0) return launch_maxsim_t<0, 1>(kp, tq, td, a, stream);
   if (mode == 2) {
-    if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "argmax capture needs the CTA-pair kernel");
-    return launch_maxsim_t<2, 1>(kp, tq, td, a, stream);
+    if (a.recs != nullptr || kp.qw != 1 || kp.h != 1)
+      return fail(HIPER_ERR_UNSUPPORTED, "argmax capture needs a dense layout, q_max_len <= 32, d_max_len <= 256");
+    return launch_maxsim_t<2, 1, false, 1, 1>(kp, tq, td, a, stream);
   }
-  if (k <= 32) return launch_maxsim_t<1, 1>(kp, tq, td, a, stream);
-  if (k <= 64) return launch_maxsim_t<1, 2>(kp, tq, td, a, stream);
-  return launch_maxsim_t<1, 4>(kp, tq, td, a, stream);
+  if (a.recs != nullptr) {  // packed corpus (N4)
+    if (mode == 0) return launch_maxsim_qh<0, 1, true>(kp, tq, td, a, stream);
+    if (k <= 32) return launch_maxsim_qh<1, 1, true>(kp, tq, td, a, stream);
+    if (k <= 64) return launch_maxsim_qh<1, 2, true>(kp, tq, td, a, stream);
+    return launch_maxsim_qh<1, 4, true>(kp, tq, td, a, stream);
+  }
+  if (mode == 0) return launch_maxsim_qh<0, 1, false>(kp, tq, td, a, stream);
+  if (k <= 32) return launch_maxsim_qh<1, 1, false>(kp, tq, td, a, stream);
+  if (k <= 64) return launch_maxsim_qh<1, 2, false>(kp, tq, td, a, stream);
+  return launch_maxsim_qh<1, 4, false>(kp, tq, td, a, stream);
 }
 
 static hiper_status launch_merge(const uint64_t* lists, int32_t n_lists, int64_t list_stride,
@@ -1021,7 +1075,8 @@ struct TopkWs {
 };
 static constexpr int32_t kLockstepWindow = 192;  // chunks (12 MB of a 256 x 128 bf16 corpus)
 
-static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t k,
+// n_q_pad / n_parts: the kernel plan's (they depend on the query slot size)
+static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_q_pad, int32_t n_parts, int32_t k,
                            int32_t world, bool with_comm, TopkWs& w) {
   size_t off = 0;
   w.status = off;
@@ -1031,9 +1086,9 @@ static void topk_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t k,
   w.qlens = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
   w.qlayout = off;
-  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
+  off = align_up(off + q_layout_bytes_max(n_q, dim), 1024);
   w.partial = off;
-  off = align_up(off + (size_t)n_parts * kEpiGroups * n_q_pad_of(n_q) * k * 8, 256);
+  off = align_up(off + (size_t)n_parts * kEpiGroups * n_q_pad * k * 8, 256);
   w.local = off;
   if (with_comm) off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
   w.gathered = off;
@@ -1062,20 +1117,24 @@ static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, cons
 extern "C" size_t hiper_maxsim_topk_workspace_size(const hiper_index* ix, int32_t n_q, int32_t k,
                                                    const hiper_comm* comm) {
   if (!ix || n_q < 0 || k < 1) return 0;
-  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, k, comm, true);
+  if (ix->pooled) return pooled_ws_size(ix, n_q, k, comm, true);
   int num_sms = 148;
   if (cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ix->device) != cudaSuccess) {
     cudaGetLastError();
     num_sms = 148;
   }
-  const bool pair = use_pair_kernel();
-  const int32_t G = n_q_pad_of(n_q) / (pair ? 8 : 4);
-  TopkWs w;
-  topk_ws_layout(n_q, ix->dim,
-                 choose_parts_topk(G, index_slots(ix), pair ? num_sms / 2 : num_sms,
-                                   (int64_t)index_slot_rows(ix) * ix->dim * 2, n_q_pad_of(n_q), k), k,
-                 comm ? comm->world : 1, comm != nullptr, w);
-  return w.total;
+  // the largest layout over the query slot sizes (this entry point does not take q_max_len)
+  size_t total = 0;
+  for (int32_t qs = 32; qs <= 128; qs *= 2) {
+    const int32_t nqp = n_q_pad_of(n_q, qs);
+    TopkWs w;
+    topk_ws_layout(n_q, ix->dim, nqp,
+                   choose_parts_topk(nqp * qs / 256, index_slots(ix), num_sms / 2,
+                                     (int64_t)index_slot_rows(ix) * ix->dim * 2, nqp, k),
+                   k, comm ? comm->world : 1, comm != nullptr, w);
+    total = std::max(total, w.total);
+  }
+  return total;
 }
 
 extern "C" hiper_status hiper_workspace_status(const void* workspace, hiper_stream_t stream) {
@@ -1087,7 +1146,7 @@ extern "C" hiper_status hiper_workspace_status(const void* workspace, hiper_stre
 // ============================================================================ pooled limit case (a12)
 // One vector per query and per chunk: S = <NORM(q), NORM(c)> via the K-pipelined pair GEMM with a
 // fused per-query register top-k (kernels/pooled_sm100_pair.cuh).
-constexpr int kPooledKP = 16;  // register top-k slots per query thread (k <= 16 on this path)
+constexpr int kPooledKP = 16;  // register top-k slots per query thread (k <= 16; larger k: warp lists)
 
 struct PooledPlan {
   int32_t n_qtiles = 0, n_ctiles = 0, n_parts = 0, n_stages = 0, q_pad = 0;
@@ -1139,6 +1198,12 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   auto kern = pp.cl == 4 ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 4>
               : pstats_on ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 2, true>
                           : pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
+  if (MODE == 1 && a.k > kPooledKP) {  // warp-cooperative lists in the partial buffer
+    if (pp.cl != 2) return fail(HIPER_ERR_UNSUPPORTED, "pooled k > %d with HIPER_POOLED_MC", kPooledKP);
+    kern = a.k <= 32 ? pooled_sm100_pair_kernel<MODE, 0, 0, 2, false, 1>
+           : a.k <= 64 ? pooled_sm100_pair_kernel<MODE, 0, 0, 2, false, 2>
+                       : pooled_sm100_pair_kernel<MODE, 0, 0, 2, false, 4>;
+  }
   if (MODE == 1 && debug_mode() == 1) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 1, 2, true>;
   if (MODE == 1 && debug_mode() == 2) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 2, 2, true>;
   if (MODE == 1 && debug_mode() == 3) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 3, 2, true>;
@@ -1218,8 +1283,6 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
                                   size_t workspace_bytes, float* out_scores, int64_t* out_ids,
                                   float* dense_scores, cudaStream_t stream,
                                   uint64_t* out_keys = nullptr) {
-  if (!dense_scores && k > kPooledKP)
-    return fail(HIPER_ERR_UNSUPPORTED, "pooled top-k supports k <= %d (got %d)", kPooledKP, k);
   DevInfo di;
   TRY(device_info(di));
   PooledPlan pp;
@@ -1243,7 +1306,7 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   a.n_qtiles = pp.n_qtiles;
   a.n_ctiles = pp.n_ctiles;
   a.n_parts = pp.n_parts;
-  a.num_kb = dim / 64;
+  a.num_kb = num_kb_of(dim);
   a.k = dense_scores ? 1 : k;
   a.n_stages = pp.n_stages;
   a.stage_bytes = pp.stage_bytes;
@@ -1310,7 +1373,7 @@ static hiper_status topk_search(const hiper_index* ix, const void* q_tokens, hip
   if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
   if (k < 1) return fail(HIPER_ERR_INVALID_ARG, "k must be >= 1");
   if (k > kMaxK) return fail(HIPER_ERR_UNSUPPORTED, "k %d > %d", k, kMaxK);
-  const bool pooled = ix->ld_pad == 1;
+  const bool pooled = ix->pooled;
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, pooled));
   if (n_q == 0) return HIPER_OK;
   if (out_keys ? !is_device_ptr(out_keys) : (!out_scores || !out_ids))
@@ -1322,10 +1385,10 @@ static hiper_status topk_search(const hiper_index* ix, const void* q_tokens, hip
   TRY(device_info(di));
   if (di.device != ix->device) return fail(HIPER_ERR_INVALID_ARG, "index lives on device %d, current is %d", ix->device, di.device);
   KernelPlan kp;
-  TRY(plan_kernel(di, n_q, index_slots(ix), index_slot_rows(ix), dim, kp, k));
+  TRY(plan_kernel(di, n_q, q_max_len, index_slots(ix), index_slot_rows(ix), dim, kp, k));
   const int32_t world = comm ? comm->world : 1;
   TopkWs w;
-  topk_ws_layout(n_q, dim, kp.n_parts, k, world, comm != nullptr, w);
+  topk_ws_layout(n_q, dim, kp.n_q_pad, kp.n_parts, k, world, comm != nullptr, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
   uint8_t* ws = (uint8_t*)workspace;
   uint32_t* status = (uint32_t*)(ws + w.status);
@@ -1343,39 +1406,28 @@ static hiper_status topk_search(const hiper_index* ix, const void* q_tokens, hip
 
   if (kp.grid > 0) {
     alignas(64) CUtensorMap tq;
-    TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
-    MaxsimArgs a{};
-    a.n_q = n_q;
-    a.n_groups = kp.n_groups;
-    a.n_parts = kp.n_parts;
-    a.ld_pad = index_slot_rows(ix);
-    a.num_kb = dim / 64;
+    TRY(make_tmap(&tq, qlayout, (int64_t)kp.n_q_pad * kp.qs, dim, 128));
+    MaxsimArgs a = maxsim_args(kp, n_q, index_slots(ix), index_slot_rows(ix), dim, qlens_dev, ix->lens);
     a.k = k;
-    a.n_stages = kp.n_stages;
-    a.a_bytes = kp.a_bytes;
-    a.stage_bytes = kp.stage_bytes;
-    a.n_chunks = index_slots(ix);
     set_packed_args(ix, a);
     a.id_base = ix->id_base;
-    a.q_lens = qlens_dev;
-    a.d_lens = ix->lens;
     a.partial = partial;
-    a.progress = (kp.pair && getenv("HIPER_NO_LOCKSTEP") == nullptr) ? progress : nullptr;
+    a.progress = getenv("HIPER_NO_LOCKSTEP") == nullptr ? progress : nullptr;
     // fewer row groups than pairs (small query batches) put ~pairs/G partitions in flight at once:
     // shrink the window so their lockstep footprint stays ~32 MB of L2 (measured at Q = 64:
     // window 64 vs 192 -> 578 vs 559 q/s)
     a.window = kLockstepWindow;
-    const int slots = kp.pair ? di.num_sms / 2 : di.num_sms;
+    const int slots = di.num_sms / 2;
     if (kp.n_groups < slots) {
       const int64_t slot_bytes = (int64_t)index_slot_rows(ix) * dim * 2;
       const int64_t w = ((int64_t)32 << 20) * kp.n_groups / ((int64_t)slots * slot_bytes);
       a.window = (int32_t)std::max<int64_t>(32, std::min<int64_t>(kLockstepWindow, w));
     }
     if (const char* e = getenv("HIPER_LOCKSTEP_WINDOW")) a.window = std::max(1, atoi(e));  // ablation
-    TRY(launch_maxsim(1, k, kp, tq, kp.pair ? ix->tmap_half : ix->tmap, a, stream));
+    TRY(launch_maxsim(1, k, kp, tq, ix->tmap_half, a, stream));
   }
   // partial lists [P][kEpiGroups][n_q_pad][k]: n_lists = P * kEpiGroups, each [n_q_pad][k]
-  const int64_t q_stride = k, list_stride = (int64_t)n_q_pad_of(n_q) * k;
+  const int64_t q_stride = k, list_stride = (int64_t)kp.n_q_pad * k;
   const int32_t n_lists = kp.grid > 0 ? kp.n_parts * kEpiGroups : 0;
   if (out_keys)
     return launch_merge(partial, n_lists, list_stride, n_q, q_stride, k, out_keys, nullptr, nullptr, stream);
@@ -1423,13 +1475,13 @@ static void scores_ws_layout(int32_t n_q, int32_t dim, ScoresWs& w) {
   w.qlens = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
   w.qlayout = off;
-  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
+  off = align_up(off + q_layout_bytes_max(n_q, dim), 1024);
   w.total = off;
 }
 
 extern "C" size_t hiper_maxsim_scores_workspace_size(const hiper_index* ix, int32_t n_q) {
   if (!ix || n_q < 0) return 0;
-  if (ix->ld_pad == 1) return pooled_ws_size(ix, n_q, 1, nullptr, false);
+  if (ix->pooled) return pooled_ws_size(ix, n_q, 1, nullptr, false);
   ScoresWs w;
   scores_ws_layout(n_q, ix->dim, w);
   return w.total;
@@ -1445,7 +1497,7 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!ix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
   if (dim != ix->dim) return fail(HIPER_ERR_DIM_MISMATCH, "query dim %d != index dim %d", dim, ix->dim);
-  const bool pooled = ix->ld_pad == 1;
+  const bool pooled = ix->pooled;
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, pooled));
   if (n_q == 0 || ix->n == 0) return HIPER_OK;
   if (!out_scores) return fail(HIPER_ERR_INVALID_ARG, "out_scores is NULL");
@@ -1455,7 +1507,7 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
   DevInfo di;
   TRY(device_info(di));
   KernelPlan kp;
-  TRY(plan_kernel(di, n_q, index_slots(ix), index_slot_rows(ix), dim, kp));
+  TRY(plan_kernel(di, n_q, q_max_len, index_slots(ix), index_slot_rows(ix), dim, kp));
   ScoresWs w;
   scores_ws_layout(n_q, dim, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
@@ -1467,25 +1519,13 @@ extern "C" hiper_status hiper_maxsim_scores(const hiper_index* ix, const void* q
   TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags, qlens_dev, qlayout, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
   alignas(64) CUtensorMap tq;
-  TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
-  MaxsimArgs a{};
-  a.n_q = n_q;
-  a.n_groups = kp.n_groups;
-  a.n_parts = kp.n_parts;
-  a.ld_pad = index_slot_rows(ix);
-  a.num_kb = dim / 64;
-  a.k = 1;
-  a.n_stages = kp.n_stages;
-  a.a_bytes = kp.a_bytes;
-  a.stage_bytes = kp.stage_bytes;
-  a.n_chunks = index_slots(ix);
+  TRY(make_tmap(&tq, qlayout, (int64_t)kp.n_q_pad * kp.qs, dim, 128));
+  MaxsimArgs a = maxsim_args(kp, n_q, index_slots(ix), index_slot_rows(ix), dim, qlens_dev, ix->lens);
   a.id_base = ix->id_base;
-  a.q_lens = qlens_dev;
-  a.d_lens = ix->lens;
   a.scores = out_scores;
   a.score_ld = ix->n;
   set_packed_args(ix, a);
-  return launch_maxsim(0, 1, kp, tq, kp.pair ? ix->tmap_half : ix->tmap, a, stream);
+  return launch_maxsim(0, 1, kp, tq, ix->tmap_half, a, stream);
 }
 
 // ============================================================================ ColTrast scores + loss
@@ -1509,7 +1549,7 @@ static void coltrast_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int3
   w.rowloss = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * 8, 1024);
   w.qlayout = off;
-  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * dim * 2, 1024);
+  off = align_up(off + q_layout_bytes_max(n_q, dim), 1024);
   w.dlayout = off;
   off = align_up(off + (size_t)std::max(n_d, 1) * ld_pad * dim * 2, 1024);
   w.scores = off;
@@ -1592,7 +1632,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
   TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
   if (d_max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "d_max_len must be >= 1");
-  if (d_max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "d_max_len %d > 256", d_max_len);
+  if (d_max_len > kMaxChunkLen) return fail(HIPER_ERR_UNSUPPORTED, "d_max_len %d > %d", d_max_len, kMaxChunkLen);
   TRY(check_lens(d_lens, n_d, d_max_len, "doc"));
   if (!d_tokens || !is_device_ptr(d_tokens) || ((uintptr_t)d_tokens & 15))
     return fail(HIPER_ERR_INVALID_ARG, "d_tokens must be 16-B aligned device memory");
@@ -1601,7 +1641,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
   TRY(device_info(di));
   const int32_t ld_pad = (int32_t)round_up(d_max_len, 16);
   KernelPlan kp;
-  TRY(plan_kernel(di, n_q, n_d, ld_pad, dim, kp));
+  TRY(plan_kernel(di, n_q, q_max_len, n_d, ld_pad, dim, kp));
   ColtrastWs w;
   coltrast_ws_layout(n_q, n_d, d_max_len, dim, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
@@ -1615,27 +1655,14 @@ extern "C" hiper_status hiper_coltrast_scores_loss(const void* q_tokens, const i
   float* S = out_scores ? out_scores : (float*)(ws + w.scores);
 
   TRY(stage_small(w, ws, q_lens, n_q, d_lens, n_d, pos_idx, stream));
-  TRY(launch_norm2(q_tokens, n_q, q_max_len, qlens_dev, n_q_pad_of(n_q), kQSlot, qlayout, d_tokens, n_d,
+  TRY(launch_norm2(q_tokens, n_q, q_max_len, qlens_dev, kp.n_q_pad, kp.qs, qlayout, d_tokens, n_d,
                    d_max_len, dlens_dev, n_d, ld_pad, dlayout, dtype, dim, flags, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
 
   alignas(64) CUtensorMap tq, td;
-  TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
-  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, kp.pair ? ld_pad / 2 : ld_pad));
-  MaxsimArgs a{};
-  a.n_q = n_q;
-  a.n_groups = kp.n_groups;
-  a.n_parts = kp.n_parts;
-  a.ld_pad = ld_pad;
-  a.num_kb = dim / 64;
-  a.k = 1;
-  a.n_stages = kp.n_stages;
-  a.a_bytes = kp.a_bytes;
-  a.stage_bytes = kp.stage_bytes;
-  a.n_chunks = n_d;
-  a.id_base = 0;
-  a.q_lens = qlens_dev;
-  a.d_lens = dlens_dev;
+  TRY(make_tmap(&tq, qlayout, (int64_t)kp.n_q_pad * kp.qs, dim, 128));
+  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, (int32_t)kp.box_rows));
+  MaxsimArgs a = maxsim_args(kp, n_q, n_d, ld_pad, dim, qlens_dev, dlens_dev);
   a.scores = S;
   a.score_ld = n_d;
   TRY(launch_maxsim(0, 1, kp, tq, td, a, stream));
@@ -1665,7 +1692,7 @@ static hiper_status pooled_dense_raw(const DevInfo& di, const __nv_bfloat16* qla
   a.n_qtiles = pp.n_qtiles;
   a.n_ctiles = pp.n_ctiles;
   a.n_parts = pp.n_parts;
-  a.num_kb = dim / 64;
+  a.num_kb = num_kb_of(dim);
   a.k = 1;
   a.n_stages = pp.n_stages;
   a.stage_bytes = pp.stage_bytes;
@@ -1829,7 +1856,8 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   TRY(validate_loss_args(n_q, n_d, pos_idx, temperature));
   TRY(validate_queries(q_tokens, dtype, q_lens, n_q, q_max_len, dim, flags));
   if (d_max_len < 1) return fail(HIPER_ERR_INVALID_ARG, "d_max_len must be >= 1");
-  if (d_max_len > 256) return fail(HIPER_ERR_UNSUPPORTED, "d_max_len %d > 256", d_max_len);
+  if (d_max_len > 256 || q_max_len > 32 || (dim != 64 && dim != 128))
+    return fail(HIPER_ERR_UNSUPPORTED, "backward supports q_max_len <= 32, d_max_len <= 256, dim 64 or 128");
   TRY(check_lens(d_lens, n_d, d_max_len, "doc"));
   if (!d_tokens || !is_device_ptr(d_tokens) || ((uintptr_t)d_tokens & 15))
     return fail(HIPER_ERR_INVALID_ARG, "d_tokens must be 16-B aligned device memory");
@@ -1838,8 +1866,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   TRY(device_info(di));
   const int32_t ld_pad = (int32_t)round_up(d_max_len, 16);
   KernelPlan kp;
-  TRY(plan_kernel(di, n_q, n_d, ld_pad, dim, kp));
-  if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "the backward pass needs the CTA-pair kernel");
+  TRY(plan_kernel(di, n_q, q_max_len, n_d, ld_pad, dim, kp));
   if (n_q > 2048) return fail(HIPER_ERR_UNSUPPORTED, "backward supports n_q <= 2048 (got %d)", n_q);
   GradWs w;
   grad_ws_layout(n_q, n_d, d_max_len, dim, w);
@@ -1857,25 +1884,13 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   float* G = (float*)(ws + w.G);
 
   TRY(stage_small(c, ws, q_lens, n_q, d_lens, n_d, pos_idx, stream));
-  TRY(launch_norm2(q_tokens, n_q, q_max_len, qlens_dev, n_q_pad_of(n_q), kQSlot, qlayout, d_tokens, n_d,
+  TRY(launch_norm2(q_tokens, n_q, q_max_len, qlens_dev, kp.n_q_pad, kp.qs, qlayout, d_tokens, n_d,
                    d_max_len, dlens_dev, n_d, ld_pad, dlayout, dtype, dim, flags, status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
   alignas(64) CUtensorMap tq, td;
-  TRY(make_tmap(&tq, qlayout, (int64_t)n_q_pad_of(n_q) * kQSlot, dim, 128));
-  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, ld_pad / 2));
-  MaxsimArgs a{};
-  a.n_q = n_q;
-  a.n_groups = kp.n_groups;
-  a.n_parts = kp.n_parts;
-  a.ld_pad = ld_pad;
-  a.num_kb = dim / 64;
-  a.k = 1;
-  a.n_stages = kp.n_stages;
-  a.a_bytes = kp.a_bytes;
-  a.stage_bytes = kp.stage_bytes;
-  a.n_chunks = n_d;
-  a.q_lens = qlens_dev;
-  a.d_lens = dlens_dev;
+  TRY(make_tmap(&tq, qlayout, (int64_t)kp.n_q_pad * kp.qs, dim, 128));
+  TRY(make_tmap(&td, dlayout, (int64_t)n_d * ld_pad, dim, (int32_t)kp.box_rows));
+  MaxsimArgs a = maxsim_args(kp, n_q, n_d, ld_pad, dim, qlens_dev, dlens_dev);
   a.scores = S;
   a.score_ld = n_d;
   a.amax = amax;
@@ -1926,16 +1941,17 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
 
 // ============================================================================ N3: two-stage retrieval
 // Stage 1: pooled cosine top-K1 (the paper's deployed retrieval) on a pooled
-// index; stage 2: exact MaxSim re-scoring of those K1 candidates on the token index of the same
-// chunks (ColBERTv2's pattern; SPEC.md:268-276 rerank), final top-k.  The stage-2
-// kernel is the CTA-pair MaxSim kernel reading candidate chunks by id (TMA coordinates), 8 queries
-// per pair scoring the union of their candidates.
+// index; stage 2: exact MaxSim re-scoring of each query's own K1 candidates on the token index of the
+// same chunks (ColBERTv2's pattern; SPEC.md:268-276 rerank), final top-k.  Stage 2 is
+// the gather kernel of kernels/rerank_gather.cuh: Q * K1 (query, candidate) pairs, each computed
+// once, HBM-bound on the candidates' rows.
 struct TwoStageWs {
   size_t pooled = 0, pooled_bytes = 0, s1_scores = 0, s1_ids = 0, slots = 0, status = 0, qlens = 0,
          qlayout = 0, S2 = 0, local = 0, gathered = 0, total = 0;
 };
+static constexpr int32_t kRerankMaxDim = 128, kRerankMaxQueryLen = 32;
 static void two_stage_ws_layout(const hiper_index* pix, const hiper_index* tix, int32_t n_q,
-                                int32_t k1, const hiper_comm* comm, TwoStageWs& w) {
+                                int32_t k1, int32_t k, const hiper_comm* comm, TwoStageWs& w) {
   size_t off = 0;
   w.pooled = off;
   w.pooled_bytes = pooled_ws_size(pix, n_q, k1, comm, true);
@@ -1945,19 +1961,19 @@ static void two_stage_ws_layout(const hiper_index* pix, const hiper_index* tix, 
   w.s1_ids = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 8, 256);
   w.slots = off;
-  off = align_up(off + (size_t)n_q_pad_of(n_q) * k1 * 4, 256);
+  off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 4, 256);
   w.status = off;
   off += 256;
   w.qlens = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * 4, 1024);
   w.qlayout = off;
-  off = align_up(off + (size_t)n_q_pad_of(n_q) * kQSlot * tix->dim * 2, 1024);
+  off = align_up(off + (size_t)n_q_pad_of(n_q) * 32 * tix->dim * 2, 1024);
   w.S2 = off;
-  off = align_up(off + (size_t)n_q_pad_of(n_q) * 8 * k1 * 4, 1024);
+  off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 4, 1024);
   w.local = off;  // multi-rank: this rank's re-scored top-k keys, then every rank's
-  if (comm) off = align_up(off + (size_t)std::max(n_q, 1) * k1 * 8, 256);
+  if (comm) off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
   w.gathered = off;
-  if (comm) off = align_up(off + (size_t)comm->world * std::max(n_q, 1) * k1 * 8, 256);
+  if (comm) off = align_up(off + (size_t)comm->world * std::max(n_q, 1) * k * 8, 256);
   w.total = off;
 }
 
@@ -1966,8 +1982,19 @@ extern "C" size_t hiper_two_stage_workspace_size(const hiper_index* pooled_idx,
                                                  int32_t k1, const hiper_comm* comm) {
   if (!pooled_idx || !token_idx || n_q < 0 || k1 < 1) return 0;
   TwoStageWs w;
-  two_stage_ws_layout(pooled_idx, token_idx, n_q, k1, comm, w);
+  two_stage_ws_layout(pooled_idx, token_idx, n_q, k1, k1, comm, w);  // k <= k1
   return w.total;
+}
+
+template <int KR>
+static hiper_status launch_rerank_select(const float* S2, const int32_t* slots, int32_t k1, int32_t n_q,
+                                         int64_t id_base, int32_t k, float* out_scores,
+                                         int64_t* out_ids, uint64_t* out_keys, cudaStream_t stream) {
+  rerank_select_kernel<KR><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, slots, k1, n_q, id_base, k, out_scores,
+                                                             out_ids, out_keys);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return HIPER_OK;
 }
 
 extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper_index* tix,
@@ -1981,13 +2008,15 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   HiperRange nv("hiper_two_stage_topk");
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!pix || !tix) return fail(HIPER_ERR_INVALID_ARG, "index is NULL");
-  if (pix->ld_pad != 1) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (max_len 1)");
-  if (tix->ld_pad == 1) return fail(HIPER_ERR_INVALID_ARG, "stage-2 index must hold token rows");
-  if (pix->packed) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (not HIPER_PACKED)");
+  if (!pix->pooled) return fail(HIPER_ERR_INVALID_ARG, "stage-1 index must be pooled (HIPER_POOLED)");
+  if (tix->pooled) return fail(HIPER_ERR_INVALID_ARG, "stage-2 index must hold token rows");
   if (pix->n != tix->n || pix->id_base != tix->id_base)
     return fail(HIPER_ERR_INVALID_ARG, "the two indexes must cover the same chunks (n, id_base)");
   if (k1 < 1 || k < 1 || k > k1) return fail(HIPER_ERR_INVALID_ARG, "need 1 <= k <= k1");
-  if (k1 > kPooledKP) return fail(HIPER_ERR_UNSUPPORTED, "k1 %d > %d", k1, kPooledKP);
+  if (k1 > kMaxK) return fail(HIPER_ERR_UNSUPPORTED, "k1 %d > %d", k1, kMaxK);
+  if (tix->dim > kRerankMaxDim || q_max_len > kRerankMaxQueryLen || tix->max_len > 256)
+    return fail(HIPER_ERR_UNSUPPORTED, "rerank supports token dim <= %d, q_max_len <= %d, max_len <= 256",
+                kRerankMaxDim, kRerankMaxQueryLen);
   {
     std::vector<int32_t> ones(std::max(n_q, 0), 1);
     TRY(validate_queries(q_pooled, dtype, ones.data(), n_q, 1, pix->dim, flags, true));
@@ -1998,7 +2027,7 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   DevInfo di;
   TRY(device_info(di));
   TwoStageWs w;
-  two_stage_ws_layout(pix, tix, n_q, k1, comm, w);
+  two_stage_ws_layout(pix, tix, n_q, k1, k, comm, w);
   TRY(check_ws(workspace, workspace_bytes, w.total));
   const bool multi = comm != nullptr && comm->world > 1;
   uint8_t* ws = (uint8_t*)workspace;
@@ -2006,74 +2035,65 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   int64_t* s1i = (int64_t*)(ws + w.s1_ids);
   int32_t* slots = (int32_t*)(ws + w.slots);
   // stage 1: pooled top-k1 (pooled queries have one row each; lengths all 1)
-  std::vector<int32_t> ones(n_q, 1);
   // (with comm: the GLOBAL pooled top-k1, identical on every rank)
+  std::vector<int32_t> ones(n_q, 1);
   TRY(pooled_search(pix, q_pooled, dtype, ones.data(), n_q, pix->dim, k1, flags, comm,
                     ws + w.pooled, w.pooled_bytes, s1s, s1i, nullptr, stream));
   int32_t launches = g_launches;
-  // stage 2: slots, token query prep, MaxSim over each row group's candidate union
-  const int32_t nqp = n_q_pad_of(n_q);
-  ids_to_slots_kernel<<<(unsigned)(((int64_t)nqp * k1 + 255) / 256), 256, 0, stream>>>(
-      s1i, n_q, nqp, k1, pix->id_base, pix->n, slots);
+  g_launches = 0;
+  // stage 2: this shard's slots, token query prep, the gather-MaxSim of every (query, own candidate)
+  const int64_t n_items = (int64_t)n_q * k1;
+  ids_to_slots_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, stream>>>(s1i, n_items, pix->id_base,
+                                                                            pix->n, slots);
   CUDA_TRY(cudaGetLastError());
+  ++g_launches;
   uint32_t* status = (uint32_t*)(ws + w.status);
   int32_t* qlens_dev = (int32_t*)(ws + w.qlens);
   __nv_bfloat16* qlayout = (__nv_bfloat16*)(ws + w.qlayout);
   float* S2 = (float*)(ws + w.S2);
-  g_launches = 0;
   CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
   TRY(prep_queries(q_tokens, dtype, q_lens, n_q, q_max_len, tix->dim, flags, qlens_dev, qlayout,
                    status, stream));
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
-  KernelPlan kp;
-  const int32_t n_slots = 8 * k1;
-  // a packed token index (N4) is read chunk by chunk through its row table: the kernel loads a
-  // 256-row window from the chunk's first packed row and the epilogue reads only its len real
-  // columns (the rows after them belong to other chunks and are never part of a max)
-  const int32_t ldp = tix->packed ? kTileRows : tix->ld_pad;
-  TRY(plan_kernel(di, n_q, n_slots, ldp, tix->dim, kp));
-  if (!kp.pair) return fail(HIPER_ERR_UNSUPPORTED, "rerank needs the CTA-pair kernel");
-  kp.n_parts = 1;  // a unit = one row group and its own candidate list
-  kp.grid = (int)std::min<int64_t>(kp.n_groups, di.num_sms / 2) * 2;
-  alignas(64) CUtensorMap tq;
-  TRY(make_tmap(&tq, qlayout, (int64_t)nqp * kQSlot, tix->dim, 128));
-  MaxsimArgs a{};
-  a.n_q = n_q;
-  a.n_groups = kp.n_groups;
-  a.n_parts = 1;
-  a.ld_pad = ldp;
-  a.row_of = tix->packed ? tix->row_of : nullptr;
-  a.num_kb = tix->dim / 64;
-  a.k = 1;
-  a.n_stages = kp.n_stages;
-  a.a_bytes = kp.a_bytes;
-  a.stage_bytes = kp.stage_bytes;
-  a.n_chunks = n_slots;
-  a.id_base = tix->id_base;
-  a.q_lens = qlens_dev;
-  a.d_lens = tix->lens;
-  a.scores = S2;
-  a.score_ld = n_slots;
-  a.cand = slots;
-  // an empty shard has no tensor map and no candidates (every slot is -1, so rerank_select never
-  // reads S2): skip the scoring launch, but still take part in the all-gather below
-  if (tix->n > 0) TRY(launch_maxsim(0, 1, kp, tq, tix->tmap_half, a, stream));
-  if (!multi) {
-    rerank_select_kernel<1><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, n_slots, slots, k1, n_q,
-                                                                tix->id_base, k, out_scores, out_ids);
+  // an empty shard has no token rows and no candidates (every slot is -1): skip the gather, but
+  // still take part in the all-gather below
+  if (tix->n > 0) {
+    alignas(64) CUtensorMap t64;  // the token index as 64-row x 64-dim boxes (only real rows fetched)
+    TRY(make_tmap(&t64, tix->tok, tix->packed ? tix->n_rows : tix->n * (int64_t)tix->ld_pad, tix->dim, 64));
+    RerankArgs ra{};
+    ra.qlay = qlayout;
+    ra.q_lens = qlens_dev;
+    ra.slots = slots;
+    ra.d_lens = tix->lens;
+    ra.row_of = tix->packed ? tix->row_of : nullptr;
+    ra.ld_pad = tix->ld_pad;
+    ra.dim = tix->dim;
+    ra.k1 = k1;
+    ra.n_items = n_items;
+    ra.S2 = S2;
+    auto kern = num_kb_of(tix->dim) == 1 ? rerank_gather_kernel<1, 6> : rerank_gather_kernel<2, 3>;
+    const int smem = 1024 + kRerankWarps * (num_kb_of(tix->dim) == 1 ? 6 : 3) * 64 * 128 * num_kb_of(tix->dim) + 256;
+    CUDA_TRY(set_max_smem((const void*)kern, smem));
+    const int64_t want = (n_items + 3) / 4;  // at least ~4 items per warp
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(di.num_sms, want / kRerankWarps));
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    bool rec = false;
+    TRY(profile_begin(stream, &ev, &rec));
+    kern<<<grid, kRerankWarps * 32, smem, stream>>>(t64, ra);
     CUDA_TRY(cudaGetLastError());
-    g_launches += launches + 2;
-    return HIPER_OK;
+    TRY(profile_end(stream, ev, rec));
+    ++g_launches;
   }
-  // multi-rank: this rank's re-scored candidates -> top-k keys; all-gather; the same merge on every
-  // rank (keys are unique and every candidate is scored by its owner: bitwise the 1-GPU answer)
-  uint64_t* local = (uint64_t*)(ws + w.local);
-  uint64_t* gathered = (uint64_t*)(ws + w.gathered);
-  rerank_select_kernel<1><<<(n_q + 7) / 8, 256, 0, stream>>>(S2, n_slots, slots, k1, n_q,
-                                                              tix->id_base, k, nullptr, nullptr, local);
-  CUDA_TRY(cudaGetLastError());
-  TRY(gather_merge(comm, local, gathered, n_q, k, out_scores, out_ids, stream));
-  g_launches += launches + 2;  // + stage 1, ids_to_slots, rerank_select
+  uint64_t* local = multi ? (uint64_t*)(ws + w.local) : nullptr;
+  float* os = multi ? nullptr : out_scores;
+  int64_t* oi = multi ? nullptr : out_ids;
+  if (k <= 32) TRY(launch_rerank_select<1>(S2, slots, k1, n_q, tix->id_base, k, os, oi, local, stream));
+  else if (k <= 64) TRY(launch_rerank_select<2>(S2, slots, k1, n_q, tix->id_base, k, os, oi, local, stream));
+  else TRY(launch_rerank_select<4>(S2, slots, k1, n_q, tix->id_base, k, os, oi, local, stream));
+  // multi-rank: every rank re-scored the candidates it owns; one all-gather of the re-scored top-k
+  // keys and the same merge on every rank (keys are unique: bitwise the 1-GPU answer)
+  if (multi) TRY(gather_merge(comm, local, (uint64_t*)(ws + w.gathered), n_q, k, out_scores, out_ids, stream));
+  g_launches += launches;
   return HIPER_OK;
 }
 

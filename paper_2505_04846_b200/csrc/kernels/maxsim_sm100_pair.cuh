@@ -54,28 +54,19 @@ __device__ __forceinline__ void lockstep_wait(const uint32_t* progress, uint32_t
   }
 }
 
-// Chunk scored in slot c of row group g: the corpus itself, or (rerank, N3) a per-group candidate list.
-// BY_ID: the instantiation can see a candidate table / row table (MODE 0 only: the rerank of N3);
-// the top-k and argmax instantiations compile these look-ups out.
-template <bool BY_ID>
-__device__ __forceinline__ int64_t slot_chunk(const MaxsimArgs& a, int32_t g, int64_t c) {
-  if (!BY_ID || a.cand == nullptr) return c;
-  const int32_t id = __ldg(a.cand + (int64_t)g * a.n_chunks + c);
-  return id < 0 ? 0 : id;
-}
-template <bool BY_ID>
-__device__ __forceinline__ bool slot_valid(const MaxsimArgs& a, int32_t g, int64_t c) {
-  return !BY_ID || a.cand == nullptr || __ldg(a.cand + (int64_t)g * a.n_chunks + c) >= 0;
-}
-
-// PACKED (N4): the slots are the tiles of a length-bucketed packed corpus (MaxsimArgs::tiles/ents):
-// the MMA N is the tile's n_rows, and the epilogue reduces each chunk over its own column segment.
+// PACKED (N4): the slots are the tiles of a length-bucketed packed corpus (MaxsimArgs::recs): the MMA
+// N is the tile's n_rows, and the epilogue reduces each chunk over its own column segment.
 // STATS: HIPER_PIPE_STATS instrumentation compiled in (diagnostics builds only; the production
 // instantiation carries none of it -- the kernel's hot loops are instruction-cache sensitive).
-template <int MODE, int KR, int DBG = 0, bool PACKED = false, bool STATS = false>
+// QW: warps (32 token rows each) per query: 1 (q_max_len <= 32), 2 (<= 64), 4 (<= 128).
+// H: MMA halves per chunk: 1 (ld_pad <= 256), 2 (256 < ld_pad <= 512; half h = rows [256h, ...)).
+template <int MODE, int KR, int DBG = 0, bool PACKED = false, bool STATS = false, int QW = 1, int H = 1>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     maxsim_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_d, const MaxsimArgs args) {
+  static_assert(QW == 1 || QW == 2 || QW == 4, "QW");
+  static_assert(H == 1 || (H == 2 && !PACKED), "two-half chunks are dense-layout only");
+  static_assert(MODE != 2 || (QW == 1 && H == 1), "argmax capture: q_max_len <= 32, ld_pad <= 256");
   extern __shared__ uint8_t smem_raw[];
   using namespace ptx;
   const uint32_t warp = warp_id();
@@ -85,19 +76,21 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   const uint32_t n_pairs = nclusters_x();
 
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t sA = base;                   // 2 x a_bytes (this CTA's 128 query rows)
-  const uint32_t sB = sA + 2 * args.a_bytes;  // n_stages x stage_bytes (this CTA's half chunk)
+  const uint32_t sA = base;                            // a_bufs x a_bytes (this CTA's 128 query rows)
+  const uint32_t sB = sA + args.a_bufs * args.a_bytes;  // n_stages x stage_bytes
   const uint32_t sBar = sB + args.n_stages * args.stage_bytes;
   const int S = args.n_stages;
   auto bar_full = [&](int s) { return sBar + 8u * s; };
   auto bar_empty = [&](int s) { return sBar + 8u * (S + s); };
   auto bar_afull = [&](int b) { return sBar + 8u * (2 * S + b); };
   auto bar_aempty = [&](int b) { return sBar + 8u * (2 * S + 2 + b); };
-  auto bar_tfull = [&](int b) { return sBar + 8u * (2 * S + 4 + b); };
-  auto bar_tempty = [&](int b) { return sBar + 8u * (2 * S + 6 + b); };
-  const uint32_t sTmemPtr = sBar + 8u * (2 * S + 8);
+  auto bar_tempty = [&](int b) { return sBar + 8u * (2 * S + 4 + b); };
+  auto bar_tfull = [&](int b) { return sBar + 8u * (2 * S + 6 + b); };  // [acc + 2 * group] (H = 2)
+  const uint32_t sTmemPtr = sBar + 8u * (2 * S + 10);
   const uint32_t sMeta = sTmemPtr + 16u;  // [S] u32: MMA N per stage (packed corpus)
   const uint32_t sRing = sBar + 512u;     // [2][32] x {w0, row0}: producer's tile batches (packed)
+  // [2 groups][2 buffers][4 warps][16] fp32: per-warp partial sums of a query that spans QW warps
+  float* xsum = reinterpret_cast<float*>(smem_raw + (sBar + 1024u - smem_u32(smem_raw)));
   uint32_t* tmem_ptr_generic =
       reinterpret_cast<uint32_t*>(smem_raw + (sTmemPtr - smem_u32(smem_raw)));
 
@@ -109,9 +102,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_afull(b), 1);
       mbar_init(bar_aempty(b), 1);
-      mbar_init(bar_tfull(b), 1);
-      mbar_init(bar_tempty(b), 8);  // 4 warps of the owning epilogue group in each of the 2 CTAs
+      mbar_init(bar_tempty(b), 8);  // 4 warps of the draining epilogue group in each of the 2 CTAs
     }
+    for (int b = 0; b < 4; ++b) mbar_init(bar_tfull(b), 1);
     fence_mbarrier_init();
   }
   if (warp == kPairAllocWarp) {
@@ -126,10 +119,17 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   // layouts, lengths) are read only after this point.
   grid_dependency_wait();
 
-  const int32_t n_units = args.n_groups * args.n_parts;  // n_groups = row-group pairs (8 queries)
+  const int32_t n_units = args.n_groups * args.n_parts;
   long long st_drain_g = 0, st_ewait_g = 0, st_tiles_g = 0;  // HIPER_PIPE_STATS (epilogue warps)
-  const int32_t half_rows = args.ld_pad >> 1;
-  const uint32_t half_tile = (uint32_t)half_rows * 128u;  // one 64-dim K-block of this CTA's half chunk
+  const uint32_t kb_bytes = args.box_rows * 128u;  // one 64-dim K-block of this CTA's rows
+  // MMA N and this CTA's first row of half h of a dense chunk
+  auto half_n = [&](int h) -> uint32_t {
+    return H == 1 ? (uint32_t)args.ld_pad : (h == 0 ? 256u : (uint32_t)args.ld_pad - 256u);
+  };
+  auto a_slot = [&](uint32_t it, uint32_t& ab, uint32_t& aph) {
+    ab = args.a_bufs == 2 ? (it & 1u) : 0u;
+    aph = args.a_bufs == 2 ? ((it >> 1) & 1u) : (it & 1u);
+  };
 
   if (warp == kPairProducerWarp) {
     // ================= TMA producer (both CTAs) =================
@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       int64_t c0, c1;
       unit_decode(args, u, g, p, c0, c1);
       if (lane == 0) {
-        const uint32_t ab = it & 1u, aph = (it >> 1) & 1u;
+        uint32_t ab, aph;
+        a_slot(it, ab, aph);
         mbar_wait(bar_aempty(ab), aph ^ 1u);
         if (rank == 0) mbar_arrive_expect_tx(bar_afull(ab), 2u * args.a_bytes);
         const uint32_t afull_leader = mapa_shared(bar_afull(ab), 0);
@@ -180,9 +181,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           nrows = ld_shared_u32(e) & 0xFFFFu;
           brow = (int32_t)ld_shared_u32(e + 4u) + (int32_t)rank * (int32_t)(nrows >> 1);
         } else {
-          const int64_t ch = slot_chunk<MODE == 0>(args, g, c);
-          const int64_t r0 = (MODE == 0 && args.row_of != nullptr) ? __ldg(args.row_of + ch) : ch * args.ld_pad;
-          brow = (int32_t)(r0 + (int64_t)rank * half_rows);
+          brow = (int32_t)(c * args.ld_pad + (int64_t)rank * (half_n(0) >> 1));
         }
         if (lane == 0) {
           if (args.progress != nullptr && rank == 0 && ((c - c0) & 15) == 0) {
@@ -190,21 +189,27 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             lockstep_publish(args.progress, pair, pos);
             lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
           }
-          // one stage = this CTA's half of one whole chunk (all dim/64 K-blocks)
-          mbar_wait(bar_empty(s), ph ^ 1u);
-          if constexpr (PACKED) st_shared_u32(sMeta + 4u * s, nrows);  // MMA N of this stage
-          if ((DBG == 2 || DBG == 3 || DBG == 4) && (c > c0 || it > 0)) {
-            if (rank == 0) mbar_arrive(bar_full(s));
-          } else {
-            if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
-            const uint32_t full_leader = mapa_shared(bar_full(s), 0);
-            for (int kb = 0; kb < args.num_kb; ++kb)
-              tma_load_2d_pair(sB + s * args.stage_bytes + kb * half_tile, &tmap_d, full_leader,
-                               kb * 64, brow);
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            // one stage = this CTA's rows of one whole chunk (half), all K-blocks
+            mbar_wait(bar_empty(s), ph ^ 1u);
+            if constexpr (PACKED) st_shared_u32(sMeta + 4u * s, nrows);  // MMA N of this stage
+            if ((DBG == 2 || DBG == 3 || DBG == 4) && (c > c0 || it > 0)) {
+              if (rank == 0) mbar_arrive(bar_full(s));
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(bar_full(s), 2u * args.stage_bytes);
+              const uint32_t full_leader = mapa_shared(bar_full(s), 0);
+              // half 1 starts at row 256 of the chunk; this CTA takes the second half of its N rows
+              const int32_t row = H == 1 ? brow
+                                         : (int32_t)(c * args.ld_pad + h * 256 + (int64_t)rank * (half_n(h) >> 1));
+              for (int kb = 0; kb < args.num_kb; ++kb)
+                tma_load_2d_pair(sB + s * args.stage_bytes + kb * kb_bytes, &tmap_d, full_leader,
+                                 kb * 64, row);
+            }
+            if (++s == S) { s = 0; ph ^= 1u; }
           }
         }
         __syncwarp();
-        if (++s == S) { s = 0; ph ^= 1u; }
       }
       streamed += (uint32_t)(c1 - c0);
     }
@@ -213,48 +218,54 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     // ================= MMA issuer: leader CTA, single thread =================
     // (highest warp id: the SMSP arbiter favours it over the epilogue warps sharing its SMSP)
     if (rank == 0 && lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(256, (uint32_t)args.ld_pad);
+      const uint32_t idesc = idesc_bf16_f32(256, half_n(0));
       int s = 0;
-      uint32_t ph = 0, it = 0, t = 0;
+      uint32_t ph = 0, it = 0, t = 0;  // t: accumulator turns (chunk halves) so far
       long long st_acc = 0, st_full = 0;
       const long long st_t0 = clock64();
       for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs, ++it) {
         int32_t g, p;
         int64_t c0, c1;
         unit_decode(args, u, g, p, c0, c1);
-        const uint32_t ab = it & 1u, aph = (it >> 1) & 1u;
+        uint32_t ab, aph;
+        a_slot(it, ab, aph);
         mbar_wait(bar_afull(ab), aph);
         tc_fence_after();
         const uint32_t a_tile = sA + ab * args.a_bytes;
-        for (int64_t c = c0; c < c1; ++c, ++t) {
-          const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
-          long long w0 = (STATS && args.stats) ? clock64() : 0;
-          mbar_wait(bar_tempty(acc), tph ^ 1u);
-          if (STATS && args.stats) {
-            st_acc += clock64() - w0;
-            w0 = clock64();
-          }
-          tc_fence_after();
-          const uint32_t d_tmem = tmem_base + acc * kAccStride;
-          mbar_wait(bar_full(s), ph);
-          if (STATS && args.stats) st_full += clock64() - w0;
-          tc_fence_after();
-          uint32_t idesc_c = idesc;
-          if constexpr (PACKED)  // MMA N = this tile's packed rows (written by the producer)
-            idesc_c = idesc_bf16_f32(256, ld_shared_u32(sMeta + 4u * s));
-          const uint32_t b_st = sB + s * args.stage_bytes;
-          for (int rep = 0; rep < (DBG == 4 ? 2 : 1); ++rep)  // DBG 4: each chunk's K loop twice
-          for (int kb = 0; kb < args.num_kb; ++kb) {
-            const uint32_t a_kb = a_tile + kb * 16384u;
-            const uint32_t b_kb = b_st + kb * half_tile;
+        for (int64_t c = c0; c < c1; ++c) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_kb + kk * 32),
-                               umma_desc_sw128(b_kb + kk * 32), idesc_c, (rep | kb | kk) != 0 ? 1u : 0u);
+          for (int h = 0; h < H; ++h, ++t) {
+            const uint32_t acc = t & 1u, tph = (t >> 1) & 1u;
+            long long w0 = (STATS && args.stats) ? clock64() : 0;
+            mbar_wait(bar_tempty(acc), tph ^ 1u);
+            if (STATS && args.stats) {
+              st_acc += clock64() - w0;
+              w0 = clock64();
+            }
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * kAccStride;
+            mbar_wait(bar_full(s), ph);
+            if (STATS && args.stats) st_full += clock64() - w0;
+            tc_fence_after();
+            uint32_t idesc_c = idesc;
+            if constexpr (PACKED)  // MMA N = this tile's packed rows (written by the producer)
+              idesc_c = idesc_bf16_f32(256, ld_shared_u32(sMeta + 4u * s));
+            if constexpr (H == 2) idesc_c = idesc_bf16_f32(256, half_n(h));
+            const uint32_t b_st = sB + s * args.stage_bytes;
+            for (int rep = 0; rep < (DBG == 4 ? 2 : 1); ++rep)  // DBG 4: each chunk's K loop twice
+            for (int kb = 0; kb < args.num_kb; ++kb) {
+              const uint32_t a_kb = a_tile + kb * 16384u;
+              const uint32_t b_kb = b_st + kb * kb_bytes;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16_ss_pair(d_tmem, umma_desc_sw128(a_kb + kk * 32),
+                                 umma_desc_sw128(b_kb + kk * 32), idesc_c, (rep | kb | kk) != 0 ? 1u : 0u);
+            }
+            mma_commit_pair_mc(bar_empty(s), 0x3);  // both CTAs' stage s free again
+            if (++s == S) { s = 0; ph ^= 1u; }
+            // both CTAs' accumulator rows ready; H = 2: the barrier of (half, draining group)
+            mma_commit_pair_mc(bar_tfull(H == 1 ? acc : acc + 2u * ((t >> 1) & 1u)), 0x3);
           }
-          mma_commit_pair_mc(bar_empty(s), 0x3);  // both CTAs' stage s free again
-          if (++s == S) { s = 0; ph ^= 1u; }
-          mma_commit_pair_mc(bar_tfull(acc), 0x3);  // both CTAs' accumulator rows ready
         }
         mma_commit_pair_mc(bar_aempty(ab), 0x3);
       }
@@ -266,18 +277,39 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     }
   } else if (warp < 8) {
     // ================= epilogue (both CTAs, each on its own 128 TMEM lanes) =================
-    // warp w reads TMEM lanes 32*(w%4)..+31 (the hardware's lane-quarter rule).
+    // warp w reads TMEM lanes 32*(w%4)..+31 (the hardware's lane-quarter rule).  Group e drains the
+    // chunks of parity e; with H = 2 it drains both halves of its chunk (accumulators 0 and 1).
     const uint32_t qslot = warp & 3u;
     const uint32_t grp = warp >> 2;
-    const uint32_t taddr_base = tmem_base + ((qslot * 32u) << 16) + grp * kAccStride;
+    const uint32_t qc = qslot / QW, part = qslot % QW;  // query within this CTA, its 32-row part
+    const uint32_t lanes = tmem_base + ((qslot * 32u) << 16);
+    const uint32_t taddr_base = lanes + grp * kAccStride;
     const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), 0);
     uint32_t t = 0, mine = 0;
+    // a query spanning QW warps: its warps' sums meet in shared memory (double-buffered by chunk)
+    auto combine = [&](float v, bool write, uint32_t idx) -> float {
+      if constexpr (QW == 1) {
+        return v;
+      } else {
+        float* xs = xsum + (grp * 2u + (mine & 1u)) * 64u;
+        if (write) xs[qslot * 16u + idx] = v;
+        named_bar_sync(1u + grp * 4u + qc, 32u * QW);
+        if (part == 0 && write) {
+          float tsum = xs[qc * QW * 16u + idx];
+#pragma unroll
+          for (int w = 1; w < QW; ++w) tsum += xs[(qc * QW + w) * 16u + idx];
+          v = tsum;
+        }
+        return v;
+      }
+    };
     for (int32_t u = (int32_t)pair; u < n_units; u += (int32_t)n_pairs) {
       int32_t g, p;
       int64_t c0, c1;
       unit_decode(args, u, g, p, c0, c1);
-      const int32_t q = g * 8 + (int32_t)rank * 4 + (int32_t)qslot;
+      const int32_t q = g * (8 / QW) + (int32_t)rank * (4 / QW) + (int32_t)qc;
       const int32_t lq = q < args.n_q ? __ldg(args.q_lens + q) : 0;
+      const bool tok_real = (int32_t)(part * 32u + lane) < lq;
       WarpTopK<KR> topk;
       topk.init();
       const int64_t first = c0 + (int64_t)((grp - (t & 1u)) & 1u);
@@ -336,8 +368,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           // Pass 2: suffix max inside each chunk -> m16[first group of a chunk] = the chunk maximum
           // (start bits are set for every group >= n_grp, so unused groups never merge into a chunk)
 #pragma unroll
-          for (int g = 14; g >= 0; --g)
-            m16[g] = ((gstart >> (g + 1)) & 1u) ? m16[g] : fmaxf(m16[g], m16[g + 1]);
+          for (int gi = 14; gi >= 0; --gi)
+            m16[gi] = ((gstart >> (gi + 1)) & 1u) ? m16[gi] : fmaxf(m16[gi], m16[gi + 1]);
           // Pass 3: the masked sum over query tokens of all 16 groups at once, by a transposed
           // butterfly (a reduce-scatter by shuffles): each round halves the groups a lane carries, and
           // lane l ends with the sum of group l >> 1.  Every group's sum is built from exactly the
@@ -346,7 +378,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           // branch-guarded butterflies (the kernel's hot loops are instruction-cache sensitive).
           float x[16];
 #pragma unroll
-          for (int g = 0; g < 16; ++g) x[g] = ((int32_t)lane < lq) ? m16[g] : 0.0f;
+          for (int gi = 0; gi < 16; ++gi) x[gi] = tok_real ? m16[gi] : 0.0f;
 #pragma unroll
           for (int w = 8; w >= 1; w >>= 1) {  // keep w groups; partner = lane ^ 2w
             const bool hi = (lane & (2u * (uint32_t)w)) != 0u;
@@ -358,7 +390,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             }
           }
           float sv = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
+          sv = combine(sv, (lane & 1u) == 0u, lane >> 1);  // a query of QW warps: add its warps' sums
           sv += 0.0f;  // canonical +0
+          if (part != 0) continue;
           // lane pair (2g, 2g + 1) holds group g; its even lane speaks for it when a chunk starts there
           // (start bits are also set past n_rows, so mask them to the groups in use)
           const uint32_t starts = gstart & (n_grp >= 16 ? 0xFFFFu : ((1u << n_grp) - 1u));
@@ -383,66 +417,69 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           }
         }
       } else {
-      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + slot_chunk<MODE == 0>(args, g, first)) : 0;
+      int32_t ld_next = (first < c1) ? __ldg(args.d_lens + first) : 0;
       for (int64_t c = first; c < c1; c += 2, ++mine) {
         const int32_t ld = ld_next;
-        if (c + 2 < c1) ld_next = __ldg(args.d_lens + slot_chunk<MODE == 0>(args, g, c + 2));
-        long long e0 = (STATS && args.stats) ? clock64() : 0;
-        mbar_wait(bar_tfull(grp), mine & 1u);
-        long long e1 = (STATS && args.stats) ? clock64() : 0;
-        if (STATS && args.stats) st_ewait_g += e1 - e0;
-        tc_fence_after();
+        if (c + 2 < c1) ld_next = __ldg(args.d_lens + c + 2);
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         int ix4[4] = {0, 0, 0, 0};
-        for (int32_t col = 0; col < ((DBG == 1 || DBG == 2 || DBG == 4) ? 0 : ld); col += 64) {
-          uint32_t v[64];
-          tmem_ld64_wait(taddr_base + (uint32_t)col, v);
-          const int rem = ld - col;
-          if constexpr (MODE == 2) {
-            max64_arg1(v, m4[0], ix4[0], col, rem);  // chains 1..3 stay at -inf
-          } else {
-            if (rem >= 64) max64(v, m4);
-            else max64_masked(v, m4, rem);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          long long e0 = (STATS && args.stats) ? clock64() : 0;
+          mbar_wait(bar_tfull(H == 1 ? grp : (uint32_t)h + 2u * grp), mine & 1u);
+          long long e1 = (STATS && args.stats) ? clock64() : 0;
+          if (STATS && args.stats) st_ewait_g += e1 - e0;
+          tc_fence_after();
+          // real columns of this half (H = 1: the chunk's length)
+          const int32_t lh = H == 1 ? ld : min(max(ld - 256 * h, 0), 256);
+          const uint32_t taddr = H == 1 ? taddr_base : lanes + (uint32_t)h * kAccStride;
+          for (int32_t col = 0; col < ((DBG == 1 || DBG == 2 || DBG == 4) ? 0 : lh); col += 64) {
+            uint32_t v[64];
+            tmem_ld64_wait(taddr + (uint32_t)col, v);
+            const int rem = lh - col;
+            if constexpr (MODE == 2) {
+              max64_arg1(v, m4[0], ix4[0], col, rem);  // chains 1..3 stay at -inf
+            } else {
+              if (rem >= 64) max64(v, m4);
+              else max64_masked(v, m4, rem);
+            }
           }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_leader);
-        if (STATS && args.stats) {
-          st_drain_g += clock64() - e1;
-          ++st_tiles_g;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(H == 1 ? tempty_leader : mapa_shared(bar_tempty(h), 0));
+          if (STATS && args.stats) {
+            st_drain_g += clock64() - e1;
+            ++st_tiles_g;
+          }
         }
         const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         if constexpr (MODE == 2) {
-          // argmax = lowest column index among the chains holding the max (reading: lowest u on ties)
-          int best = 0x7FFFFFFF;
-#pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4)
-            if (m4[c4] == m && ix4[c4] < best) best = ix4[c4];
           if (q < args.n_q)
-            args.amax[((int64_t)q * args.score_ld + c) * 32 + lane] = (uint8_t)best;
+            args.amax[((int64_t)q * args.score_ld + c) * 32 + lane] = (uint8_t)ix4[0];
         }
-        float sv = ((int32_t)lane < lq) ? m : 0.0f;
+        float sv = tok_real ? m : 0.0f;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        sv = combine(sv, lane == 0u, 0u);  // a query of QW warps: add its warps' sums in warp order
         sv += 0.0f;  // canonical +0
+        if (part != 0) continue;
         if constexpr (MODE == 0 || MODE == 2) {
-          if (lane == 0 && q < args.n_q)
-            args.scores[(int64_t)q * args.score_ld + c] = slot_valid<MODE == 0>(args, g, c) ? sv : -INFINITY;
+          if (lane == 0 && q < args.n_q) args.scores[(int64_t)q * args.score_ld + c] = sv;
         } else {
-          const uint64_t key = make_key(sv, args.id_base + c);
+          // (QW > 1: only lane 0 holds the combined sum)
+          const uint64_t key = make_key(QW == 1 ? sv : __shfl_sync(0xffffffffu, sv, 0), args.id_base + c);
           if (key > topk.thresh) topk.insert(key, args.k, lane);
         }
       }
       }  // !PACKED
       if constexpr (MODE == 1) {
-        // partial lists: [P][kEpiGroups][8G][k]
-        uint64_t* dst = args.partial +
-                        (((int64_t)p * kEpiGroups + grp) * args.n_groups * 8 + q) * args.k;
+        if (part == 0) {  // partial lists: [P][kEpiGroups][q_pad][k]
+          uint64_t* dst = args.partial + (((int64_t)p * kEpiGroups + grp) * args.q_pad + q) * args.k;
 #pragma unroll
-        for (int r = 0; r < KR; ++r) {
-          const int i = r * 32 + (int)lane;
-          if (i < args.k) dst[i] = topk.v[r];
+          for (int r = 0; r < KR; ++r) {
+            const int i = r * 32 + (int)lane;
+            if (i < args.k) dst[i] = topk.v[r];
+          }
         }
       }
     }

@@ -62,7 +62,13 @@ __device__ __forceinline__ float pooled_thr_score(uint64_t thr) {
 // needed by CTA r of both pairs is loaded once, half by each of them, and TMA-multicast to both, so
 // the chunk operand costs half the L2 reads.  tmap_c then has a 64-row box.
 // STATS: HIPER_PIPE_STATS instrumentation compiled in (diagnostics only; see the MaxSim pair kernel).
-template <int MODE, int KP, int DBG = 0, int CL = 2, bool STATS = false>
+// KP > 0: each epilogue thread keeps its query's list in KP registers (k <= KP, the fast path).
+// KP == 0 (16 < k <= 128): each (unit, query) list lives in its final place in `partial` (L2-resident,
+// zeroed at the unit's start); the rare hits are inserted by the whole warp, one hit lane at a time:
+// the warp loads that lane's list (KRG = ceil(k / 32) keys per lane, coalesced), inserts every hit
+// of the lane with the warp-cooperative sorted insert of WarpTopK, stores it back, and hands the new
+// k-th key back to the lane as its filter threshold.
+template <int MODE, int KP, int DBG = 0, int CL = 2, bool STATS = false, int KRG = 1>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     pooled_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_c, const PooledArgs args) {
@@ -216,9 +222,15 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       int32_t qt, p, t0, t1;
       decode(u, qt, p, t0, t1);
       const int32_t q = qt * 256 + (int32_t)rank * 128 + (int32_t)qslot * 32 + (int32_t)lane;
-      uint64_t v[KP];
+      uint64_t v[KP > 0 ? KP : 1];
 #pragma unroll
-      for (int m = 0; m < KP; ++m) v[m] = 0ull;
+      for (int m = 0; m < (KP > 0 ? KP : 1); ++m) v[m] = 0ull;
+      // KP == 0: this warp's 32 lists ([32][k] keys, consecutive queries) start empty
+      uint64_t* wlists = args.partial + (((int64_t)p * kEpiGroups + grp) * args.q_pad + (q - (int32_t)lane)) * k;
+      if constexpr (MODE == 1 && KP == 0) {
+        for (int32_t i = (int32_t)lane; i < 32 * k; i += 32) wlists[i] = 0ull;
+        __syncwarp();
+      }
       uint64_t thr = 0ull;        // key of rank k-1 (0 while the list is not full)
       uint64_t gth = 0ull, pub = 0ull;  // shared bound seen / own thr last published
       if (args.gthr != nullptr && q < args.q_pad)
@@ -271,7 +283,54 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               for (int j = 0; j < 64; ++j)
                 hits |= (uint64_t)(__uint_as_float(r[j]) >= thr_f && j < nj) << j;
             }
-            if (hits) {
+            if constexpr (KP == 0) {
+              // warp-cooperative insertion into the lists of the lanes that have hits
+              if (__ballot_sync(0xffffffffu, hits != 0ull) != 0u) {
+                float xs[64];
+#pragma unroll
+                for (int j = 0; j < 64; ++j) xs[j] = __uint_as_float(r[j]) + 0.0f;
+                uint32_t hl = __ballot_sync(0xffffffffu, hits != 0ull);
+                while (hl) {
+                  const int src = __ffs(hl) - 1;
+                  hl &= hl - 1u;
+                  uint64_t hm = __shfl_sync(0xffffffffu, (unsigned long long)hits, src);
+                  const uint64_t g_src = __shfl_sync(0xffffffffu, (unsigned long long)gth, src);
+                  uint64_t* L = wlists + (int64_t)src * k;
+                  WarpTopK<KRG> top;
+#pragma unroll
+                  for (int rr = 0; rr < KRG; ++rr) {
+                    const int i = rr * 32 + (int)lane;
+                    top.v[rr] = i < k ? L[i] : 0ull;
+                  }
+                  uint64_t tv = 0ull;
+#pragma unroll
+                  for (int rr = 0; rr < KRG; ++rr)
+                    if (rr == ((k - 1) >> 5)) tv = top.v[rr];
+                  top.thresh = __shfl_sync(0xffffffffu, (unsigned long long)tv, (k - 1) & 31);
+                  while (hm) {
+                    const int j = __ffsll((long long)hm) - 1;
+                    hm &= hm - 1;
+                    const float sc = __shfl_sync(0xffffffffu, xs[j], src);
+                    const uint64_t key = make_key(sc, args.id_base + cbase + col + j);
+                    if (key > top.thresh && key > g_src) {
+                      if (STATS && args.stats && lane == (uint32_t)src) ++st_ins;
+                      top.insert(key, k, lane);
+                    }
+                  }
+#pragma unroll
+                  for (int rr = 0; rr < KRG; ++rr) {
+                    const int i = rr * 32 + (int)lane;
+                    if (i < k) L[i] = top.v[rr];
+                  }
+                  if (lane == (uint32_t)src) {
+                    thr = top.thresh;
+                    lim = thr > gth ? thr : gth;
+                    thr_f = pooled_thr_score(lim);
+                  }
+                }
+                __syncwarp();
+              }
+            } else if (hits) {
               float xs[64];  // rare path: a local copy so the hits can be indexed dynamically
 #pragma unroll
               for (int j = 0; j < 64; ++j) xs[j] = __uint_as_float(r[j]) + 0.0f;
@@ -324,7 +383,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           }
         }
       }
-      if constexpr (MODE == 1) {
+      if constexpr (MODE == 1 && KP > 0) {
         if (q < args.n_q) {
           uint64_t* dst = args.partial + (((int64_t)p * kEpiGroups + grp) * args.q_pad + q) * k;
 #pragma unroll

@@ -74,11 +74,11 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(const uint64_t* __restr
   }
 }
 
-// NEXT N3, stage-2 selection: query q (row group g = q / 8, slot block r = q % 8) owns slots
-// [r*K1, r*K1 + K1) of its group's candidate list; its re-scored candidates are merged into an exact
-// top-k (score desc, id asc).  One warp per query, K1 <= 32.
+// NEXT N3, stage-2 selection: query q's re-scored candidates S[q][0..K1) (slot s valid iff
+// cand[q][s] >= 0) -> its exact top-k (score desc, id asc), decoded and/or as keys.  One warp per
+// query, K1 <= 128 (32 candidates per round).
 template <int KR>
-__global__ void __launch_bounds__(256) rerank_select_kernel(const float* __restrict__ S, int64_t slots,
+__global__ void __launch_bounds__(256) rerank_select_kernel(const float* __restrict__ S,
                                                             const int32_t* __restrict__ cand,
                                                             int32_t K1, int32_t n_q, int64_t id_base,
                                                             int32_t k, float* __restrict__ out_scores,
@@ -87,20 +87,22 @@ __global__ void __launch_bounds__(256) rerank_select_kernel(const float* __restr
   const uint32_t lane = threadIdx.x & 31;
   const int32_t q = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (q >= n_q) return;
-  const int64_t g = q / 8, s0 = (int64_t)(q % 8) * K1;
-  uint64_t cand_key = 0ull;
-  if ((int32_t)lane < K1) {
-    const int32_t c = cand[g * slots + s0 + lane];
-    if (c >= 0) cand_key = make_key(S[(int64_t)q * slots + s0 + lane] + 0.0f, id_base + c);
-  }
   WarpTopK<KR> top;
   top.init();
-  uint32_t mask = __ballot_sync(0xffffffffu, cand_key > 0ull);
-  while (mask) {
-    const int src = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const uint64_t key = __shfl_sync(0xffffffffu, cand_key, src);
-    if (key > top.thresh) top.insert(key, k, lane);
+  for (int32_t s0 = 0; s0 < K1; s0 += 32) {
+    const int32_t s = s0 + (int32_t)lane;
+    uint64_t cand_key = 0ull;
+    if (s < K1) {
+      const int32_t c = cand[(int64_t)q * K1 + s];
+      if (c >= 0) cand_key = make_key(S[(int64_t)q * K1 + s] + 0.0f, id_base + c);
+    }
+    uint32_t mask = __ballot_sync(0xffffffffu, cand_key > top.thresh);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint64_t key = __shfl_sync(0xffffffffu, cand_key, src);
+      if (key > top.thresh) top.insert(key, k, lane);
+    }
   }
 #pragma unroll
   for (int r = 0; r < KR; ++r) {
@@ -114,15 +116,13 @@ __global__ void __launch_bounds__(256) rerank_select_kernel(const float* __restr
   }
 }
 
-// Stage-1 ids (int64 global, -1 = none) -> stage-2 slot table [n_q_pad][K1] of local chunk indices;
-// ids outside this shard [id_base, id_base + n) (re-scored by the rank that owns them) -> -1.
-__global__ void ids_to_slots_kernel(const int64_t* __restrict__ ids, int32_t n_q, int32_t n_q_pad,
-                                    int32_t K1, int64_t id_base, int64_t n,
-                                    int32_t* __restrict__ slots) {
+// Stage-1 ids (int64 global, -1 = none) [n_q][K1] -> stage-2 slot table [n_q][K1] of local chunk
+// indices; ids outside this shard [id_base, id_base + n) (re-scored by the rank that owns them) -> -1.
+__global__ void ids_to_slots_kernel(const int64_t* __restrict__ ids, int64_t n_items, int64_t id_base,
+                                    int64_t n, int32_t* __restrict__ slots) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)n_q_pad * K1) return;
-  const int64_t q = e / K1;
-  const int64_t id = q < n_q ? ids[e] : -1;
+  if (e >= n_items) return;
+  const int64_t id = ids[e];
   slots[e] = (id >= id_base && id < id_base + n) ? (int32_t)(id - id_base) : -1;
 }
 

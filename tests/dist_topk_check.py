@@ -91,7 +91,7 @@ def main():
             del full, fidx
         del shard, idx
     # ---- NEXT N3 across ranks: global pooled top-k1, owner re-scoring, one more all-gather
-    Ct, Lt, dp, k1, k = 4003, 128, 768, 16, 10
+    Ct, Lt, dp, k1, k = 4003, 128, 768, 100, 10
     tl_all = gen.lengths(81, Ct, Lt, True)
     c0, c1 = rank * Ct // world, (rank + 1) * Ct // world
     to_dev16 = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda().view(torch.bfloat16)
@@ -99,7 +99,7 @@ def main():
     ql2 = gen.lengths(83, 21, Lq, True, stream=gen.QLEN)
     qp2 = gen.queries(83, 21, 1, dp, corpus_seed=82, n_chunks=Ct, L=1, sigma_q=np.float32(8.0))
     pidx = H.hiper_index_build(to_dev16(gen.corpus(82, c0, c1 - c0, 1, dp)), np.ones(c1 - c0, np.int32),
-                               id_base=c0)
+                               id_base=c0, flags=H.HIPER_POOLED)
     tidx = H.hiper_index_build(to_dev16(gen.corpus(81, c0, c1 - c0, Lt, d)), tl_all[c0:c1], id_base=c0)
     s2, i2 = H.hiper_two_stage_topk(pidx, tidx, to_dev16(qp2), to_dev16(qt2), ql2, k1, k, comm=comm)
     torch.cuda.synchronize()
@@ -108,7 +108,8 @@ def main():
     dist.all_gather(gs, s2)
     dist.all_gather(gi, i2)
     if rank == 0:
-        fp = H.hiper_index_build(to_dev16(gen.corpus(82, 0, Ct, 1, dp)), np.ones(Ct, np.int32))
+        fp = H.hiper_index_build(to_dev16(gen.corpus(82, 0, Ct, 1, dp)), np.ones(Ct, np.int32),
+                                flags=H.HIPER_POOLED)
         ft = H.hiper_index_build(to_dev16(gen.corpus(81, 0, Ct, Lt, d)), tl_all)
         fs, fi = H.hiper_two_stage_topk(fp, ft, to_dev16(qp2), to_dev16(qt2), ql2, k1, k)
         for r in range(world):

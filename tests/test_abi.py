@@ -35,7 +35,15 @@ def test_library_is_sm100a_only():
                           capture_output=True, text=True).stdout
     for mnem in ("UTCHMMA", "UTMALDG", "LDTM"):   # tcgen05.mma, TMA, tcgen05.ld
         assert mnem in sass, mnem
-    assert "HMMA" not in sass.replace("UTCHMMA", "")
+    # legacy warp-level HMMA only in the N3 stage-2 gather kernel (HBM-bound on the gathered candidate
+    # rows: DESIGN.md §7.4); every dense contraction (MaxSim, pooled GEMM) is tcgen05 (UTCHMMA)
+    funcs = re.split(r"\n\s+Function : ", sass)[1:]
+    with_hmma = [f.split("\n", 1)[0] for f in funcs if "HMMA" in f.replace("UTCHMMA", "")]
+    assert with_hmma and all("rerank_gather_kernel" in f for f in with_hmma), with_hmma
+    for f in funcs:
+        name = f.split("\n", 1)[0]
+        if "maxsim_sm100_pair_kernel" in name or "pooled_sm100_pair_kernel" in name:
+            assert "UTCHMMA" in f, name
 
 
 def test_status_strings():
@@ -53,8 +61,10 @@ def test_host_validation_before_device():
     lens = np.ones(4, np.int32)
     P = lens.ctypes.data_as(ctypes.c_void_p)
     assert L.hiper_index_build(None, 0, P, -1, 8, 128, 0, 0, None, ctypes.byref(out)) == 1
-    assert L.hiper_index_build(None, 0, P, 4, 8, 96, 0, 0, None, ctypes.byref(out)) == 12
-    assert L.hiper_index_build(None, 0, P, 4, 300, 128, 0, 0, None, ctypes.byref(out)) == 12
+    assert L.hiper_index_build(None, 0, P, 4, 8, 72, 0, 0, None, ctypes.byref(out)) == 12   # dim % 16
+    assert L.hiper_index_build(None, 0, P, 4, 8, 272, 0, 0, None, ctypes.byref(out)) == 12  # dim > 256
+    assert L.hiper_index_build(None, 0, P, 4, 600, 128, 0, 0, None, ctypes.byref(out)) == 12  # > 512
+    assert L.hiper_index_build(None, 0, P, 4, 8, 128, 0, 32, None, ctypes.byref(out)) == 1  # POOLED, len 8
     assert L.hiper_index_build(None, 0, P, 4, 8, 128, 0, 1 << 7, None, ctypes.byref(out)) == 1
     zero = np.array([1, 0, 1, 1], np.int32)
     assert L.hiper_index_build(None, 0, zero.ctypes.data_as(ctypes.c_void_p), 4, 8, 128, 0, 0,

@@ -42,7 +42,7 @@ def case(C, Q, kind="planted", dtype="bf16", seed=11, qseed=12):
 @pytest.mark.parametrize("C,Q,dtype", [(1000, 8, "f32"), (777, 300, "bf16"), (256, 256, "bf16")])
 def test_pooled_dense_scores(H, C, Q, dtype):
     corp, q = case(C, Q, kind="iid", dtype=dtype)
-    idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32))
+    idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32), flags=H.HIPER_POOLED)
     assert idx.ld_pad == 1
     lay = bits(idx.layout().clone())
     assert np.array_equal(lay[:, 0], oracle.norm_rows(corp[:, 0]))     # layout bitwise (a1)
@@ -53,11 +53,13 @@ def test_pooled_dense_scores(H, C, Q, dtype):
     assert np.all(np.abs(S) <= 1 + 2.0 ** -6)
 
 
-@pytest.mark.parametrize("k,kind", [(10, "planted"), (16, "iid"), (1, "iid")])
+@pytest.mark.parametrize("k,kind", [(10, "planted"), (16, "iid"), (1, "iid"), (17, "iid"),
+                                    (100, "planted"), (128, "iid")])
 def test_pooled_topk(H, k, kind):
     C, Q = 5000, 300
     corp, q = case(C, Q, kind=kind)
-    idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32), id_base=77)
+    idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32), id_base=77,
+                              flags=H.HIPER_POOLED)
     s, i = H.hiper_maxsim_topk(idx, to_dev(q), np.ones(Q, np.int32), k)
     s, i = s.cpu().numpy(), i.cpu().numpy()
     lay = bits(idx.layout().clone())
@@ -72,11 +74,13 @@ def test_pooled_topk(H, k, kind):
 
 def test_pooled_edge_cases(H):
     corp, q = case(3, 5)
-    idx = H.hiper_index_build(to_dev(corp), np.ones(3, np.int32))
+    idx = H.hiper_index_build(to_dev(corp), np.ones(3, np.int32), flags=H.HIPER_POOLED)
     s, i = H.hiper_maxsim_topk(idx, to_dev(q), np.ones(5, np.int32), 6)
     assert (i.cpu().numpy()[:, 3:] == -1).all()
+    s, i = H.hiper_maxsim_topk(idx, to_dev(q), np.ones(5, np.int32), 40)   # warp-list path, k > n
+    assert (i.cpu().numpy()[:, 3:] == -1).all() and (i.cpu().numpy()[:, :3] >= 0).all()
     with pytest.raises(H.HiperError) as e:
-        H.hiper_maxsim_topk(idx, to_dev(q), np.ones(5, np.int32), 17)
+        H.hiper_maxsim_topk(idx, to_dev(q), np.ones(5, np.int32), 129)
     assert e.value.name == "HIPER_ERR_UNSUPPORTED"
     qq = np.zeros((5, 2, D), np.uint16)
     with pytest.raises(H.HiperError) as e:
@@ -90,7 +94,7 @@ def test_config5_full_size(H):
     C, Q, k = 3_600_000, 4096, 10
     corpus = torch.empty((C, 1, D), dtype=torch.bfloat16, device="cuda")
     device.corpus_(corpus, 21, 0)
-    idx = H.hiper_index_build(corpus, np.ones(C, np.int32), flags=H.HIPER_BORROW_TOKENS)
+    idx = H.hiper_index_build(corpus, np.ones(C, np.int32), flags=H.HIPER_BORROW_TOKENS | H.HIPER_POOLED)
     q = torch.empty((Q, 1, D), dtype=torch.bfloat16, device="cuda")
     device.queries_(q, 22, corpus_seed=21, n_chunks=C, L=1)
     s, i = H.hiper_maxsim_topk(idx, q, np.ones(Q, np.int32), k)

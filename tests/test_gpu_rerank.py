@@ -22,7 +22,8 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda().view(torch.bfloat16)
 
 
-@pytest.mark.parametrize("C,n_q,k1,k", [(3000, 37, 16, 10), (500, 8, 8, 8), (20, 5, 16, 3)])
+@pytest.mark.parametrize("C,n_q,k1,k", [(3000, 37, 16, 10), (500, 8, 8, 8), (20, 5, 16, 3),
+                                        (3000, 37, 100, 10), (1500, 9, 128, 100)])
 def test_two_stage_matches_oracle(H, C, n_q, k1, k):
     L, Lq, d, dp = 128, 32, 128, 768
     tok = gen.corpus(81, 0, C, L, d)
@@ -32,7 +33,8 @@ def test_two_stage_matches_oracle(H, C, n_q, k1, k):
     ql = gen.lengths(83, n_q, Lq, True, stream=gen.QLEN)
     qp = gen.queries(83, n_q, 1, dp, corpus_seed=82, n_chunks=C, L=1, sigma_q=np.float32(8.0))
     base = 1000
-    pidx = H.hiper_index_build(to_dev(pooled), np.ones(C, np.int32), id_base=base)
+    pidx = H.hiper_index_build(to_dev(pooled), np.ones(C, np.int32), id_base=base,
+                               flags=H.HIPER_POOLED)
     tidx = H.hiper_index_build(to_dev(tok), tl, id_base=base)
     s, i = H.hiper_two_stage_topk(pidx, tidx, to_dev(qp), to_dev(qt), ql, k1, k)
     s, i = s.cpu().numpy(), i.cpu().numpy()
@@ -74,7 +76,7 @@ def test_two_stage_packed_token_index_bitwise(H):
     qt = gen.queries(93, n_q, Lq, d, corpus_seed=91, n_chunks=C, L=L, chunk_lens_fn=lambda c: tl[c])
     ql = gen.lengths(93, n_q, Lq, True, stream=gen.QLEN)
     qp = gen.queries(93, n_q, 1, dp, corpus_seed=92, n_chunks=C, L=1, sigma_q=np.float32(8.0))
-    pidx = H.hiper_index_build(to_dev(pooled), np.ones(C, np.int32), id_base=7)
+    pidx = H.hiper_index_build(to_dev(pooled), np.ones(C, np.int32), id_base=7, flags=H.HIPER_POOLED)
     dense = H.hiper_index_build(to_dev(tok), tl, id_base=7)
     packed = H.hiper_index_build(to_dev(tok), tl, id_base=7, flags=H.HIPER_PACKED)
     assert packed.packed

@@ -107,7 +107,7 @@ def test_token_shards_merge_vs_oracle(H, packed, W, k, empty):
         assert_topk_ok(s[r], i[r], S_o[r], ids, k, qlen[r], d, f"W={W} k={k} query {r}")
 
 
-@pytest.mark.parametrize("W,k", [(2, 10), (4, 16)])
+@pytest.mark.parametrize("W,k", [(2, 10), (4, 16), (3, 100)])
 def test_pooled_shards_merge_vs_oracle(H, W, k):
     C, Q, dp = 3001, 21, 768
     corp = gen.corpus(31, 0, C, 1, dp)
@@ -116,7 +116,7 @@ def test_pooled_shards_merge_vs_oracle(H, W, k):
     qd = to_dev(q)
 
     def make_index(a, b):
-        return H.hiper_index_build(to_dev(corp[a:b]), ones_c[a:b], id_base=a)
+        return H.hiper_index_build(to_dev(corp[a:b]), ones_c[a:b], id_base=a, flags=H.HIPER_POOLED)
 
     full = make_index(0, C)
     s_ref, i_ref = [t.cpu().numpy() for t in H.hiper_maxsim_topk(full, qd, ones_q, k)]
