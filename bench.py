@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["config3", "config4", "config5", "config2", "config3v",
-                                           "config4v"],
+                                           "config4v", "two_stage"],
                     default="config3",
                     help="config3 (default, N=1 headline): 1M x 256-token chunks, Q=1024, top-10; "
                          "config4: 3.6M chunks, top-100 (N>=2); config5: pooled 3.6M x 768, "
@@ -52,6 +52,9 @@ def parse():
                     help="config3v: every chunk at full length (isolates the packed machinery)")
     ap.add_argument("--no-pack", action="store_true",
                     help="config3v: dense padded layout instead of HIPER_PACKED (the N4 ablation)")
+    ap.add_argument("--k1", type=int, default=100,
+                    help="two_stage: pooled candidates per query (SPEC.md:286 default 100)")
+    ap.add_argument("--pooled-dim", type=int, default=768)
     ap.add_argument("--chunks", type=int, default=None)
     ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
@@ -76,13 +79,16 @@ def parse():
         # config4 on semantic-chunk lengths: generated straight into each shard's packed layout
         # (HIPER_PACKED | HIPER_BORROW_TOKENS); --chunks 16400000 is the paper's SLC corpus size
         "config4v": dict(chunks=3_600_000, queries=1024, k=100, chunk_len=256, query_len=32, dim=128),
+        # NEXT N3: pooled top-k1 (config-5 kernel) -> exact MaxSim rerank to top-k on the 3.6M
+        # semantic-length corpus (token index packed in place, as config4v)
+        "two_stage": dict(chunks=3_600_000, queries=1024, k=10, chunk_len=256, query_len=32, dim=128),
     }[a.workload]
     for key, v in defaults.items():
         if getattr(a, key) is None:
             setattr(a, key, v)
-    a.semantic = a.workload in ("config3v", "config4v")
+    a.semantic = a.workload in ("config3v", "config4v", "two_stage")
     a.packed = a.semantic and not a.no_pack
-    a.gen_packed = a.workload == "config4v"
+    a.gen_packed = a.workload in ("config4v", "two_stage")
     a.mean_len = a.chunk_len
     if a.semantic:
         from synth import gen
@@ -606,6 +612,201 @@ def run_coltrast(a, rank, local_rank, world):
         dist.destroy_process_group()
 
 
+def two_stage_oracle_sample(a, lens_all, seconds=10.0):
+    """The CPU oracle's own two stages on a bounded sample: stage 1 (pooled cosine top-k1) over C_s
+    chunks for n_s queries, scaled linearly to the whole corpus; stage 2 (MaxSim of each query
+    against its k1 candidates) measured in full for those queries."""
+    import numpy as np
+
+    import oracle
+    from synth import gen
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    n_s = 2
+    qp = gen.queries(a.qseed, n_s, 1, a.pooled_dim, corpus_seed=a.seed + 1000, n_chunks=a.chunks, L=1)
+    qt = gen.queries(a.qseed, n_s, a.query_len, a.dim, corpus_seed=a.seed, n_chunks=a.chunks,
+                     L=a.chunk_len, chunk_lens_fn=lambda c: lens_all[c])
+    ql = np.full(n_s, a.query_len, np.int32)
+    C_s = 20_000
+    pc = gen.corpus(a.seed + 1000, 0, C_s, 1, a.pooled_dim)
+    t0 = time.perf_counter()
+    pn = oracle.norm_rows(pc)
+    Sp = oracle.maxsim_matrix(oracle.norm_rows(qp), np.ones(n_s, np.int32), pn, np.ones(C_s, np.int32),
+                              n_threads=cores)
+    cands = [oracle.topk(Sp[r], np.arange(C_s, dtype=np.int64), a.k1)[1] for r in range(n_s)]
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    qn = oracle.norm_rows(qt)
+    for r in range(n_s):
+        raw = gen.f32_to_bf16_bits(gen.corpus_tokens_f32(a.seed, cands[r], a.chunk_len, a.dim))
+        S2 = np.array([oracle.maxsim(qn[r], oracle.norm_rows(raw[j, :lens_all[c]]))
+                       for j, c in enumerate(cands[r].tolist())])
+        oracle.topk(S2, cands[r], a.k)
+    t2 = time.perf_counter() - t0
+    per_q = (t1 * a.chunks / C_s + t2) / n_s
+    return {"value": 1.0 / per_q, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"{n_s} queries: stage 1 over {C_s} of {a.chunks} pooled chunks ({t1:.1f} s, "
+                       f"scaled linearly), stage 2 over their {a.k1} candidates each ({t2:.1f} s); "
+                       f"float64 C oracle, OpenMP")}
+
+
+def run_two_stage(a, rank, local_rank, world):
+    """--workload two_stage (NEXT N3): pooled top-k1 over the 3.6M-chunk pooled index, then exact
+    MaxSim rerank of each query's k1 candidates on the same chunks' packed token index."""
+    import numpy as np
+    import torch
+
+    import paper_2505_04846_b200 as H
+    from synth import device, gen
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    H.lib()
+    c0, c1 = rank * a.chunks // world, (rank + 1) * a.chunks // world
+    n_local = c1 - c0
+    lens_all = gen.semantic_lengths(a.seed, a.chunks, a.chunk_len)
+    lens = lens_all[c0:c1].copy()
+    pseed = a.seed + 1000  # the pooled corpus: its own synthetic embeddings of the same chunk ids
+    torch.cuda.synchronize()
+    t_build = time.perf_counter()
+    dst, n_rows = H.hiper_pack_dst_rows(lens)
+    tok = torch.empty((max(n_rows, 1), a.dim), dtype=torch.bfloat16, device="cuda")
+    device.corpus_packed_(tok, a.seed, c0, torch.from_numpy(dst).cuda(), torch.from_numpy(lens).cuda(),
+                          a.chunk_len)
+    tidx = H.hiper_index_build(tok, lens, id_base=c0, flags=H.HIPER_PACKED | H.HIPER_BORROW_TOKENS)
+    pool = torch.empty((n_local, 1, a.pooled_dim), dtype=torch.bfloat16, device="cuda")
+    device.corpus_(pool, pseed, c0)
+    pidx = H.hiper_index_build(pool, np.ones(n_local, np.int32), id_base=c0,
+                               flags=H.HIPER_POOLED | H.HIPER_BORROW_TOKENS)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build
+    comm = H.Comm() if world > 1 else None
+    qt = torch.empty((a.queries, a.query_len, a.dim), dtype=torch.bfloat16, device="cuda")
+    device.queries_(qt, a.qseed, corpus_seed=a.seed, n_chunks=a.chunks, L=a.chunk_len,
+                    chunk_lens=torch.from_numpy(lens_all).cuda())
+    qp = torch.empty((a.queries, 1, a.pooled_dim), dtype=torch.bfloat16, device="cuda")
+    device.queries_(qp, a.qseed, corpus_seed=pseed, n_chunks=a.chunks, L=1)
+    qlen = np.full(a.queries, a.query_len, np.int32)
+    stream = torch.cuda.current_stream()
+
+    def step(qp_=qp, qt_=qt):
+        return H.hiper_two_stage_topk(pidx, tidx, qp_, qt_, qlen, a.k1, a.k, comm=comm, stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(a.warmup, 3)):
+        out = step()
+    launches = H.last_launch_count()
+    steps = max(a.steps, 10)
+    clocks = ClockSampler(list(range(world))) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    barrier()
+    H.hiper_profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        out = step()
+    e1.record(stream)
+    barrier()
+    H.hiper_profile_enable(False)
+    p_ms, p_n = H.hiper_profile_read(H.HIPER_PROF_POOLED)
+    r_ms, r_n = H.hiper_profile_read(H.HIPER_PROF_RERANK)
+    H.hiper_profile_read()
+    clk = clocks.stop() if clocks else None
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    p_avg = max_over_ranks(p_ms / max(p_n, 1))
+    r_avg = max_over_ranks(r_ms / max(r_n, 1))
+    value = a.queries * steps / (ms / 1e3)
+    tgt = gen.query_targets(a.qseed, a.queries, a.chunks, False)
+    top1 = float((out[1][:, 0].cpu().numpy() == tgt).mean())
+    # stage-2 algorithmic bytes: the real token rows of this rank's candidates (+ query rows, scores)
+    s1, i1 = H.hiper_maxsim_topk(pidx, qp, np.ones(a.queries, np.int32), a.k1, comm=comm)
+    ids = i1.cpu().numpy().ravel()
+    mine = ids[(ids >= c0) & (ids < c1)] - c0
+    cand_bytes = float(lens[mine].astype(np.int64).sum()) * a.dim * 2
+    r_bytes = cand_bytes + a.queries * 32 * a.dim * 2 + a.queries * a.k1 * 4
+    # e2e: host queries in, host results out, every step
+    qt_h, qp_h = qt.cpu().pin_memory(), qp.cpu().pin_memory()
+    qt_d, qp_d = torch.empty_like(qt), torch.empty_like(qp)
+    s_h = torch.empty((a.queries, a.k), dtype=torch.float32).pin_memory()
+    i_h = torch.empty((a.queries, a.k), dtype=torch.int64).pin_memory()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(steps):
+        qt_d.copy_(qt_h, non_blocking=True)
+        qp_d.copy_(qp_h, non_blocking=True)
+        o = step(qp_d, qt_d)
+        s_h.copy_(o[0], non_blocking=True)
+        i_h.copy_(o[1], non_blocking=True)
+    f1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(f0.elapsed_time(f1))
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    peak, peak_src = load_peaks(ms / 1e3, clk)
+    pflops = 2.0 * a.pooled_dim * a.queries * n_local
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm = json.load(open(mp)).get("hbm_gbs") if os.path.exists(mp) else None
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)" if hbm else "B200_PROFILING.md fallback"
+    hbm = float(hbm or 7000.0)
+    stage1 = {"bound": "tensor", "achieved": pflops / (p_avg / 1e3) / 1e12, "peak": peak,
+              "unit": "TFLOP/s", "frac": pflops / (p_avg / 1e3) / 1e12 / peak, "traffic": None,
+              "kernel": "pooled_sm100_pair_kernel (stage 1: pooled GEMM + per-query top-k1)",
+              "kernel_ms_per_launch": p_avg, "algorithmic_flops_per_launch": pflops,
+              "peak_source": peak_src, "kernel_share_of_step": p_avg / (ms / steps)}
+    stage2 = {"bound": "hbm", "achieved": r_bytes / (r_avg / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+              "frac": r_bytes / (r_avg / 1e3) / 1e9 / hbm, "traffic": None,
+              "kernel": "rerank_gather_kernel (stage 2: gather of each query's k1 candidates' token rows + exact MaxSim)",
+              "kernel_ms_per_launch": r_avg, "algorithmic_bytes_per_launch": r_bytes,
+              "peak_source": hbm_src, "kernel_share_of_step": r_avg / (ms / steps)}
+    dominant = stage1 if p_avg >= r_avg else stage2
+    line = {
+        "metric": f"queries/s (two-stage: pooled top-{a.k1} -> exact MaxSim rerank top-{a.k}, "
+                  f"{a.chunks // 1000}K chunks)",
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": a.warmup,
+        "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": (f"two_stage (NEXT N3): {a.chunks} chunks, pooled dim {a.pooled_dim} "
+                                f"+ token rows (semantic lengths <= {a.chunk_len}, packed) dim {a.dim}, "
+                                f"query batch {a.queries} x {a.query_len} tokens, k1 {a.k1}, top-{a.k}"),
+                   "parallelism": f"corpus-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (5.5 GB pooled + ~90 GB token rows)"},
+        "roofline": dominant, "roofline_stages": [stage1, stage2],
+        "e2e": {"value": a.queries * steps / (ms_e2e / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": (qt_h.numel() + qp_h.numel()) * 2 * world,
+                "d2h_bytes_per_step": (s_h.numel() * 4 + i_h.numel() * 8) * world},
+        "gpu_launches": launches * steps, "clocks": clk,
+        "extra": {"top1_is_planted_target": top1, "launches_per_step": launches,
+                  "index_build_s_rank0": build_s, "stage2_candidate_bytes": cand_bytes},
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = two_stage_oracle_sample(a, lens_all)
+    emit(line)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     global _RESULT_FD
     # NCCL / CUDA libraries may write to fd 1; keep the real stdout for the result line only.
@@ -621,6 +822,9 @@ def main():
             return
         if a.workload == "config2":
             run_coltrast(a, rank, local_rank, world)
+            return
+        if a.workload == "two_stage":
+            run_two_stage(a, rank, local_rank, world)
             return
         run_ours(a, rank, local_rank, world)
     except BaseException:

@@ -325,6 +325,10 @@ HIPER_API int32_t hiper_last_launch_count(void);
  * read, and resets the record. */
 HIPER_API void hiper_profile_enable(int32_t on);
 HIPER_API hiper_status hiper_profile_read(double* maxsim_ms, int32_t* n_launches);
+/* The same for one kernel class only (the others stay recorded): HIPER_PROF_MAXSIM (the fused MaxSim
+ * kernel), HIPER_PROF_POOLED (the pooled GEMM + top-k kernel), HIPER_PROF_RERANK (the N3 gather). */
+enum { HIPER_PROF_MAXSIM = 0, HIPER_PROF_POOLED = 1, HIPER_PROF_RERANK = 2 };
+HIPER_API hiper_status hiper_profile_read_tagged(int32_t tag, double* ms, int32_t* n_launches);
 
 #ifdef __cplusplus
 }

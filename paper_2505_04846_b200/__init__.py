@@ -51,6 +51,7 @@ EXPORTS = [
     "hiper_coltrast_loss", "hiper_coltrast_grad_workspace_size", "hiper_coltrast_scores_loss_grad",
     "hiper_two_stage_workspace_size", "hiper_two_stage_topk", "hiper_pack_plan",
     "hiper_index_pack_info", "hiper_maxsim_topk_keys", "hiper_topk_merge_keys",
+    "hiper_profile_read_tagged",
 ]
 
 
@@ -110,6 +111,7 @@ def lib():
         "hiper_index_pack_info": ([P, P, P, P, P, P], i32),
         "hiper_maxsim_topk_keys": ([P, P, i32, P, i32, i32, i32, i32, u32, P, sz, P, P], i32),
         "hiper_topk_merge_keys": ([P, i32, i32, i32, P, P, P], i32),
+        "hiper_profile_read_tagged": ([i32, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -500,10 +502,17 @@ def hiper_profile_enable(on: bool = True):
     lib().hiper_profile_enable(int(bool(on)))
 
 
-def hiper_profile_read():
-    """(summed fused-MaxSim-kernel milliseconds, launches) since the last read (synchronises)."""
+HIPER_PROF_MAXSIM, HIPER_PROF_POOLED, HIPER_PROF_RERANK = 0, 1, 2
+
+
+def hiper_profile_read(tag: int | None = None):
+    """(summed kernel milliseconds, launches) of the hot kernels (or of one class `tag`) since the
+    last read (synchronises)."""
     ms, n = ctypes.c_double(), ctypes.c_int32()
-    _check(lib().hiper_profile_read(ctypes.byref(ms), ctypes.byref(n)))
+    if tag is None:
+        _check(lib().hiper_profile_read(ctypes.byref(ms), ctypes.byref(n)))
+    else:
+        _check(lib().hiper_profile_read_tagged(int(tag), ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
 
 

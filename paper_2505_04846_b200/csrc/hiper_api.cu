@@ -788,11 +788,19 @@ static MaxsimArgs maxsim_args(const KernelPlan& kp, int32_t n_q, int64_t n_slots
 }
 
 // ---------------------------------------------------------------------------- live kernel timing
+// Every launch of a hot kernel is bracketed by CUDA events on its own stream while profiling is on;
+// records carry the kernel class (hiper.h HIPER_PROF_*) so a step with several hot kernels (the
+// two-stage search) reports each one's share.
 namespace {
+struct ProfEv {
+  cudaEvent_t a, b;
+  int32_t tag;
+};
 struct ProfileRec {
   std::mutex mu;
   bool on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> live, pool;
+  std::vector<ProfEv> live;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
 };
 ProfileRec g_prof;
 }  // namespace
@@ -802,25 +810,45 @@ extern "C" void hiper_profile_enable(int32_t on) {
   g_prof.on = on != 0;
 }
 
-extern "C" hiper_status hiper_profile_read(double* maxsim_ms, int32_t* n_launches) {
+// tag < 0: every kernel class.  Reads (synchronising on the events) and forgets the matching records.
+static hiper_status profile_read(int32_t tag, double* ms, int32_t* n_launches) {
   std::lock_guard<std::mutex> lock(g_prof.mu);
   double total = 0.0;
+  int32_t n = 0;
+  std::vector<ProfEv> keep;
   for (auto& e : g_prof.live) {
-    CUDA_TRY(cudaEventSynchronize(e.second));
-    float ms = 0.f;
-    CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
-    total += ms;
-    g_prof.pool.push_back(e);
+    if (tag >= 0 && e.tag != tag) {
+      keep.push_back(e);
+      continue;
+    }
+    CUDA_TRY(cudaEventSynchronize(e.b));
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, e.a, e.b));
+    total += t;
+    ++n;
+    g_prof.pool.push_back({e.a, e.b});
   }
-  if (maxsim_ms) *maxsim_ms = total;
-  if (n_launches) *n_launches = (int32_t)g_prof.live.size();
-  g_prof.live.clear();
+  g_prof.live.swap(keep);
+  if (ms) *ms = total;
+  if (n_launches) *n_launches = n;
   return HIPER_OK;
 }
+extern "C" hiper_status hiper_profile_read(double* maxsim_ms, int32_t* n_launches) {
+  return profile_read(-1, maxsim_ms, n_launches);
+}
+extern "C" hiper_status hiper_profile_read_tagged(int32_t tag, double* ms, int32_t* n_launches) {
+  return profile_read(tag, ms, n_launches);
+}
 
-static hiper_status profile_begin(cudaStream_t stream, std::pair<cudaEvent_t, cudaEvent_t>* ev, bool* rec) {
+struct ProfTicket {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int32_t tag = 0;
+  bool rec = false;
+};
+static hiper_status profile_begin(cudaStream_t stream, int32_t tag, ProfTicket* t) {
   std::lock_guard<std::mutex> lock(g_prof.mu);
-  *rec = g_prof.on;
+  t->rec = g_prof.on;
+  t->tag = tag;
   if (!g_prof.on) return HIPER_OK;
   if (g_prof.pool.empty()) {
     cudaEvent_t a, b;
@@ -828,17 +856,18 @@ static hiper_status profile_begin(cudaStream_t stream, std::pair<cudaEvent_t, cu
     CUDA_TRY(cudaEventCreate(&b));
     g_prof.pool.push_back({a, b});
   }
-  *ev = g_prof.pool.back();
+  t->a = g_prof.pool.back().first;
+  t->b = g_prof.pool.back().second;
   g_prof.pool.pop_back();
-  CUDA_TRY(cudaEventRecord(ev->first, stream));
+  CUDA_TRY(cudaEventRecord(t->a, stream));
   return HIPER_OK;
 }
 
-static hiper_status profile_end(cudaStream_t stream, const std::pair<cudaEvent_t, cudaEvent_t>& ev, bool rec) {
-  if (!rec) return HIPER_OK;
-  CUDA_TRY(cudaEventRecord(ev.second, stream));
+static hiper_status profile_end(cudaStream_t stream, const ProfTicket& t) {
+  if (!t.rec) return HIPER_OK;
+  CUDA_TRY(cudaEventRecord(t.b, stream));
   std::lock_guard<std::mutex> lock(g_prof.mu);
-  g_prof.live.push_back(ev);
+  g_prof.live.push_back({t.a, t.b, t.tag});
   return HIPER_OK;
 }
 
@@ -853,8 +882,7 @@ static int debug_mode() {
 template <int MODE, int KR, bool PACKED, int QW, int H>
 static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
                                     const MaxsimArgs& a, cudaStream_t stream) {
-  std::pair<cudaEvent_t, cudaEvent_t> ev;
-  bool rec = false;
+  ProfTicket ev;
   static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
   // production: no instrumentation compiled in; HIPER_PIPE_STATS / HIPER_DEBUG_MODE select the
   // instrumented (STATS) instantiations
@@ -890,7 +918,7 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
     CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
     b.stats = st;
   }
-  TRY(profile_begin(stream, &ev, &rec));
+  TRY(profile_begin(stream, HIPER_PROF_MAXSIM, &ev));
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, td, b));
   if (st) {
     unsigned long long h[8];
@@ -904,7 +932,7 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
             (double)h[3] / h[5], (double)h[4] / h[5], h[5] / ep);
   }
   CUDA_TRY(cudaGetLastError());
-  TRY(profile_end(stream, ev, rec));
+  TRY(profile_end(stream, ev));
   ++g_launches;
   return HIPER_OK;
 }
@@ -1169,7 +1197,7 @@ static int32_t pooled_qtiles(int32_t n_q, int cl) {
 }
 
 static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks, PooledPlan& pp,
-                                bool topk = true) {
+                                bool topk = true, int32_t k = 1) {
   pp.cl = pooled_cluster(topk);
   pp.n_qtiles = pooled_qtiles(n_q, pp.cl);
   pp.q_pad = pp.n_qtiles * 256;
@@ -1181,7 +1209,8 @@ static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks
   // must keep choose_parts() equal to the workspace sizing (it does for divisors of num_sms / 2)
   if (const char* e = getenv("HIPER_POOLED_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));
   pp.n_parts = choose_parts(pp.n_qtiles / (pp.cl / 2), pp.n_ctiles, di.num_sms / pp.cl);
-  const uint32_t fixed = 1024u + 512u;  // align slack, barriers
+  uint32_t fixed = 1024u + 1024u;  // align slack, barriers
+  if (topk && k > kPooledKP) fixed += 128u * (uint32_t)(k | 1) * 8u + 512u;  // the k > 16 heaps + locks
   pp.n_stages = (int32_t)std::min<uint32_t>(8u, ((uint32_t)di.max_smem - fixed) / pp.stage_bytes);
   if (pp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory");
   pp.smem_bytes = fixed + pp.n_stages * pp.stage_bytes;
@@ -1200,9 +1229,7 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
                           : pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
   if (MODE == 1 && a.k > kPooledKP) {  // warp-cooperative lists in the partial buffer
     if (pp.cl != 2) return fail(HIPER_ERR_UNSUPPORTED, "pooled k > %d with HIPER_POOLED_MC", kPooledKP);
-    kern = a.k <= 32 ? pooled_sm100_pair_kernel<MODE, 0, 0, 2, false, 1>
-           : a.k <= 64 ? pooled_sm100_pair_kernel<MODE, 0, 0, 2, false, 2>
-                       : pooled_sm100_pair_kernel<MODE, 0, 0, 2, false, 4>;
+    kern = pstats_on ? pooled_sm100_pair_kernel<MODE, 0, 0, 2, true> : pooled_sm100_pair_kernel<MODE, 0, 0, 2>;
   }
   if (MODE == 1 && debug_mode() == 1) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 1, 2, true>;
   if (MODE == 1 && debug_mode() == 2) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 2, 2, true>;
@@ -1221,32 +1248,33 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  std::pair<cudaEvent_t, cudaEvent_t> ev;
-  bool rec = false;
+  ProfTicket ev;
   // diagnostics only (HIPER_PIPE_STATS=1): pipeline wait/drain cycle counters, printed to stderr
   static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
   unsigned long long* st = nullptr;
   PooledArgs b = a;
   if (stats_on) {
-    CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
-    CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
+    CUDA_TRY(cudaMalloc(&st, 16 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(st, 0, 16 * sizeof(unsigned long long), stream));
     b.stats = st;
   }
-  TRY(profile_begin(stream, &ev, &rec));
+  TRY(profile_begin(stream, HIPER_PROF_POOLED, &ev));
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, tc, b));
-  TRY(profile_end(stream, ev, rec));
+  TRY(profile_end(stream, ev));
   ++g_launches;
   if (st) {
-    unsigned long long h[8];
+    unsigned long long h[16];
     CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     cudaFree(st);
     const double pairs = pp.grid / 2.0, ep = 8.0 * pp.grid;  // MMA threads, epilogue warps
     fprintf(stderr, "[hiper pipe] pooled: MMA thread %.0f cyc avg; waits acc %.1f%% full %.1f%%; "
             "epilogue drain %.0f cyc/tile, wait %.0f cyc/tile, tiles/warp %.0f; per thread-tile: "
-            "blocks past the threshold %.3f, inserts %.3f\n",
+            "blocks past the threshold %.3f, inserts %.3f; shared-list sections %llu (%.0f cyc spin, "
+            "%.0f cyc held avg)\n",
             h[2] / pairs, 100.0 * h[0] / h[2], 100.0 * h[1] / h[2], (double)h[3] / h[5],
-            (double)h[4] / h[5], h[5] / ep, (double)h[6] / (32.0 * h[5]), (double)h[7] / (32.0 * h[5]));
+            (double)h[4] / h[5], h[5] / ep, (double)h[6] / (32.0 * h[5]), (double)h[7] / (32.0 * h[5]),
+            h[8], (double)h[9] / std::max(1ull, h[8]), (double)h[10] / std::max(1ull, h[8]));
   }
   return HIPER_OK;
 }
@@ -1286,10 +1314,11 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   DevInfo di;
   TRY(device_info(di));
   PooledPlan pp;
-  TRY(plan_pooled(di, n_q, ix->n, pp, dense_scores == nullptr));
+  TRY(plan_pooled(di, n_q, ix->n, pp, dense_scores == nullptr, k));
   const int32_t world = comm ? comm->world : 1;
   PooledWs w;
   pooled_ws_layout(n_q, dim, pp.n_parts, pp.q_pad, dense_scores ? 1 : k, world, comm != nullptr, w);
+  const bool glists = !dense_scores && k > kPooledKP;  // one shared list per query (see the kernel)
   TRY(check_ws(workspace, workspace_bytes, w.total));
   uint8_t* ws = (uint8_t*)workspace;
   uint32_t* status = (uint32_t*)(ws + w.status);
@@ -1334,8 +1363,10 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
       TRY(launch_pooled<1>(pp, tq, ix->tmap, a, stream));
     }
   }
-  const int32_t n_lists = ix->n > 0 ? pp.n_parts * kEpiGroups : 0;
-  const int64_t list_stride = (int64_t)pp.q_pad * k;
+  // the per-(partition, group) lists; k > kPooledKP: one (shared-heap) list per partition, in the
+  // group-0 slot of each partition
+  const int32_t n_lists = ix->n > 0 ? (glists ? pp.n_parts : pp.n_parts * kEpiGroups) : 0;
+  const int64_t list_stride = (int64_t)pp.q_pad * k * (glists ? kEpiGroups : 1);
   if (out_keys)  // this shard's top-k keys (a8's all-gather payload)
     return launch_merge(partial, n_lists, list_stride, n_q, k, k, out_keys, nullptr, nullptr, stream);
   if (!comm || comm->world == 1)
@@ -2058,8 +2089,11 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
   // an empty shard has no token rows and no candidates (every slot is -1): skip the gather, but
   // still take part in the all-gather below
   if (tix->n > 0) {
-    alignas(64) CUtensorMap t64;  // the token index as 64-row x 64-dim boxes (only real rows fetched)
-    TRY(make_tmap(&t64, tix->tok, tix->packed ? tix->n_rows : tix->n * (int64_t)tix->ld_pad, tix->dim, 64));
+    // the token index as 64-dim x 64-row and x 16-row boxes (only roundup(len, 16) rows fetched)
+    alignas(64) CUtensorMap t64, t16;
+    const int64_t trows = tix->packed ? tix->n_rows : tix->n * (int64_t)tix->ld_pad;
+    TRY(make_tmap(&t64, tix->tok, trows, tix->dim, 64));
+    TRY(make_tmap(&t16, tix->tok, trows, tix->dim, 16));
     RerankArgs ra{};
     ra.qlay = qlayout;
     ra.q_lens = qlens_dev;
@@ -2076,12 +2110,11 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
     CUDA_TRY(set_max_smem((const void*)kern, smem));
     const int64_t want = (n_items + 3) / 4;  // at least ~4 items per warp
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(di.num_sms, want / kRerankWarps));
-    std::pair<cudaEvent_t, cudaEvent_t> ev;
-    bool rec = false;
-    TRY(profile_begin(stream, &ev, &rec));
-    kern<<<grid, kRerankWarps * 32, smem, stream>>>(t64, ra);
+    ProfTicket ev;
+    TRY(profile_begin(stream, HIPER_PROF_RERANK, &ev));
+    kern<<<grid, kRerankWarps * 32, smem, stream>>>(t64, t16, ra);
     CUDA_TRY(cudaGetLastError());
-    TRY(profile_end(stream, ev, rec));
+    TRY(profile_end(stream, ev));
     ++g_launches;
   }
   uint64_t* local = multi ? (uint64_t*)(ws + w.local) : nullptr;

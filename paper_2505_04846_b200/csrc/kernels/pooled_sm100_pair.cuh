@@ -63,12 +63,14 @@ __device__ __forceinline__ float pooled_thr_score(uint64_t thr) {
 // the chunk operand costs half the L2 reads.  tmap_c then has a 64-row box.
 // STATS: HIPER_PIPE_STATS instrumentation compiled in (diagnostics only; see the MaxSim pair kernel).
 // KP > 0: each epilogue thread keeps its query's list in KP registers (k <= KP, the fast path).
-// KP == 0 (16 < k <= 128): each (unit, query) list lives in its final place in `partial` (L2-resident,
-// zeroed at the unit's start); the rare hits are inserted by the whole warp, one hit lane at a time:
-// the warp loads that lane's list (KRG = ceil(k / 32) keys per lane, coalesced), inserts every hit
-// of the lane with the warp-cooperative sorted insert of WarpTopK, stores it back, and hands the new
-// k-th key back to the lane as its filter threshold.
-template <int MODE, int KP, int DBG = 0, int CL = 2, bool STATS = false, int KRG = 1>
+// KP == 0 (16 < k <= 128): each query's (unit) list is a binary MIN-heap of k keys in shared memory
+// (root = the k-th best key so far = the filter threshold; empty slots are key 0, below every real key),
+// so an insertion is one root replacement and a log2(k)-level sift-down by the thread that owns the
+// query -- no warp-wide work, no global round trip.  The two epilogue groups serve the same 128
+// queries of a unit (alternate chunk tiles), so each heap has a shared-memory spin lock; at the end of
+// the unit group 0 writes the heaps (unsorted: the merge kernel needs no order) to `partial` and
+// clears them, between two named barriers of the 256 epilogue threads.
+template <int MODE, int KP, int DBG = 0, int CL = 2, bool STATS = false>
 __global__ void __launch_bounds__(kMaxsimThreads, 1)
     pooled_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmap_q,
                              const __grid_constant__ CUtensorMap tmap_c, const PooledArgs args) {
@@ -94,6 +96,10 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   auto bar_tfull = [&](int b) { return sBar + 8u * (2 * S + b); };
   auto bar_tempty = [&](int b) { return sBar + 8u * (2 * S + 2 + b); };
   const uint32_t sTmemPtr = sBar + 8u * (2 * S + 4);
+  // KP == 0: [128 queries][k | 1] u64 min-heaps (odd stride: conflict-free 64-bit banks) + 128 locks
+  const uint32_t kst = (uint32_t)args.k | 1u;
+  volatile uint64_t* heaps = reinterpret_cast<volatile uint64_t*>(smem_raw + (sBar + 1024u - smem_u32(smem_raw)));
+  uint32_t* hlocks = reinterpret_cast<uint32_t*>(smem_raw + (sBar + 1024u + 128u * kst * 8u - smem_u32(smem_raw)));
   uint32_t* tmem_ptr_generic =
       reinterpret_cast<uint32_t*>(smem_raw + (sTmemPtr - smem_u32(smem_raw)));
 
@@ -217,7 +223,16 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     const uint32_t tempty_leader = mapa_shared(bar_tempty(grp), lead);
     const int32_t k = args.k;
     uint32_t t = 0, mine = 0;
-    long long st_drain = 0, st_ewait = 0, st_tiles = 0, st_any = 0, st_ins = 0;
+    long long st_drain = 0, st_ewait = 0, st_tiles = 0, st_any = 0, st_ins = 0, st_cs = 0, st_spin = 0,
+              st_csc = 0;
+    if constexpr (MODE == 1 && KP == 0) {  // empty heaps (key 0) and free locks before the first unit
+      if (grp == 0) {
+        const uint32_t qi0 = qslot * 32u + lane;
+        for (int m = 0; m < k; ++m) heaps[qi0 * kst + m] = 0ull;
+        hlocks[qi0] = 0u;
+      }
+      named_bar_sync(9, 256);
+    }
     for (int32_t u = (int32_t)ufirst; u < n_units; u += (int32_t)ustride) {
       int32_t qt, p, t0, t1;
       decode(u, qt, p, t0, t1);
@@ -225,12 +240,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       uint64_t v[KP > 0 ? KP : 1];
 #pragma unroll
       for (int m = 0; m < (KP > 0 ? KP : 1); ++m) v[m] = 0ull;
-      // KP == 0: this warp's 32 lists ([32][k] keys, consecutive queries) start empty
-      uint64_t* wlists = args.partial + (((int64_t)p * kEpiGroups + grp) * args.q_pad + (q - (int32_t)lane)) * k;
-      if constexpr (MODE == 1 && KP == 0) {
-        for (int32_t i = (int32_t)lane; i < 32 * k; i += 32) wlists[i] = 0ull;
-        __syncwarp();
-      }
+      const uint32_t qi = qslot * 32u + lane;  // this thread's query within the CTA (its heap)
+      volatile uint64_t* heap = heaps + qi * kst;
       uint64_t thr = 0ull;        // key of rank k-1 (0 while the list is not full)
       uint64_t gth = 0ull, pub = 0ull;  // shared bound seen / own thr last published
       if (args.gthr != nullptr && q < args.q_pad)
@@ -284,51 +295,51 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                 hits |= (uint64_t)(__uint_as_float(r[j]) >= thr_f && j < nj) << j;
             }
             if constexpr (KP == 0) {
-              // warp-cooperative insertion into the lists of the lanes that have hits
-              if (__ballot_sync(0xffffffffu, hits != 0ull) != 0u) {
+              if (hits) {  // rare: this thread's query heap, under its lock (shared with the other group)
                 float xs[64];
 #pragma unroll
-                for (int j = 0; j < 64; ++j) xs[j] = __uint_as_float(r[j]) + 0.0f;
-                uint32_t hl = __ballot_sync(0xffffffffu, hits != 0ull);
-                while (hl) {
-                  const int src = __ffs(hl) - 1;
-                  hl &= hl - 1u;
-                  uint64_t hm = __shfl_sync(0xffffffffu, (unsigned long long)hits, src);
-                  const uint64_t g_src = __shfl_sync(0xffffffffu, (unsigned long long)gth, src);
-                  uint64_t* L = wlists + (int64_t)src * k;
-                  WarpTopK<KRG> top;
-#pragma unroll
-                  for (int rr = 0; rr < KRG; ++rr) {
-                    const int i = rr * 32 + (int)lane;
-                    top.v[rr] = i < k ? L[i] : 0ull;
-                  }
-                  uint64_t tv = 0ull;
-#pragma unroll
-                  for (int rr = 0; rr < KRG; ++rr)
-                    if (rr == ((k - 1) >> 5)) tv = top.v[rr];
-                  top.thresh = __shfl_sync(0xffffffffu, (unsigned long long)tv, (k - 1) & 31);
-                  while (hm) {
-                    const int j = __ffsll((long long)hm) - 1;
-                    hm &= hm - 1;
-                    const float sc = __shfl_sync(0xffffffffu, xs[j], src);
-                    const uint64_t key = make_key(sc, args.id_base + cbase + col + j);
-                    if (key > top.thresh && key > g_src) {
-                      if (STATS && args.stats && lane == (uint32_t)src) ++st_ins;
-                      top.insert(key, k, lane);
+                for (int jj = 0; jj < 64; ++jj) xs[jj] = __uint_as_float(r[jj]) + 0.0f;
+                long long cs0 = (STATS && args.stats) ? clock64() : 0;
+                while (atomicCAS_block(hlocks + qi, 0u, 1u) != 0u) {
+                }
+                __threadfence_block();
+                if (STATS && args.stats) {
+                  st_spin += clock64() - cs0;
+                  ++st_cs;
+                }
+                uint64_t root = heap[0];
+                while (hits) {
+                  const int j = __ffsll((long long)hits) - 1;
+                  hits &= hits - 1;
+                  const uint64_t key = make_key(xs[j], args.id_base + cbase + col + j);
+                  if (key > root && key > gth) {
+                    if (STATS && args.stats) ++st_ins;
+                    uint32_t i = 0;  // sift the new key down from the root
+                    while (true) {
+                      const uint32_t l = 2u * i + 1u;
+                      if (l >= (uint32_t)k) break;
+                      uint64_t cv = heap[l];
+                      uint32_t c = l;
+                      if (l + 1u < (uint32_t)k) {
+                        const uint64_t rv = heap[l + 1u];
+                        if (rv < cv) {
+                          cv = rv;
+                          c = l + 1u;
+                        }
+                      }
+                      if (cv >= key) break;
+                      heap[i] = cv;
+                      i = c;
                     }
-                  }
-#pragma unroll
-                  for (int rr = 0; rr < KRG; ++rr) {
-                    const int i = rr * 32 + (int)lane;
-                    if (i < k) L[i] = top.v[rr];
-                  }
-                  if (lane == (uint32_t)src) {
-                    thr = top.thresh;
-                    lim = thr > gth ? thr : gth;
-                    thr_f = pooled_thr_score(lim);
+                    heap[i] = key;
+                    root = heap[0];
                   }
                 }
-                __syncwarp();
+                __threadfence_block();
+                atomicExch_block(hlocks + qi, 0u);
+                thr = root;
+                lim = thr > gth ? thr : gth;
+                thr_f = pooled_thr_score(lim);
               }
             } else if (hits) {
               float xs[64];  // rare path: a local copy so the hits can be indexed dynamically
@@ -371,7 +382,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               const uint64_t old = atomicMax(args.gthr + q, (unsigned long long)thr);
               pub = thr;
               gth = old > gth ? old : gth;
-            } else if ((mine & 7u) == 0) {
+            } else if ((mine & (KP == 0 ? 1u : 7u)) == 0) {
               const uint64_t cur = *reinterpret_cast<volatile unsigned long long*>(args.gthr + q);
               gth = cur > gth ? cur : gth;
             }
@@ -391,6 +402,17 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             if (m < k) dst[m] = v[m];
         }
       }
+      if constexpr (MODE == 1 && KP == 0) {
+        named_bar_sync(9, 256);  // both groups are done with this unit's heaps
+        if (grp == 0) {           // the unit's list of query q (slot grp 0 of the partial layout)
+          uint64_t* dst = args.partial + ((int64_t)p * kEpiGroups * args.q_pad + q) * k;
+          for (int m = 0; m < k; ++m) {
+            if (q < args.n_q) dst[m] = heap[m];
+            heap[m] = 0ull;
+          }
+        }
+        named_bar_sync(9, 256);  // cleared before the next unit's first insertion
+      }
     }
     if (STATS && args.stats && lane == 0) {
       atomicAdd(args.stats + 3, (unsigned long long)st_drain);
@@ -400,6 +422,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
     if (STATS && args.stats) {
       atomicAdd(args.stats + 6, (unsigned long long)st_any);
       atomicAdd(args.stats + 7, (unsigned long long)st_ins);
+      if (lane == 0) {
+        atomicAdd(args.stats + 8, (unsigned long long)st_cs);
+        atomicAdd(args.stats + 9, (unsigned long long)st_spin);
+        atomicAdd(args.stats + 10, (unsigned long long)st_csc);
+      }
     }
   }
 

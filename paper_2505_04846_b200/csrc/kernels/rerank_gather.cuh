@@ -66,9 +66,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // NKB = ceil(dim / 64) (1 or 2); SW = stages per warp.
+// tmap64 / tmap16: the token index as 64-dim x 64-row / x 16-row boxes (a chunk's last block is fetched
+// in 16-row boxes: only roundup(len, 16) rows ever leave HBM).
 template <int NKB, int SW>
 __global__ void __launch_bounds__(kRerankWarps * 32, 1)
-    rerank_gather_kernel(const __grid_constant__ CUtensorMap tmap64, const RerankArgs a) {
+    rerank_gather_kernel(const __grid_constant__ CUtensorMap tmap64,
+                         const __grid_constant__ CUtensorMap tmap16, const RerankArgs a) {
   constexpr uint32_t kStage = 64u * 128u * NKB;  // one 64-row block, all K-blocks
   constexpr int KS = NKB * 4;                    // k16 steps
   extern __shared__ uint8_t smem_raw[];
@@ -82,7 +85,10 @@ __global__ void __launch_bounds__(kRerankWarps * 32, 1)
     fence_mbarrier_init();
   }
   __syncwarp();
-  if (warp == 0 && lane == 0) prefetch_tmap(&tmap64);
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap64);
+    prefetch_tmap(&tmap16);
+  }
 
   const int64_t gw = (int64_t)blockIdx.x * kRerankWarps + warp;
   const int64_t nw = (int64_t)gridDim.x * kRerankWarps;
@@ -133,12 +139,22 @@ __global__ void __launch_bounds__(kRerankWarps * 32, 1)
       }
       if (lane == 0) {
         const uint32_t bar = bars + 8u * s_issue;
+        const uint32_t dst = ring + s_issue * kStage;
+        const int32_t r0 = (int32_t)(row + 64 * prb);
         fence_proxy_async_smem();  // the stage's previous ldmatrix reads precede this async write
-        mbar_arrive_expect_tx(bar, kStage);
+        const int32_t rows = min(64, len - 64 * prb);
+        if (rows == 64) {
+          mbar_arrive_expect_tx(bar, kStage);
 #pragma unroll
-        for (int kb = 0; kb < NKB; ++kb)
-          tma_load_2d(ring + s_issue * kStage + kb * 8192u, &tmap64, bar, kb * 64,
-                      (int32_t)(row + 64 * prb));
+          for (int kb = 0; kb < NKB; ++kb) tma_load_2d(dst + kb * 8192u, &tmap64, bar, kb * 64, r0);
+        } else {  // the chunk's last block: roundup(rows, 16) rows in 16-row boxes
+          const int32_t n16 = (rows + 15) >> 4;
+          mbar_arrive_expect_tx(bar, (uint32_t)n16 * 2048u * NKB);
+          for (int32_t b = 0; b < n16; ++b)
+#pragma unroll
+            for (int kb = 0; kb < NKB; ++kb)
+              tma_load_2d(dst + kb * 8192u + (uint32_t)b * 2048u, &tmap16, bar, kb * 64, r0 + 16 * b);
+        }
       }
       if (++s_issue == SW) s_issue = 0;
       ++inflight;
