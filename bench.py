@@ -201,36 +201,59 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ oracle leg
+def host_cpu_model():
+    """The host CPU model name (lscpu), for the cpu_baseline record."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class OracleSample:
+    """A bounded sample of the workload for the CPU oracle: C_s chunks (generated and NORM'd once,
+    build-time on both sides) and n_q queries.  run() times the oracle as it stands: NORM of the
+    sample queries + MaxSim of every (query, chunk) pair + exact top-k."""
+
+    def __init__(self, a, n_chunks_sample, n_queries_sample=None):
+        import numpy as np
+
+        import oracle
+        from synth import gen
+        self.a = a
+        self.cores = len(os.sched_getaffinity(0))
+        self.nq = n_queries_sample or (256 if a.chunk_len == 1 else 4)
+        self.C_s = int(n_chunks_sample)
+        corp = gen.corpus(a.seed, 0, self.C_s, a.chunk_len, a.dim)
+        self.clen = (gen.semantic_lengths(a.seed, self.C_s, a.chunk_len) if getattr(a, "semantic", False)
+                     else np.full(self.C_s, a.chunk_len, np.int32))
+        self.cn = oracle.norm_rows(corp)
+        self.q = gen.queries(a.qseed, self.nq, a.query_len, a.dim, corpus_seed=a.seed,
+                             n_chunks=a.chunks, L=a.chunk_len)
+        self.ids = np.arange(self.C_s, dtype=np.int64)
+
+    def run(self):
+        """(queries/s over the full corpus, extrapolated linearly in its size; seconds)."""
+        import numpy as np
+
+        import oracle
+        t0 = time.perf_counter()
+        qn = oracle.norm_rows(self.q)
+        S = oracle.maxsim_matrix(qn, np.full(self.nq, self.a.query_len, np.int32), self.cn, self.clen,
+                                 n_threads=self.cores)
+        for r in range(self.nq):
+            oracle.topk(S[r], self.ids, self.a.k)
+        dt = time.perf_counter() - t0
+        return self.nq / (dt * self.a.chunks / self.C_s), dt
+
+
 def oracle_sample(a, n_chunks_sample, n_queries_sample=None):
-    """Time the CPU oracle (as it stands) on a bounded sample of the same workload.
-
-    Timed: NORM of the sample queries + MaxSim of every (query, chunk) pair + exact top-k.
-    (The corpus NORM is build-time on both sides and excluded.)"""
-    import numpy as np
-
-    import oracle
-    from synth import gen
-    cores = len(os.sched_getaffinity(0))
-    if n_queries_sample is None:
-        n_queries_sample = 256 if a.chunk_len == 1 else 4
-    C_s = int(n_chunks_sample)
-    corp = gen.corpus(a.seed, 0, C_s, a.chunk_len, a.dim)
-    clen = (gen.semantic_lengths(a.seed, C_s, a.chunk_len) if getattr(a, "semantic", False)
-            else np.full(C_s, a.chunk_len, np.int32))
-    cn = oracle.norm_rows(corp)
-    q = gen.queries(a.qseed, n_queries_sample, a.query_len, a.dim, corpus_seed=a.seed,
-                    n_chunks=a.chunks, L=a.chunk_len)
-    ids = np.arange(C_s, dtype=np.int64)
-    t0 = time.perf_counter()
-    qn = oracle.norm_rows(q)
-    S = oracle.maxsim_matrix(qn, np.full(n_queries_sample, a.query_len, np.int32), cn, clen,
-                             n_threads=cores)
-    for r in range(n_queries_sample):
-        oracle.topk(S[r], ids, a.k)
-    dt = time.perf_counter() - t0
-    # queries/s over the full corpus, extrapolated linearly in the corpus size
-    qps = n_queries_sample / (dt * a.chunks / C_s)
-    return qps, dt, cores, C_s, n_queries_sample
+    smp = OracleSample(a, n_chunks_sample, n_queries_sample)
+    qps, dt = smp.run()
+    return qps, dt, smp.cores, smp.C_s, smp.nq
 
 
 def calibrated_oracle(a, seconds):
@@ -246,25 +269,29 @@ def run_reference(a, rank, world):
         return
     import oracle
     oracle.build()
-    per_step = max(1.0, min(6.0, 150.0 / max(1, a.steps + a.warmup)))
+    # each step: the same bounded sample (generated and NORM'd once, outside the timed steps), sized so
+    # the whole --warmup W --steps K run stays within ~2.5 minutes of oracle work
+    per_step = max(0.5, min(6.0, 150.0 / max(1, a.steps + a.warmup)))
     _, dt0, cores, _, nq = oracle_sample(a, 64)
     C_s = int(max(64, min(200_000, 64 * per_step / max(dt0, 1e-3), a.chunks)))
+    smp = OracleSample(a, C_s, nq)
     times = []
     for i in range(a.warmup + a.steps):
-        qps, dt, cores, C_s, nq = oracle_sample(a, C_s, nq)
+        _, dt = smp.run()
         if i >= a.warmup:
             times.append(dt)
     dt = sum(times) / len(times)
     value = nq / (dt * a.chunks / C_s)
+    cores = smp.cores
     sample = (f"{nq} queries x {C_s} chunks per step (of {a.chunks}); queries/s extrapolated "
-              f"linearly to the full corpus; float64 C oracle, OpenMP over pairs")
+              f"linearly to the full corpus; float64 C oracle, OpenMP over pairs; host {host_cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(a, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": host_cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -284,8 +311,7 @@ def run_ours(a, rank, local_rank, world):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     H.lib()
-    c0 = rank * a.chunks // world
-    c1 = (rank + 1) * a.chunks // world
+    c0, c1 = H.hiper_shard_range(a.chunks, world, rank)
     n_local = c1 - c0
     corpus = None
     if not a.gen_packed:
@@ -439,6 +465,7 @@ def run_ours(a, rank, local_rank, world):
             "value": qps, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": (f"{nq} queries x {C_s} chunks ({dt:.1f} s: query NORM + MaxSim + top-k), "
                        f"extrapolated linearly to {a.chunks} chunks; float64 C oracle, OpenMP"),
+            "cpu_model": host_cpu_model(),
         }
     emit(line)
     if dist is not None:
@@ -480,6 +507,7 @@ def coltrast_oracle_sample(a, seed, qseed):
         n_s = min(B, n_s * 4)
     step_s = dt * B / n_s
     return {"value": 1.0 / step_s, "unit": "steps/s", "cores": cores, "kind": "oracle",
+            "cpu_model": host_cpu_model(),
             "sample": f"{n_s} of {B} query rows x {B} docs ({dt:.1f} s: NORM + MaxSim + InfoNCE rows), "
                       f"extrapolated linearly to the {B}x{B} step; float64 C oracle, OpenMP"}
 
@@ -645,6 +673,7 @@ def two_stage_oracle_sample(a, lens_all, seconds=10.0):
     t2 = time.perf_counter() - t0
     per_q = (t1 * a.chunks / C_s + t2) / n_s
     return {"value": 1.0 / per_q, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": host_cpu_model(),
             "sample": (f"{n_s} queries: stage 1 over {C_s} of {a.chunks} pooled chunks ({t1:.1f} s, "
                        f"scaled linearly), stage 2 over their {a.k1} candidates each ({t2:.1f} s); "
                        f"float64 C oracle, OpenMP")}
@@ -665,7 +694,7 @@ def run_two_stage(a, rank, local_rank, world):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     H.lib()
-    c0, c1 = rank * a.chunks // world, (rank + 1) * a.chunks // world
+    c0, c1 = H.hiper_shard_range(a.chunks, world, rank)
     n_local = c1 - c0
     lens_all = gen.semantic_lengths(a.seed, a.chunks, a.chunk_len)
     lens = lens_all[c0:c1].copy()

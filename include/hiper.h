@@ -112,6 +112,10 @@ HIPER_API int32_t hiper_version(void); /* major*10000 + minor*100 + patch */
  * binding uses torch.distributed); every rank then calls hiper_comm_create.  The communicator carries
  * exactly one collective per query batch: an ncclAllGather of each shard's local top-k keys
  * (BASELINE.json north_star: "merged with one NCCL all-gather over NVLink"). */
+/* The corpus shard plan (pure host function): rank r of `world` holds chunks [c0, c1) =
+ * [r * n / world, (r + 1) * n / world) -- contiguous, sizes within one of each other; builds its index
+ * with id_base = c0. */
+HIPER_API hiper_status hiper_shard_range(int64_t n, int32_t world, int32_t rank, int64_t* c0, int64_t* c1);
 HIPER_API hiper_status hiper_comm_unique_id(uint8_t id[128]);
 HIPER_API hiper_status hiper_comm_create(const uint8_t id[128], int32_t world, int32_t rank, int32_t device,
                                hiper_comm** out);

@@ -51,7 +51,7 @@ EXPORTS = [
     "hiper_coltrast_loss", "hiper_coltrast_grad_workspace_size", "hiper_coltrast_scores_loss_grad",
     "hiper_two_stage_workspace_size", "hiper_two_stage_topk", "hiper_pack_plan",
     "hiper_index_pack_info", "hiper_maxsim_topk_keys", "hiper_topk_merge_keys",
-    "hiper_profile_read_tagged",
+    "hiper_profile_read_tagged", "hiper_shard_range",
 ]
 
 
@@ -112,6 +112,7 @@ def lib():
         "hiper_maxsim_topk_keys": ([P, P, i32, P, i32, i32, i32, i32, u32, P, sz, P, P], i32),
         "hiper_topk_merge_keys": ([P, i32, i32, i32, P, P, P], i32),
         "hiper_profile_read_tagged": ([i32, P, P], i32),
+        "hiper_shard_range": ([i64, i32, i32, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -184,6 +185,13 @@ def _dev_ptr(t):
 
 
 # ---------------------------------------------------------------------------------------- comm
+def hiper_shard_range(n: int, world: int, rank: int):
+    """(c0, c1): the chunks rank `rank` of `world` holds (the library's shard plan; id_base = c0)."""
+    c0, c1 = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().hiper_shard_range(int(n), int(world), int(rank), ctypes.byref(c0), ctypes.byref(c1)))
+    return c0.value, c1.value
+
+
 class Comm:
     """NCCL communicator for the corpus-sharded search; bootstrapped over torch.distributed."""
 

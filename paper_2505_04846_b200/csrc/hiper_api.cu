@@ -1025,6 +1025,17 @@ static hiper_status gather_merge(const hiper_comm_s* c, const uint64_t* local, u
                                  int32_t n_q, int32_t k, float* out_scores, int64_t* out_ids,
                                  cudaStream_t stream);
 
+extern "C" hiper_status hiper_shard_range(int64_t n, int32_t world, int32_t rank, int64_t* c0,
+                                          int64_t* c1) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world || !c0 || !c1)
+    return fail(HIPER_ERR_INVALID_ARG, "bad shard arguments (n %lld, world %d, rank %d)", (long long)n,
+                world, rank);
+  // contiguous ranges, sizes differing by at most one: [rank * n / world, (rank + 1) * n / world)
+  *c0 = (int64_t)((__int128)rank * n / world);
+  *c1 = (int64_t)((__int128)(rank + 1) * n / world);
+  return HIPER_OK;
+}
+
 extern "C" hiper_status hiper_comm_unique_id(uint8_t id[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   if (!id) return fail(HIPER_ERR_INVALID_ARG, "id is NULL");

@@ -1,5 +1,5 @@
 // synth.cu -- device implementation of synth/gen.py's counter-based generator (same integer recipe,
-// bit-identical outputs; checked by tests/test_synth_gpu.py).  Holds none of the method's arithmetic:
+// bit-identical outputs; checked by tests/test_gpu_parity.py::test_synth_device_matches_numpy).  Holds none of the method's arithmetic:
 // it only draws raw token embeddings for benchmarks/tests at sizes numpy cannot produce quickly
 // (e.g. a 1M x 256 x 128 corpus, 65.5 GB, generated directly in HBM).
 #include <cuda_bf16.h>

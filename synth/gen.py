@@ -3,7 +3,7 @@
 This module holds NONE of the method's arithmetic (no normalisation, no dot products, no max/sum,
 no top-k, no loss): it only draws token embeddings.  It is a counter-based generator, so any
 (chunk, token, dim) element can be produced independently and identically here and on the device
-(``synth/csrc/synth.cu`` implements the same integer recipe; ``tests/test_synth_gpu.py`` checks the
+(``synth/csrc/synth.cu`` implements the same integer recipe; ``tests/test_gpu_parity.py::test_synth_device_matches_numpy`` checks the
 two bitwise).
 
 Recipe (DESIGN.md "Input recipe"):

@@ -66,7 +66,7 @@ def main():
     for k, packed in ((10, False), (100, False), (10, True)):
         lens_use = sem_all if packed else lens_all
         flags = H.HIPER_PACKED if packed else 0
-        c0, c1 = rank * C // world, (rank + 1) * C // world
+        c0, c1 = H.hiper_shard_range(C, world, rank)
         shard = torch.empty((c1 - c0, L, d), dtype=torch.bfloat16, device="cuda")
         device.corpus_(shard, seed, c0)
         idx = H.hiper_index_build(shard, lens_use[c0:c1], id_base=c0, flags=flags)
@@ -93,7 +93,7 @@ def main():
     # ---- NEXT N3 across ranks: global pooled top-k1, owner re-scoring, one more all-gather
     Ct, Lt, dp, k1, k = 4003, 128, 768, 100, 10
     tl_all = gen.lengths(81, Ct, Lt, True)
-    c0, c1 = rank * Ct // world, (rank + 1) * Ct // world
+    c0, c1 = H.hiper_shard_range(Ct, world, rank)
     to_dev16 = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda().view(torch.bfloat16)
     qt2 = gen.queries(83, 21, Lq, d, corpus_seed=81, n_chunks=Ct, L=Lt, chunk_lens_fn=lambda c: tl_all[c])
     ql2 = gen.lengths(83, 21, Lq, True, stream=gen.QLEN)
