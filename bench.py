@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--qseed", type=int, default=2)
     ap.add_argument("--grad", action="store_true",
                     help="config2 only: time forward + backward (NEXT N1) instead of forward only")
+    ap.add_argument("--full-loss", action="store_true",
+                    help="config2 only: time the full ColTrast loss L = (L_LI + L_C)/2 (NEXT N2): "
+                         "L_C over every rank's pooled passages gathered over NVLink peer memory "
+                         "(HIPER_N2_NCCL=1: through ncclAllGather instead)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -538,6 +542,12 @@ def run_coltrast(a, rank, local_rank, world):
            torch.empty(1, dtype=torch.float32, device="cuda"))
     stream = torch.cuda.current_stream()
 
+    comm = H.Comm() if (a.full_loss and world > 1) else None
+    if a.full_loss:
+        dp = a.pooled_dim
+        dpool = to_dev(gen.corpus(9 + 100 * rank, 0, B, 1, dp)[:, 0])
+        qpool = to_dev(gen.queries(10 + 100 * rank, B, 1, dp, corpus_seed=9 + 100 * rank, n_chunks=B,
+                                   L=1, diagonal=True, sigma_q=np.float32(4.0))[:, 0])
     if a.grad:
         nbg = H.lib().hiper_coltrast_grad_workspace_size(B, B, L, d)
         gws, gwp, gwn = H._workspace(nbg, "cuda")
@@ -546,6 +556,11 @@ def run_coltrast(a, rank, local_rank, world):
         import ctypes
 
     def step(qd=qs, dd=docs):
+        if a.full_loss:
+            losses, _, _ = H.hiper_coltrast_loss(qd, ql, dd, dl, qpool, dpool, n_max=world * B,
+                                                 tau_li=1.0, tau_c=0.05, comm=comm, stream=stream)
+            out[1].copy_(losses[2:3])
+            return
         if a.grad:
             H._check(H.lib().hiper_coltrast_scores_loss_grad(
                 H._dev_ptr(qd), H._ptr(ql), B, Lq, H._dev_ptr(dd), H._ptr(dl), B, L, d,
@@ -586,7 +601,8 @@ def run_coltrast(a, rank, local_rank, world):
     e1.record(stream)
     barrier()
     H.hiper_profile_enable(False)
-    kern_ms, kern_n = H.hiper_profile_read()
+    kern_ms, kern_n = H.hiper_profile_read(H.HIPER_PROF_MAXSIM)
+    H.hiper_profile_read()  # (the full loss's pooled GEMM launches: not the a10 kernel)
     clk = clocks.stop() if clocks else None
     ms = max_over_ranks(e0.elapsed_time(e1))
     kern_avg = max_over_ranks(kern_ms / max(kern_n, 1))
@@ -615,7 +631,10 @@ def run_coltrast(a, rank, local_rank, world):
     value = world * steps / (ms / 1e3)
     line = {
         "metric": ("ColTrast in-batch MaxSim scores + InfoNCE + backward (N1) steps/s (B=256, configs[1])"
-                   if a.grad else "ColTrast in-batch MaxSim scores + InfoNCE steps/s (B=256, configs[1])"),
+                   if a.grad else
+                   ("ColTrast full loss (L_LI + L_C over the gathered pooled passages, N2) steps/s "
+                    f"(B=256 per rank, {'NCCL all-gather' if os.environ.get('HIPER_N2_NCCL') else 'NVLink peer-window gather'})")
+                   if a.full_loss else "ColTrast in-batch MaxSim scores + InfoNCE steps/s (B=256, configs[1])"),
         "value": value, "unit": "steps/s", "n_gpus": world, "steps": steps, "warmup": a.warmup,
         "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",

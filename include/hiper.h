@@ -268,6 +268,26 @@ HIPER_API hiper_status hiper_coltrast_loss(const void* q_tokens, const int32_t* 
                                            float* out_scores_c, int32_t* out_m,
                                            hiper_stream_t stream);
 
+/* The gather of L_C's candidates: with a communicator of ranks on one node, every rank NORMs its
+ * pooled passages straight into its own window -- device memory exported once with CUDA IPC and mapped
+ * by every peer when the communicator is first used here (collective) -- and publishes a ready epoch;
+ * one kernel then reads the local and the peers' windows over NVLink in min(N, W) order into the
+ * candidate matrix (no ncclAllGather, no reorder copies).  Without IPC (ranks on different nodes), or
+ * with HIPER_N2_NCCL set, an ncclAllGather feeds the same kernel.
+ *
+ * hiper_coltrast_loss_simulated (test support): the same computation for rank `rank` of `world`
+ * simulated ranks on ONE GPU: d_pooled_all is device [world][b][dp], every simulated rank's passages
+ * (each rank's own are its slice); everything else as hiper_coltrast_loss. */
+HIPER_API size_t hiper_coltrast_loss_simulated_workspace_size(int32_t b, int32_t d_max_len, int32_t dim,
+                                                              int32_t dp, int32_t n_max, int32_t world);
+HIPER_API hiper_status hiper_coltrast_loss_simulated(
+    const void* q_tokens, const int32_t* q_lens, int32_t q_max_len, const void* d_tokens,
+    const int32_t* d_lens, int32_t d_max_len, int32_t dim, const void* q_pooled,
+    const void* d_pooled_all, int32_t dp, int32_t b, hiper_dtype dtype, uint32_t flags,
+    int32_t n_max, float tau_li, float tau_c, int32_t world, int32_t rank, void* workspace,
+    size_t workspace_bytes, float* out_losses, float* out_scores_c, int32_t* out_m,
+    hiper_stream_t stream);
+
 /* ------------------------------------------------------------------ NEXT N1: backward of L_LI
  * Forward exactly as hiper_coltrast_scores_loss (the fused kernel additionally records the argmax
  * doc token of every max), then the gradient of L_LI with respect to the RAW token inputs:

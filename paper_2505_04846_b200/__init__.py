@@ -51,7 +51,8 @@ EXPORTS = [
     "hiper_coltrast_loss", "hiper_coltrast_grad_workspace_size", "hiper_coltrast_scores_loss_grad",
     "hiper_two_stage_workspace_size", "hiper_two_stage_topk", "hiper_pack_plan",
     "hiper_index_pack_info", "hiper_maxsim_topk_keys", "hiper_topk_merge_keys",
-    "hiper_profile_read_tagged", "hiper_shard_range",
+    "hiper_profile_read_tagged", "hiper_shard_range", "hiper_coltrast_loss_simulated",
+    "hiper_coltrast_loss_simulated_workspace_size",
 ]
 
 
@@ -113,6 +114,10 @@ def lib():
         "hiper_topk_merge_keys": ([P, i32, i32, i32, P, P, P], i32),
         "hiper_profile_read_tagged": ([i32, P, P], i32),
         "hiper_shard_range": ([i64, i32, i32, P, P], i32),
+        "hiper_coltrast_loss_simulated_workspace_size": ([i32, i32, i32, i32, i32, i32], sz),
+        "hiper_coltrast_loss_simulated": ([P, P, i32, P, P, i32, i32, P, P, i32, i32, i32, u32, i32,
+                                           ctypes.c_float, ctypes.c_float, i32, i32, P, sz, P, P, P,
+                                           P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -550,6 +555,32 @@ def hiper_coltrast_loss(q_tokens, q_lens, d_tokens, d_lens, q_pooled, d_pooled, 
         float(tau_li), float(tau_c), comm.handle if comm else None, ctypes.c_void_p(wp), wn,
         _dev_ptr(losses), _dev_ptr(S), ctypes.byref(mo), _stream_ptr(stream)))
     losses._hiper_ws = ws
+    return losses, S, mo.value
+
+
+def hiper_coltrast_loss_simulated(q_tokens, q_lens, d_tokens, d_lens, q_pooled, d_pooled_all, *,
+                                  world: int, rank: int, n_max: int, tau_li: float = 1.0,
+                                  tau_c: float = 0.05, flags: int = 0, want_scores: bool = False,
+                                  stream=None):
+    """N2 test support: hiper_coltrast_loss for rank `rank` of `world` simulated ranks on one GPU;
+    d_pooled_all [world][b][dp] holds every simulated rank's pooled passages."""
+    torch = _torch()
+    b, q_max_len, dim = q_tokens.shape
+    _, d_max_len, _ = d_tokens.shape
+    dp = d_pooled_all.shape[-1]
+    ql, dl = _host_i32(q_lens), _host_i32(d_lens)
+    m = min(n_max, world * b)
+    nb = lib().hiper_coltrast_loss_simulated_workspace_size(b, d_max_len, dim, dp, n_max, world)
+    ws, wp, wn = _workspace(nb, q_tokens.device)
+    _keep(ws, stream)
+    losses = torch.empty(3, dtype=torch.float32, device=q_tokens.device)
+    S = torch.empty((b, m), dtype=torch.float32, device=q_tokens.device) if want_scores else None
+    mo = ctypes.c_int32()
+    _check(lib().hiper_coltrast_loss_simulated(
+        _dev_ptr(q_tokens), _ptr(ql), q_max_len, _dev_ptr(d_tokens), _ptr(dl), d_max_len, dim,
+        _dev_ptr(q_pooled), _dev_ptr(d_pooled_all), dp, b, _dtype_code(q_tokens), flags, n_max,
+        float(tau_li), float(tau_c), world, rank, ctypes.c_void_p(wp), wn, _dev_ptr(losses),
+        _dev_ptr(S), ctypes.byref(mo), _stream_ptr(stream)))
     return losses, S, mo.value
 
 

@@ -27,6 +27,7 @@
 #include "kernels/maxsim_sm100_pair.cuh"
 #include "kernels/pooled_sm100_pair.cuh"
 #include "kernels/rerank_gather.cuh"
+#include "kernels/peer_gather.cuh"
 #include "kernels/norm_layout.cuh"
 #include "kernels/topk_merge.cuh"
 
@@ -1000,7 +1001,16 @@ static hiper_status launch_merge(const uint64_t* lists, int32_t n_lists, int64_t
 struct hiper_comm_s {
   ncclComm_t comm = nullptr;
   int32_t world = 1, rank = 0, device = 0;
+  // NEXT N2 peer windows (kernels/peer_gather.cuh): this rank's window [256 B ready word | 2 parity
+  // buffers of win_bytes] exported with CUDA IPC; peer[r] = rank r's window mapped here (peer[rank] =
+  // win).  Set up collectively on first use (peer_windows); epoch counts hiper_coltrast_loss calls.
+  size_t win_bytes = 0;
+  void* win = nullptr;
+  std::vector<void*> peer;
+  unsigned long long epoch = 0;
+  bool ipc_failed = false;
 };
+static constexpr size_t kWinHeader = 256;
 
 #define NCCL_TRY(expr)                                                                          \
   do {                                                                                          \
@@ -1066,8 +1076,69 @@ extern "C" hiper_status hiper_comm_create(const uint8_t id[128], int32_t world, 
   return HIPER_OK;
 }
 
+static void release_windows(hiper_comm_s* c) {
+  for (int32_t r = 0; r < (int32_t)c->peer.size(); ++r)
+    if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+  if (c->win) cudaFree(c->win);
+  c->peer.clear();
+  c->win = nullptr;
+  c->win_bytes = 0;
+}
+
+// Collective: every rank calls it with the same `bytes` (the same b, dp).  Allocates this rank's
+// window, all-gathers the IPC handles over the communicator, maps every peer's window.
+static hiper_status peer_windows(hiper_comm_s* c, size_t bytes, cudaStream_t stream) {
+  if (c->win_bytes >= bytes && c->win) return HIPER_OK;
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  release_windows(c);
+  CUDA_TRY(cudaMalloc(&c->win, kWinHeader + 2 * bytes));
+  CUDA_TRY(cudaMemset(c->win, 0, kWinHeader));  // ready epoch 0
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->win));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  uint8_t* dh = nullptr;
+  CUDA_TRY(cudaMalloc(&dh, 64 * (size_t)(c->world + 2)));
+  CUDA_TRY(cudaMemcpyAsync(dh, &h, 64, cudaMemcpyHostToDevice, stream));
+  NCCL_TRY(ncclAllGather(dh, dh + 64, 64, ncclUint8, c->comm, stream));
+  std::vector<cudaIpcMemHandle_t> all(c->world);
+  CUDA_TRY(cudaMemcpyAsync(all.data(), dh + 64, 64 * (size_t)c->world, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  TRY(nccl_async_check(c, "all-gather of IPC handles"));
+  c->peer.assign(c->world, nullptr);
+  for (int32_t r = 0; r < c->world; ++r) {
+    if (r == c->rank) {
+      c->peer[r] = c->win;
+      continue;
+    }
+    if (cudaIpcOpenMemHandle(&c->peer[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      c->peer[r] = nullptr;
+      c->ipc_failed = true;  // e.g. ranks on different nodes: the NCCL gather remains
+    }
+  }
+  // agree on success (every rank must take the same path) and make sure every rank has mapped every
+  // window before any rank signals into one
+  int32_t* flag = reinterpret_cast<int32_t*>(dh + 64 * (size_t)(c->world + 1));
+  const int32_t bad = c->ipc_failed ? 1 : 0;
+  CUDA_TRY(cudaMemcpyAsync(flag, &bad, 4, cudaMemcpyHostToDevice, stream));
+  NCCL_TRY(ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, c->comm, stream));
+  int32_t any_bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&any_bad, flag, 4, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  cudaFree(dh);
+  if (any_bad) {
+    c->ipc_failed = true;
+    release_windows(c);
+    return HIPER_OK;
+  }
+  c->win_bytes = bytes;
+  c->epoch = 0;
+  return HIPER_OK;
+}
+
 extern "C" hiper_status hiper_comm_destroy(hiper_comm* c) {
   if (!c) return HIPER_OK;
+  release_windows(c);
   ncclResult_t r = c->comm ? ncclCommDestroy(c->comm) : ncclSuccess;
   delete c;
   if (r != ncclSuccess) return fail(HIPER_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
@@ -1750,7 +1821,7 @@ struct FullLossWs {
   size_t li_bytes = 0;
 };
 static void full_loss_ws_layout(int32_t b, int32_t d_max_len, int32_t dim, int32_t dp, int32_t m,
-                                int32_t world, FullLossWs& w) {
+                                int32_t world, FullLossWs& w, int32_t n_ones = 0) {
   ColtrastWs cw;
   coltrast_ws_layout(b, b, d_max_len, dim, cw);
   size_t off = 0;
@@ -1758,7 +1829,7 @@ static void full_loss_ws_layout(int32_t b, int32_t d_max_len, int32_t dim, int32
   w.li_bytes = cw.total;
   off = align_up(off + cw.total, 1024);
   w.ones = off;
-  off = align_up(off + (size_t)std::max(b, 1) * 4, 1024);
+  off = align_up(off + (size_t)std::max(std::max(b, n_ones), 1) * 4, 1024);
   w.qp = off;
   off = align_up(off + (size_t)std::max(b, 1) * dp * 2, 1024);
   w.dp = off;
@@ -1783,15 +1854,21 @@ extern "C" size_t hiper_coltrast_loss_workspace_size(int32_t b, int32_t d_max_le
   return w.total;
 }
 
-extern "C" hiper_status hiper_coltrast_loss(
+static bool n2_force_nccl() {
+  static const bool f = getenv("HIPER_N2_NCCL") != nullptr;  // A/B: the NCCL all-gather path
+  return f;
+}
+
+// The full loss.  Exactly one of: comm (real ranks; the gather reads the peers' windows over NVLink,
+// or NCCL when IPC is unavailable), sim_world > 0 (test support: d_pooled holds every simulated rank's
+// passages [sim_world][b][dp] on this GPU and this call plays rank sim_rank), or neither (one rank).
+static hiper_status coltrast_loss_impl(
     const void* q_tokens, const int32_t* q_lens, int32_t q_max_len, const void* d_tokens,
     const int32_t* d_lens, int32_t d_max_len, int32_t dim, const void* q_pooled,
     const void* d_pooled, int32_t dp, int32_t b, hiper_dtype dtype, uint32_t flags, int32_t n_max,
-    float tau_li, float tau_c, const hiper_comm* comm, void* workspace, size_t workspace_bytes,
-    float* out_losses, float* out_scores_c, int32_t* out_m, hiper_stream_t stream_) {
-  g_launches = 0;
-  HiperRange nv("hiper_coltrast_loss");
-  cudaStream_t stream = (cudaStream_t)stream_;
+    float tau_li, float tau_c, hiper_comm_s* comm, int32_t sim_world, int32_t sim_rank,
+    void* workspace, size_t workspace_bytes, float* out_losses, float* out_scores_c, int32_t* out_m,
+    cudaStream_t stream) {
   if (b == 0) return fail(HIPER_ERR_EMPTY_BATCH, "empty batch");
   if (b < 0) return fail(HIPER_ERR_INVALID_ARG, "b < 0");
   if (n_max < b) return fail(HIPER_ERR_INVALID_ARG, "N (%d) < local batch (%d): positives must fit (SPEC NTooSmall)", n_max, b);
@@ -1802,11 +1879,15 @@ extern "C" hiper_status hiper_coltrast_loss(
       ((uintptr_t)q_pooled & 15) || ((uintptr_t)d_pooled & 15))
     return fail(HIPER_ERR_INVALID_ARG, "pooled inputs must be 16-B aligned device memory");
   if (!out_losses) return fail(HIPER_ERR_INVALID_ARG, "out_losses is NULL");
-  const int32_t world = comm ? comm->world : 1;
-  const int32_t rank = comm ? comm->rank : 0;
+  const bool sim = sim_world > 0;
+  if (sim && (sim_rank < 0 || sim_rank >= sim_world || sim_world > kMaxPeers))
+    return fail(HIPER_ERR_INVALID_ARG, "simulated rank %d of %d (<= %d)", sim_rank, sim_world, kMaxPeers);
+  const int32_t world = comm ? comm->world : (sim ? sim_world : 1);
+  const int32_t rank = comm ? comm->rank : (sim ? sim_rank : 0);
+  if (world > kMaxPeers) return fail(HIPER_ERR_UNSUPPORTED, "world %d > %d", world, kMaxPeers);
   const int32_t m = (int32_t)std::min<int64_t>(n_max, (int64_t)world * b);
   FullLossWs w;
-  full_loss_ws_layout(b, d_max_len, dim, dp, m, world, w);
+  full_loss_ws_layout(b, d_max_len, dim, dp, m, world, w, sim ? world * b : b);
   TRY(check_ws(workspace, workspace_bytes, w.total));
   uint8_t* ws = (uint8_t*)workspace;
   DevInfo di;
@@ -1814,40 +1895,62 @@ extern "C" hiper_status hiper_coltrast_loss(
   // L_LI on the local rank (writes out_losses[0])
   TRY(hiper_coltrast_scores_loss(q_tokens, q_lens, b, q_max_len, d_tokens, d_lens, b, d_max_len, dim,
                                  dtype, flags, nullptr, tau_li, ws + w.li, w.li_bytes, nullptr,
-                                 out_losses, stream_));
+                                 out_losses, (hiper_stream_t)stream));
   int32_t launches = g_launches;
   // pooled rows -> NORM'd bf16 (the length array is all ones: one row per item)
-  std::vector<int32_t> ones(b, 1);
+  const int32_t n_norm = sim ? world * b : b;  // simulated: every rank's passages
+  std::vector<int32_t> ones(n_norm, 1);
   int32_t* lens1 = (int32_t*)(ws + w.ones);
   __nv_bfloat16* qp = (__nv_bfloat16*)(ws + w.qp);
   __nv_bfloat16* dpp = (__nv_bfloat16*)(ws + w.dp);
   __nv_bfloat16* gathered = (__nv_bfloat16*)(ws + w.gathered);
   __nv_bfloat16* cand = (__nv_bfloat16*)(ws + w.cand);
   float* Sc = out_scores_c ? out_scores_c : (float*)(ws + w.sc);
-  TRY(stage_h2d(lens1, ones.data(), (size_t)b * 4, stream));
+  TRY(stage_h2d(lens1, ones.data(), (size_t)n_norm * 4, stream));
   uint32_t* status = (uint32_t*)(ws + w.li);  // the L_LI workspace's status word (same stream order)
   g_launches = 0;
   TRY(launch_norm(q_pooled, dtype, b, 1, lens1, b, 1, dp, flags, qp, status, stream));
-  TRY(launch_norm(d_pooled, dtype, b, 1, lens1, b, 1, dp, flags, dpp, status, stream));
-  launches += g_launches;
-  // gather: local positives first, then the other ranks in (rank, position) order, m rows
-  const size_t row_bytes = (size_t)dp * 2;
-  if (world > 1) {
+  // candidates: local positives first, then the other ranks in (rank, position) order, m rows
+  if (comm && world > 1 && !n2_force_nccl() && !comm->ipc_failed)
+    TRY(peer_windows(comm, (size_t)b * dp * 2, stream));
+  const bool windows = comm && world > 1 && !n2_force_nccl() && comm->win != nullptr;
+  PeerGatherArgs ga{};
+  ga.world = world;
+  ga.rank = rank;
+  ga.b = b;
+  ga.dp = dp;
+  ga.m = m;
+  ga.cand = cand;
+  if (windows) {
+    // NORM straight into this rank's window of this epoch, publish it, read every peer's over NVLink
+    const unsigned long long epoch = ++comm->epoch;
+    const size_t par = kWinHeader + (size_t)(epoch & 1ull) * comm->win_bytes;
+    TRY(launch_norm(d_pooled, dtype, b, 1, lens1, b, 1, dp, flags,
+                    (__nv_bfloat16*)((uint8_t*)comm->win + par), status, stream));
+    peer_signal_kernel<<<1, 1, 0, stream>>>((unsigned long long*)comm->win, epoch);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    for (int32_t r = 0; r < world; ++r) {
+      ga.src[r] = (const __nv_bfloat16*)((const uint8_t*)comm->peer[r] + par);
+      ga.ready[r] = r == rank ? nullptr : (const unsigned long long*)comm->peer[r];
+    }
+    ga.epoch = epoch;
+  } else if (sim) {
+    TRY(launch_norm(d_pooled, dtype, n_norm, 1, lens1, n_norm, 1, dp, flags, gathered, status, stream));
+    for (int32_t r = 0; r < world; ++r) ga.src[r] = gathered + (size_t)r * b * dp;
+  } else if (world > 1) {  // NCCL: all-gather of every rank's NORM'd passages, then the same ordering
+    TRY(launch_norm(d_pooled, dtype, b, 1, lens1, b, 1, dp, flags, dpp, status, stream));
     NCCL_TRY(ncclAllGather(dpp, gathered, (size_t)b * dp, ncclBfloat16, comm->comm, stream));
     TRY(nccl_async_check(comm, "ncclAllGather of pooled passages"));
-    CUDA_TRY(cudaMemcpyAsync(cand, gathered + (size_t)rank * b * dp, (size_t)b * row_bytes,
-                             cudaMemcpyDeviceToDevice, stream));
-    int64_t filled = b;
-    for (int32_t j = 0; j < world && filled < m; ++j) {
-      if (j == rank) continue;
-      const int64_t take = std::min<int64_t>(b, m - filled);
-      CUDA_TRY(cudaMemcpyAsync(cand + filled * dp, gathered + (size_t)j * b * dp, take * row_bytes,
-                               cudaMemcpyDeviceToDevice, stream));
-      filled += take;
-    }
+    for (int32_t r = 0; r < world; ++r) ga.src[r] = gathered + (size_t)r * b * dp;
   } else {
-    CUDA_TRY(cudaMemcpyAsync(cand, dpp, (size_t)b * row_bytes, cudaMemcpyDeviceToDevice, stream));
+    TRY(launch_norm(d_pooled, dtype, b, 1, lens1, b, 1, dp, flags, dpp, status, stream));
+    ga.src[0] = dpp;
   }
+  peer_gather_kernel<<<(unsigned)m, 128, 0, stream>>>(ga);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  launches += g_launches;
   if (flags & HIPER_VALIDATE_SYNC) TRY(sync_status(status, stream));
   // L_C scores [b][m] and loss (writes out_losses[1] and out_losses[2] = (L_LI + L_C) / 2)
   g_launches = 0;
@@ -1856,6 +1959,46 @@ extern "C" hiper_status hiper_coltrast_loss(
   g_launches += launches;
   if (out_m) *out_m = m;
   return HIPER_OK;
+}
+
+extern "C" hiper_status hiper_coltrast_loss(
+    const void* q_tokens, const int32_t* q_lens, int32_t q_max_len, const void* d_tokens,
+    const int32_t* d_lens, int32_t d_max_len, int32_t dim, const void* q_pooled,
+    const void* d_pooled, int32_t dp, int32_t b, hiper_dtype dtype, uint32_t flags, int32_t n_max,
+    float tau_li, float tau_c, const hiper_comm* comm, void* workspace, size_t workspace_bytes,
+    float* out_losses, float* out_scores_c, int32_t* out_m, hiper_stream_t stream_) {
+  g_launches = 0;
+  HiperRange nv("hiper_coltrast_loss");
+  return coltrast_loss_impl(q_tokens, q_lens, q_max_len, d_tokens, d_lens, d_max_len, dim, q_pooled,
+                            d_pooled, dp, b, dtype, flags, n_max, tau_li, tau_c,
+                            const_cast<hiper_comm_s*>(comm), 0, 0, workspace, workspace_bytes,
+                            out_losses, out_scores_c, out_m, (cudaStream_t)stream_);
+}
+
+extern "C" size_t hiper_coltrast_loss_simulated_workspace_size(int32_t b, int32_t d_max_len,
+                                                               int32_t dim, int32_t dp, int32_t n_max,
+                                                               int32_t world) {
+  if (b < 0 || dim <= 0 || dp <= 0 || world < 1) return 0;
+  const int32_t m = (int32_t)std::min<int64_t>(std::max(n_max, 0), (int64_t)world * b);
+  FullLossWs w;
+  full_loss_ws_layout(b, d_max_len, dim, dp, m, world, w, world * b);
+  return w.total;
+}
+
+extern "C" hiper_status hiper_coltrast_loss_simulated(
+    const void* q_tokens, const int32_t* q_lens, int32_t q_max_len, const void* d_tokens,
+    const int32_t* d_lens, int32_t d_max_len, int32_t dim, const void* q_pooled,
+    const void* d_pooled_all, int32_t dp, int32_t b, hiper_dtype dtype, uint32_t flags,
+    int32_t n_max, float tau_li, float tau_c, int32_t world, int32_t rank, void* workspace,
+    size_t workspace_bytes, float* out_losses, float* out_scores_c, int32_t* out_m,
+    hiper_stream_t stream_) {
+  g_launches = 0;
+  HiperRange nv("hiper_coltrast_loss_simulated");
+  if (world < 1) return fail(HIPER_ERR_INVALID_ARG, "world < 1");
+  return coltrast_loss_impl(q_tokens, q_lens, q_max_len, d_tokens, d_lens, d_max_len, dim, q_pooled,
+                            d_pooled_all, dp, b, dtype, flags, n_max, tau_li, tau_c, nullptr, world,
+                            rank, workspace, workspace_bytes, out_losses, out_scores_c, out_m,
+                            (cudaStream_t)stream_);
 }
 
 

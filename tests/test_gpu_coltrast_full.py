@@ -67,3 +67,33 @@ def test_full_coltrast_errors(H):
         H.hiper_coltrast_loss(to_dev(z), np.ones(b), to_dev(z), np.ones(b), to_dev(zp), to_dev(zp),
                               n_max=8, tau_c=0.0)
     assert e.value.name == "HIPER_ERR_BAD_TEMPERATURE"
+
+
+@pytest.mark.parametrize("world,b,dp,n_max", [(3, 24, 768, 72), (3, 24, 768, 29), (4, 17, 80, 40),
+                                              (2, 33, 4096, 66), (5, 8, 768, 8)])
+def test_full_coltrast_loss_simulated_ranks(H, world, b, dp, n_max):
+    """N2 with `world` simulated ranks on ONE GPU: every rank's pooled passages live in one buffer and
+    the library's candidate gather (the kernel that reads the peers' windows over NVLink on a real
+    node) builds each rank's min(N, W) candidates in (local first, then rank, position) order; the
+    losses equal the oracle's (SPEC.md:321-329 gather_candidates)."""
+    L, Lq = 64, 32
+    pools = [gen.corpus(50 + r, 0, b, 1, dp)[:, 0] for r in range(world)]
+    allp = np.stack(pools)                                           # [world][b][dp]
+    for rank in range(world):
+        d = gen.corpus(30 + rank, 0, b, L, 128)
+        q = gen.queries(40 + rank, b, Lq, 128, corpus_seed=30 + rank, n_chunks=b, L=L,
+                        diagonal=True, sigma_q=gen.SIGMA_Q_HARD)
+        dl = gen.lengths(30 + rank, b, L, True)
+        ql = gen.lengths(40 + rank, b, Lq, True, stream=gen.QLEN)
+        qpool = gen.queries(60 + rank, b, 1, dp, corpus_seed=50 + rank, n_chunks=b, L=1,
+                            diagonal=True, sigma_q=np.float32(4.0))[:, 0]
+        losses, S, m = H.hiper_coltrast_loss_simulated(
+            to_dev(q), ql, to_dev(d), dl, to_dev(qpool), to_dev(allp), world=world, rank=rank,
+            n_max=n_max, tau_li=1.0, tau_c=0.05, want_scores=True)
+        cands = np.stack(oracle.gather_candidates([list(p) for p in pools], rank, n_max))
+        assert m == len(cands) == min(n_max, world * b)
+        L_li, L_c, L_tot, S_c = oracle_full(q, ql, d, dl, qpool, cands, 1.0, 0.05)
+        got = losses.cpu().numpy().astype(np.float64)
+        for g, o, name in zip(got, (L_li, L_c, L_tot), ("L_LI", "L_C", "L")):
+            assert abs(g - o) <= max(1e-4 * abs(o), 1e-7), (rank, name, g, o)
+        assert np.all(np.abs(S.cpu().numpy() - S_c) <= np.maximum(2e-3 * np.abs(S_c), dp * 2.0 ** -24))
