@@ -25,7 +25,6 @@
 #include "kernels/infonce.cuh"
 #include "kernels/maxsim_backward.cuh"
 #include "kernels/maxsim_sm100_pair.cuh"
-#include "kernels/maxsim_sm100_ts.cuh"
 #include "kernels/pooled_sm100_pair.cuh"
 #include "kernels/rerank_gather.cuh"
 #include "kernels/peer_gather.cuh"
@@ -939,68 +938,6 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
   return HIPER_OK;
 }
 
-// The TS kernel (A resident in TMEM, 7 accumulator slots; kernels/maxsim_sm100_ts.cuh) for the
-// production shape.  HIPER_MAXSIM_TS=0/1 overrides the default.
-static bool ts_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("HIPER_MAXSIM_TS");
-    return e ? e[0] == '1' : false;
-  }();
-  return on;
-}
-template <int MODE, int KR>
-static hiper_status launch_maxsim_ts(const KernelPlan& kp, const CUtensorMap& tq, const CUtensorMap& td,
-                                     const MaxsimArgs& a, cudaStream_t stream) {
-  ProfTicket ev;
-  static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
-  static const bool n128 = getenv("HIPER_TS_N128") != nullptr;  // experiment: 3 slots of 128
-  auto kern = stats_on ? (n128 ? maxsim_ts_kernel<MODE, KR, true, 128> : maxsim_ts_kernel<MODE, KR, true, 64>)
-                       : (n128 ? maxsim_ts_kernel<MODE, KR, false, 128> : maxsim_ts_kernel<MODE, KR, false, 64>);
-  CUDA_TRY(set_max_smem((const void*)kern, (int)kp.smem_bytes));
-  unsigned long long* st = nullptr;
-  MaxsimArgs b = a;
-  if (stats_on) {
-    CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
-    CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));
-    b.stats = st;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)kp.grid);
-  cfg.blockDim = dim3(kMaxsimThreads);
-  cfg.dynamicSmemBytes = kp.smem_bytes;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  TRY(profile_begin(stream, HIPER_PROF_MAXSIM, &ev));
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq, td, b));
-  CUDA_TRY(cudaGetLastError());
-  TRY(profile_end(stream, ev));
-  ++g_launches;
-  if (st) {
-    unsigned long long h[8];
-    CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, stream));
-    CUDA_TRY(cudaStreamSynchronize(stream));
-    cudaFree(st);
-    const double pairs = kp.grid / 2.0, ep = 8.0 * kp.grid;
-    fprintf(stderr, "[hiper pipe] maxsim TS: MMA thread %.0f cyc avg; waits slot %.1f%% full %.1f%%, "
-            "issue %.1f%%; epilogue drain %.0f cyc/slot, wait %.0f cyc/slot, slots/warp %.0f\n",
-            h[2] / pairs, 100.0 * h[0] / h[2], 100.0 * h[1] / h[2], 100.0 * h[6] / h[2],
-            (double)h[3] / h[5], (double)h[4] / h[5], h[5] / ep);
-  }
-  return HIPER_OK;
-}
-static bool ts_shape(const KernelPlan& kp, const MaxsimArgs& a, int mode) {
-  return (mode == 0 || mode == 1) && a.recs == nullptr && kp.qw == 1 && kp.h == 1 && a.ld_pad == 256 &&
-         a.num_kb == 2 && kp.a_bufs == 2 && ts_enabled();
-}
-
 // MODE 0 dense scores, 1 top-k (KR = ceil(k / 32) register ranks per lane), 2 scores + argmax;
 // packed (a.recs) or dense; QW = kp.qw warps per query; H = kp.h MMA halves per chunk.
 template <int MODE, int KR, bool PACKED>
@@ -1026,12 +963,6 @@ static hiper_status launch_maxsim_qh(const KernelPlan& kp, const CUtensorMap& tq
 static hiper_status launch_maxsim(int mode, int k, const KernelPlan& kp, const CUtensorMap& tq,
                                   const CUtensorMap& td, const MaxsimArgs& a, cudaStream_t stream) {
   if (kp.grid == 0) return HIPER_OK;
-  if (ts_shape(kp, a, mode)) {
-    if (mode == 0) return launch_maxsim_ts<0, 1>(kp, tq, td, a, stream);
-    if (k <= 32) return launch_maxsim_ts<1, 1>(kp, tq, td, a, stream);
-    if (k <= 64) return launch_maxsim_ts<1, 2>(kp, tq, td, a, stream);
-    return launch_maxsim_ts<1, 4>(kp, tq, td, a, stream);
-  }
   if (mode == 2) {
     if (a.recs != nullptr || kp.qw != 1 || kp.h != 1)
       return fail(HIPER_ERR_UNSUPPORTED, "argmax capture needs a dense layout, q_max_len <= 32, d_max_len <= 256");

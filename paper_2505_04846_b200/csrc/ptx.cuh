@@ -268,22 +268,6 @@ __device__ __forceinline__ void mma_bf16_ss_pair(uint32_t d_tmem, uint64_t adesc
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// D[tmem of both CTAs] (+)= A[tmem of both CTAs] * B[smem of both CTAs]^T (A resident in tensor
-// memory: row = lane, K packed two bf16 per 32-bit column), M = 256 across the pair.
-__device__ __forceinline__ void mma_bf16_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
-                                                 uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Shared memory -> tensor memory copy of a 128-row x 256-bit slab (one K = 16 bf16 step of a K-major
-// operand tile described by `sdesc`) into both CTAs' TMEM (each from its own shared memory).
-__device__ __forceinline__ void tmem_cp_128x256b_pair(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
-}
 // Arrive once on the barrier at the same smem offset in every CTA of `cta_mask` when all prior
 // tcgen05.mma of this thread completed.
 __device__ __forceinline__ void mma_commit_pair_mc(uint32_t bar, uint16_t cta_mask) {
