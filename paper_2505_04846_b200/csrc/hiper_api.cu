@@ -752,14 +752,25 @@ static hiper_status plan_kernel(const DevInfo& di, int32_t n_q, int32_t q_max_le
   // one stage = this CTA's rows of one chunk (half): ld_pad / 2, or 128 of a 256-row half
   kp.box_rows = kp.h == 2 ? 128u : (uint32_t)slot_rows / 2;
   kp.stage_bytes = kp.box_rows * 128u * nkb;
-  // A double-buffered across units when two stages still fit, else single-buffered (large dims)
-  for (kp.a_bufs = 2; kp.a_bufs >= 1; --kp.a_bufs) {
-    const uint32_t fixed = 1024u /*align slack*/ + kp.a_bufs * kp.a_bytes + 2048u /*barriers, ring, sums*/;
+  // The A tile is double-buffered across units unless one buffer buys an extra B stage on long
+  // units: a unit boundary then costs one A load (~1 us), while the extra stage hides L2 latency and
+  // lockstep pauses on every chunk (config3, same box: 5 -> 6 stages, 633 -> 646 q/s,
+  // profiles/r02/ablation/one_a_buffer.txt).  Large dims fall back to one buffer anyway.
+  auto stages_for = [&](int32_t bufs, uint32_t& smem) {
+    const uint32_t fixed = 1024u /*align slack*/ + bufs * kp.a_bytes + 2048u /*barriers, ring, sums*/;
     const uint32_t avail = (uint32_t)di.max_smem > fixed ? (uint32_t)di.max_smem - fixed : 0u;
-    kp.n_stages = (int32_t)std::min<uint32_t>(12u, avail / kp.stage_bytes);
-    kp.smem_bytes = fixed + kp.n_stages * kp.stage_bytes;
-    if (kp.n_stages >= 2) break;
-  }
+    const int32_t st = (int32_t)std::min<uint32_t>(12u, avail / kp.stage_bytes);
+    smem = fixed + (uint32_t)st * kp.stage_bytes;
+    return st;
+  };
+  uint32_t smem1 = 0, smem2 = 0;
+  const int32_t st1 = stages_for(1, smem1), st2 = stages_for(2, smem2);
+  const bool long_units = kp.n_parts > 0 && n_slots / kp.n_parts >= 64;
+  static const char* force = getenv("HIPER_A_BUFS");  // ablation: force 1 or 2
+  const bool one = force ? force[0] == '1' : (st2 < 2 || (long_units && st1 > st2));
+  kp.a_bufs = one ? 1 : 2;
+  kp.n_stages = one ? st1 : st2;
+  kp.smem_bytes = one ? smem1 : smem2;
   if (kp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory for 2 stages");
   const int64_t units = (int64_t)kp.n_groups * kp.n_parts;
   kp.grid = (int)std::min<int64_t>(units, slots) * 2;
