@@ -36,6 +36,7 @@ def widen(a):
     (32, 48, 32, 96, 128, "f32", 1.0, "planted"),
     (16, 40, 20, 64, 64, "bf16", 0.1, "iid"),
     (37, 37, 32, 128, 128, "bf16", 0.5, "planted"),
+    (64, 80, 32, 256, 128, "bf16", 1.0, "planted"),   # 8 query tiles x full-length docs (streamed paths)
 ])
 def test_li_backward_matches_oracle(H, n_q, n_d, Lq, Ld, d, dtype, tau, kind):
     corp = gen.corpus(71, 0, n_d, Ld, d, kind=kind, dtype=dtype)
