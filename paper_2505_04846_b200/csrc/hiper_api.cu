@@ -2015,9 +2015,10 @@ extern "C" hiper_status hiper_coltrast_loss_simulated(
 
 // ============================================================================ N1: L_LI backward
 struct GradWs {
-  size_t base = 0, amax = 0, G = 0, sorted = 0, bucket = 0, total = 0;
+  size_t base = 0, amax = 0, G = 0, sorted = 0, bucket = 0, qpart = 0, total = 0;
   ColtrastWs cw;
 };
+static constexpr int32_t kGqRangesMax = 8;  // chunk ranges of the streamed grad_q (partials)
 static void grad_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim, GradWs& w) {
   coltrast_ws_layout(n_q, n_d, d_max_len, dim, w.cw);
   size_t off = align_up(w.cw.total, 1024);
@@ -2029,6 +2030,8 @@ static void grad_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t 
   off = align_up(off + (size_t)std::max(n_q, 1) * 32 * std::max(n_d, 1) * 2, 1024);
   w.bucket = off;
   off = align_up(off + (size_t)std::max(n_d, 1) * 258 * 4, 1024);
+  w.qpart = off;  // [R][n_q * 32][dim] fp32 partial sums of grad_q
+  off = align_up(off + (size_t)kGqRangesMax * std::max(n_q, 1) * 32 * dim * 4, 1024);
   w.total = off;
 }
 
@@ -2101,18 +2104,32 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   const int64_t qrows = (int64_t)n_q * q_max_len;
   const unsigned qblocks = (unsigned)((qrows + 7) / 8);
   const size_t dsmem = (size_t)n_q * 32 * 3 + (size_t)n_q * 8 + 2 * 8 * 257 * 4;
+  // grad_q: chunk tiles streamed through shared memory per 8 queries (partials over R chunk ranges)
+  const int32_t qblk = (n_q + kGqWarps - 1) / kGqWarps;
+  const int32_t R = std::max(1, std::min({kGqRangesMax, n_d, di.num_sms / std::max(qblk, 1)}));
+  alignas(64) CUtensorMap tdg;  // doc rows as 64-dim x ld_pad boxes
+  TRY(make_tmap(&tdg, dlayout, (int64_t)n_d * ld_pad, dim, ld_pad));
+  float* qpart = (float*)(ws + w.qpart);
   auto launch_grads = [&](auto vpl, auto tin) -> hiper_status {
     constexpr int VPL = decltype(vpl)::value;
     using Tin = decltype(tin);
-    grad_q_kernel<VPL, Tin><<<qblocks, 256, 0, stream>>>(G, amax, n_q, n_d, dlayout, ld_pad,
-                                                         (const Tin*)q_tokens, q_max_len, qlens_dev,
-                                                         an, grad_q);
+    auto gqs = grad_q_stream_kernel<VPL / 2>;
+    const int gsm = 1024 + 2 * ld_pad * 128 * (VPL / 2) + 64;
+    CUDA_TRY(set_max_smem((const void*)gqs, gsm));
+    gqs<<<(unsigned)(qblk * R), (kGqWarps + 1) * 32, gsm, stream>>>(tdg, G, amax, n_q, n_d, ld_pad,
+                                                                    qlens_dev, R, qpart);
     CUDA_TRY(cudaGetLastError());
+    grad_q_reduce_kernel<VPL, Tin><<<qblocks, 256, 0, stream>>>(qpart, R, n_q, (const Tin*)q_tokens,
+                                                                q_max_len, qlens_dev, an, grad_q);
+    CUDA_TRY(cudaGetLastError());
+    g_launches += 1;
+    // grad_d: sort-only pass (one block per doc), then one warp per output row for the gathers.
+    // (A per-doc CTA streaming the query rows through shared memory was 2.2x slower: a few hub doc
+    // rows take most argmax hits and serialise their threads -- profiles/r02/ablation/grad.txt.)
     auto gk = grad_d_kernel<VPL, Tin>;
     CUDA_TRY(set_max_smem((const void*)gk, (int)dsmem));
     uint16_t* srt = (uint16_t*)(ws + w.sorted);
     int32_t* bkt = (int32_t*)(ws + w.bucket);
-    // sort-only pass (one block per doc), then one warp per output row for the gathers
     gk<<<(unsigned)n_d, 256, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
                                               (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d,
                                               srt, bkt);

@@ -3,15 +3,18 @@
 // Chain rule (the objective is trained by backpropagation):
 //   G_ij          = (softmax_j(S_i / tau)_j - [j == pos_i]) / (B tau)            infonce_grad_kernel
 //   a(i,t,j)      = argmax_{u < len_j} <qn_{i,t}, dn_{j,u}>  (saved by the forward, MODE 2)
-//   g_q(i,t)      = sum_j G_ij dn_{j, a(i,t,j)}                                   grad_q_kernel
+//   g_q(i,t)      = sum_j G_ij dn_{j, a(i,t,j)}                  grad_q_stream_kernel + _reduce
 //   g_d(j,u)      = sum_i sum_{t: a(i,t,j) = u} G_ij qn_{i,t}                      grad_d_kernel
 //   dL/dx (row)   = inv (g - y (y . g)),  y = x inv, inv = 1 / ||x||   (NORM's Jacobian; skipped
 //                   with HIPER_ASSUME_NORMALIZED)
 // qn / dn are the bf16 NORM'd operands of the forward (the kernels' layouts); the Jacobian uses the
 // fp32 y = x * inv of the raw row.  All sums run in a fixed order (deterministic, no atomics).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+
+#include "../ptx.cuh"
 
 namespace hiper {
 
@@ -75,15 +78,96 @@ __device__ __forceinline__ void norm_backward_row(const Tin* xrow, const float (
   for (int v = 0; v < VPL; ++v) out[lane * VPL + v] = inv * (g[v] - x[v] * inv * yg);
 }
 
-// One warp per (query i, query token t); lanes own VPL = dim/32 consecutive dims.
+// grad_q by streaming: a CTA owns 8 queries (its 8 consumer warps; lane = query token t) and a range of
+// chunks; a producer warp TMA-loads each chunk's NORM'd rows (64-dim x ld_pad boxes, 128B swizzle)
+// into a 2-stage ring, and every thread adds G_ij * dn_{j, a(i,t,j)} for its own argmax row straight
+// from shared memory into 64 * NKB fp32 registers.  Each chunk tile is read from L2 once per 8 queries
+// (by TMA) instead of 256 rows gathered per (query, chunk) warp; the swizzle spreads the 32 lanes'
+// random rows over the 8 16-byte bank groups.  Partial sums per chunk range go to `part`
+// [R][n_q * 32][D]; grad_q_reduce_kernel adds them in range order (deterministic) and applies NORM's
+// Jacobian.
+constexpr int kGqWarps = 8;
+template <int NKB>
+__global__ void __launch_bounds__((kGqWarps + 1) * 32, 1)
+    grad_q_stream_kernel(const __grid_constant__ CUtensorMap tmap_d, const float* __restrict__ G,
+                         const uint8_t* __restrict__ amax, int32_t B, int32_t M, int32_t ld_pad,
+                         const int32_t* __restrict__ q_lens, int32_t R, float* __restrict__ part) {
+  constexpr int D = 64 * NKB;
+  extern __shared__ uint8_t smem_raw[];
+  using namespace ptx;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t kb_bytes = (uint32_t)ld_pad * 128u;
+  const uint32_t stage_bytes = kb_bytes * NKB;
+  const uint32_t bars = base + 2u * stage_bytes;  // full[2], empty[2]
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bars + 8u * s, 1);
+      mbar_init(bars + 16u + 8u * s, kGqWarps);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+  const int32_t qb = blockIdx.x / R, r = blockIdx.x % R;
+  const int32_t j0 = (int32_t)((int64_t)r * M / R), j1 = (int32_t)((int64_t)(r + 1) * M / R);
+  if (warp == kGqWarps) {  // producer
+    if (lane == 0) {
+      prefetch_tmap(&tmap_d);
+      for (int32_t j = j0; j < j1; ++j) {
+        const uint32_t s = (uint32_t)(j - j0) & 1u, ph = ((uint32_t)(j - j0) >> 1) & 1u;
+        mbar_wait(bars + 16u + 8u * s, ph ^ 1u);
+        mbar_arrive_expect_tx(bars + 8u * s, stage_bytes);
+#pragma unroll
+        for (int kb = 0; kb < NKB; ++kb)
+          tma_load_2d(base + s * stage_bytes + kb * kb_bytes, &tmap_d, bars + 8u * s, kb * 64, j * ld_pad);
+      }
+    }
+    return;
+  }
+  const int32_t i = qb * kGqWarps + (int32_t)warp;
+  const int32_t t = (int32_t)lane;
+  const bool valid = i < B && t < q_lens[i < B ? i : 0];
+  float acc[D];
+#pragma unroll
+  for (int v = 0; v < D; ++v) acc[v] = 0.0f;
+  for (int32_t j = j0; j < j1; ++j) {
+    const uint32_t s = (uint32_t)(j - j0) & 1u, ph = ((uint32_t)(j - j0) >> 1) & 1u;
+    const float g = i < B ? __ldg(G + (int64_t)i * M + j) : 0.0f;
+    const uint32_t u = i < B ? __ldg(amax + ((int64_t)i * M + j) * 32 + t) : 0u;
+    mbar_wait(bars + 8u * s, ph);
+    if (valid) {
+      const uint32_t row = base + s * stage_bytes + u * 128u;
+#pragma unroll
+      for (int c = 0; c < 8 * NKB; ++c) {
+        const uint32_t addr = row + (uint32_t)(c >> 3) * kb_bytes + ((((uint32_t)c & 7u) ^ (u & 7u)) << 4);
+        uint32_t w0, w1, w2, w3;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(addr));
+        const uint32_t w[4] = {w0, w1, w2, w3};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc[c * 8 + 2 * e] = fmaf(g, __uint_as_float(w[e] << 16), acc[c * 8 + 2 * e]);
+          acc[c * 8 + 2 * e + 1] = fmaf(g, __uint_as_float(w[e] & 0xFFFF0000u), acc[c * 8 + 2 * e + 1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bars + 16u + 8u * s);
+  }
+  if (i < B) {
+    float4* dst = reinterpret_cast<float4*>(part + (((int64_t)r * B + i) * 32 + t) * D);
+#pragma unroll
+    for (int v = 0; v < D / 4; ++v) dst[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+  }
+}
+
+// One warp per (query i, token t): sum the R partial rows in range order, NORM's Jacobian.
 template <int VPL, typename Tin>
-__global__ void __launch_bounds__(256) grad_q_kernel(const float* __restrict__ G,
-                                                     const uint8_t* __restrict__ amax, int32_t B,
-                                                     int32_t M, const __nv_bfloat16* __restrict__ dlay,
-                                                     int32_t ld_pad, const Tin* __restrict__ xq,
-                                                     int32_t q_max_len, const int32_t* __restrict__ q_lens,
-                                                     uint32_t assume_normalized,
-                                                     float* __restrict__ grad_q) {
+__global__ void __launch_bounds__(256) grad_q_reduce_kernel(const float* __restrict__ part, int32_t R,
+                                                            int32_t B, const Tin* __restrict__ xq,
+                                                            int32_t q_max_len,
+                                                            const int32_t* __restrict__ q_lens,
+                                                            uint32_t assume_normalized,
+                                                            float* __restrict__ grad_q) {
   constexpr int D = VPL * 32;
   const uint32_t lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -98,13 +182,10 @@ __global__ void __launch_bounds__(256) grad_q_kernel(const float* __restrict__ G
   float g[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) g[v] = 0.0f;
-#pragma unroll 8
-  for (int32_t j = 0; j < M; ++j) {
-    const float gij = G[(int64_t)i * M + j];
-    const int32_t u = amax[((int64_t)i * M + j) * 32 + t];
-    const __nv_bfloat16* dr = dlay + ((int64_t)j * ld_pad + u) * D + lane * VPL;
+  for (int32_t r = 0; r < R; ++r) {
+    const float* pr = part + (((int64_t)r * B + i) * 32 + t) * D + lane * VPL;
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) g[v] = fmaf(gij, __bfloat162float(dr[v]), g[v]);
+    for (int v = 0; v < VPL; ++v) g[v] += pr[v];
   }
   norm_backward_row<VPL, Tin>(xq + row * D, g, assume_normalized != 0, out, lane);
 }

@@ -51,4 +51,10 @@ if has ncu; then
   timeout 300 $P > gpurun_out/plain_p.log 2>&1 && \
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:pooled -s 1 -c 1 -o gpurun_out/prof_pooled $P > gpurun_out/ncu_pooled.log 2>&1
 fi
+# keep gpurun_out under gpurun's 64 MiB copy-back limit: summarise the captures here, keep only the
+# MaxSim report
+for r in gpurun_out/prof_*.ncu-rep; do
+  [ -f "$r" ] && python tools/ncu_summary.py "$r" 30 > "${r%.ncu-rep}_summary.txt" 2>&1
+done
+rm -f gpurun_out/prof_packed.ncu-rep gpurun_out/prof_pooled.ncu-rep
 echo evidence_done
