@@ -21,7 +21,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhiper.so")
+# HIPER_LIB=debug loads the build with device-side checks (libhiper_debug.so; tests/test_gpu_debug_build.py)
+LIB_PATH = os.path.join(_HERE, "libhiper_debug.so" if os.environ.get("HIPER_LIB") == "debug"
+                        else "libhiper.so")
 
 HIPER_F32, HIPER_BF16 = 0, 1
 HIPER_ASSUME_NORMALIZED = 1

@@ -43,15 +43,17 @@ def _run(cmd):
     return r.stdout + r.stderr
 
 
-def build_hiper(force=False, verbose=False) -> str:
-    out = os.path.join(PKG, "libhiper.so")
+def build_hiper(force=False, verbose=False, debug=False) -> str:
+    """libhiper.so; debug=True: libhiper_debug.so with the device-side checks (HIPER_DASSERT)."""
+    out = os.path.join(PKG, "libhiper_debug.so" if debug else "libhiper.so")
     srcs = (glob.glob(os.path.join(PKG, "csrc", "**", "*.cu*"), recursive=True)
             + [os.path.join(ROOT, "include", "hiper.h")])
     if force or _stale(out, srcs):
         inc, lib = nccl_dirs()
         tmp = out + f".tmp{os.getpid()}"
         cmd = [NVCC, *ARCH, *COMMON, "-I", os.path.join(ROOT, "include"), "-I", inc,
-               "-DHIPER_BUILD", os.path.join(PKG, "csrc", "hiper_api.cu"), "-o", tmp,
+               "-DHIPER_BUILD", *(["-DHIPER_DEVICE_ASSERTS"] if debug else []),
+               os.path.join(PKG, "csrc", "hiper_api.cu"), "-o", tmp,
                "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
@@ -73,7 +75,12 @@ def build_synth(force=False) -> str:
 
 
 def build_all(force=False, verbose=False):
-    return build_hiper(force, verbose), build_synth(force)
+    """The product library, its device-assert twin and the generator, compiled concurrently."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(3) as ex:
+        jobs = [ex.submit(build_hiper, force, verbose), ex.submit(build_hiper, force, False, True),
+                ex.submit(build_synth, force)]
+        return tuple(j.result() for j in jobs)
 
 
 if __name__ == "__main__":

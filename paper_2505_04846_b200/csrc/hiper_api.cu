@@ -2286,6 +2286,7 @@ extern "C" hiper_status hiper_two_stage_topk(const hiper_index* pix, const hiper
     ra.dim = tix->dim;
     ra.k1 = k1;
     ra.n_items = n_items;
+    ra.n_index = tix->n;
     ra.S2 = S2;
     auto kern = num_kb_of(tix->dim) == 1 ? rerank_gather_kernel<1, 6> : rerank_gather_kernel<2, 3>;
     const int smem = 1024 + kRerankWarps * (num_kb_of(tix->dim) == 1 ? 6 : 3) * 64 * 128 * num_kb_of(tix->dim) + 256;

@@ -399,6 +399,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           const uint32_t gl = (lane >> 1) & 15u;
           const bool speaker = ((starts >> gl) & 1u) != 0u && (lane & 1u) == 0u;
           const int32_t chunk_l = (int32_t)__shfl_sync(0xffffffffu, rec, 16 + __popc(gstart & ((1u << gl) - 1u)));
+          if (speaker)
+            HIPER_DASSERT(chunk_l >= 0 && (MODE != 0 || chunk_l < args.score_ld), chunk_l, args.score_ld);
           if constexpr (MODE == 0) {
             if (speaker && q < args.n_q) args.scores[(int64_t)q * args.score_ld + chunk_l] = sv;
           } else {
@@ -473,6 +475,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       }
       }  // !PACKED
       if constexpr (MODE == 1) {
+        HIPER_DASSERT(q < args.q_pad && p < args.n_parts, q, p);
         if (part == 0) {  // partial lists: [P][kEpiGroups][q_pad][k]
           uint64_t* dst = args.partial + (((int64_t)p * kEpiGroups + grp) * args.q_pad + q) * args.k;
 #pragma unroll

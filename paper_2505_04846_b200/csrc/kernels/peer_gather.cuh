@@ -17,6 +17,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "../ptx.cuh"
+
 namespace hiper {
 
 constexpr int kMaxPeers = 64;
@@ -51,6 +53,7 @@ __global__ void __launch_bounds__(128) peer_gather_kernel(const PeerGatherArgs a
     r = k < a.rank ? k : k + 1;
     row = (int32_t)(o - (int64_t)k * a.b);
   }
+  HIPER_DASSERT(r >= 0 && r < a.world && row >= 0 && row < a.b, r, row);
   if (a.ready[r] != nullptr && threadIdx.x == 0) {
     while (ld_acquire_sys(a.ready[r]) < a.epoch) __nanosleep(128);
   }

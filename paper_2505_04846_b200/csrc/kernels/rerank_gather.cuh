@@ -42,6 +42,7 @@ struct RerankArgs {
   int32_t dim;
   int32_t k1;
   int64_t n_items;            // n_q * k1
+  int64_t n_index;            // chunks in the token index (debug-build bound check)
   float* S2;                  // [n_q][k1] exact MaxSim of each (query, candidate); untouched for -1
 };
 
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(kRerankWarps * 32, 1)
     mc = -1, ml = 0, mr = 0;
     if (rel < n_rel) {
       mc = __ldg(a.slots + i0 + rel);
+      HIPER_DASSERT(mc < a.n_index, mc, a.n_index);
       if (mc >= 0) {
         ml = __ldg(a.d_lens + mc);
         mr = a.row_of != nullptr ? __ldg(a.row_of + mc) : (int64_t)mc * a.ld_pad;

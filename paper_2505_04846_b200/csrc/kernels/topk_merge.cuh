@@ -123,6 +123,7 @@ __global__ void ids_to_slots_kernel(const int64_t* __restrict__ ids, int64_t n_i
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_items) return;
   const int64_t id = ids[e];
+  HIPER_DASSERT(id >= -1, (uint32_t)id, (uint32_t)e);
   slots[e] = (id >= id_base && id < id_base + n) ? (int32_t)(id - id_base) : -1;
 }
 

@@ -75,6 +75,20 @@ __device__ __noinline__ void hiper_watchdog_fail(const char* what, uint32_t a, u
   printf("hiper: %s watchdog block %d thread %d 0x%x 0x%x\n", what, blockIdx.x, threadIdx.x, a, b);
   __trap();
 }
+// Device-side checks of the debug build (libhiper_debug.so, -DHIPER_DEVICE_ASSERTS; the stand-in for
+// compute-sanitizer, which this pool does not offer): a failed check prints and traps.  The production
+// library compiles them out.
+#ifdef HIPER_DEVICE_ASSERTS
+#define HIPER_DASSERT(cond, a, b)                                                        \
+  do {                                                                                   \
+    if (!(cond)) ::hiper::ptx::hiper_watchdog_fail("assert " #cond, (uint32_t)(a), (uint32_t)(b)); \
+  } while (0)
+#else
+#define HIPER_DASSERT(cond, a, b) \
+  do {                            \
+  } while (0)
+#endif
+
 // Wait until the phase with the given parity has completed.  try_wait suspends the thread in hardware
 // until the phase completes or the (10 ms) time hint expires, so waiting warps do not spin on issue
 // slots shared with the epilogue's arithmetic.
