@@ -1303,7 +1303,7 @@ static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks
   if (const char* e = getenv("HIPER_POOLED_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));
   pp.n_parts = choose_parts(pp.n_qtiles / (pp.cl / 2), pp.n_ctiles, di.num_sms / pp.cl);
   uint32_t fixed = 1024u + 1024u;  // align slack, barriers
-  if (topk && k > kPooledKP) fixed += 128u * (uint32_t)(k | 1) * 8u + 512u;  // the k > 16 heaps + locks
+  if (topk && k > kPooledKP) fixed += 128u * (uint32_t)(k | 1) * 8u + 512u + 8192u;  // heaps, locks, top-8
   pp.n_stages = (int32_t)std::min<uint32_t>(8u, ((uint32_t)di.max_smem - fixed) / pp.stage_bytes);
   if (pp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory");
   pp.smem_bytes = fixed + pp.n_stages * pp.stage_bytes;
@@ -1374,7 +1374,7 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
 
 struct PooledWs {
   size_t status = 0, progress = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0,
-         gthr = 0, total = 0;
+         gthr = 0, pub8 = 0, total = 0;
 };
 static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t q_pad, int32_t k,
                              int32_t world, bool with_comm, PooledWs& w) {
@@ -1395,6 +1395,8 @@ static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t 
   if (with_comm) off = align_up(off + (size_t)world * std::max(n_q, 1) * k * 8, 256);
   w.gthr = off;
   off = align_up(off + (size_t)q_pad * 8, 256);
+  w.pub8 = off;  // k > kPooledKP: [q_pad][n_parts] published 8th-best keys
+  if (k > kPooledKP) off = align_up(off + (size_t)q_pad * std::max(n_parts, 1) * 8, 256);
   w.total = off;
 }
 
@@ -1443,6 +1445,10 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   if (!dense_scores && getenv("HIPER_NO_SHARED_BOUND") == nullptr) {
     a.gthr = (unsigned long long*)(ws + w.gthr);
     CUDA_TRY(cudaMemsetAsync(a.gthr, 0, (size_t)pp.q_pad * 8, stream));
+    if (glists && getenv("HIPER_NO_PUB8") == nullptr) {
+      a.pub8 = (unsigned long long*)(ws + w.pub8);
+      CUDA_TRY(cudaMemsetAsync(a.pub8, 0, (size_t)pp.q_pad * std::max(pp.n_parts, 1) * 8, stream));
+    }
   }
   if (ix->n > 0) {
     alignas(64) CUtensorMap tq;

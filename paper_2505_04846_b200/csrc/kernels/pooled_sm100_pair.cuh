@@ -39,6 +39,10 @@ struct PooledArgs {
   // so no item with a key <= gthr[q] can be in the final top-k: the lists skip such items.  Without
   // it each list pays ~k(1 + ln(n/k)) insertions for its own n items (~0.5 per thread per tile here).
   unsigned long long* gthr;
+  // KP == 0: a stronger shared bound.  pub8[q][p] = the 8th-best key unit (., p) holds for query q
+  // (atomicMax, monotone).  If m = ceil(k / 8) partitions each hold 8 keys >= T, at least k keys of the
+  // corpus are >= T, so a key below the m-th largest pub8 value cannot be in the top k.
+  unsigned long long* pub8;
   unsigned long long* stats;  // pipeline statistics (HIPER_PIPE_STATS), or nullptr: [0] MMA cycles
                               // waiting for a free accumulator, [1] for a full stage, [2] MMA
                               // thread total, [3] epilogue drain cycles, [4] epilogue wait, [5] tiles
@@ -100,6 +104,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
   const uint32_t kst = (uint32_t)args.k | 1u;
   volatile uint64_t* heaps = reinterpret_cast<volatile uint64_t*>(smem_raw + (sBar + 1024u - smem_u32(smem_raw)));
   uint32_t* hlocks = reinterpret_cast<uint32_t*>(smem_raw + (sBar + 1024u + 128u * kst * 8u - smem_u32(smem_raw)));
+  // KP == 0: [128 queries][8] u64, each query's 8 best keys of the unit (descending), under the lock
+  volatile uint64_t* top8 = reinterpret_cast<volatile uint64_t*>(
+      smem_raw + (sBar + 1024u + 128u * kst * 8u + 512u - smem_u32(smem_raw)));
   uint32_t* tmem_ptr_generic =
       reinterpret_cast<uint32_t*>(smem_raw + (sTmemPtr - smem_u32(smem_raw)));
 
@@ -229,10 +236,34 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       if (grp == 0) {
         const uint32_t qi0 = qslot * 32u + lane;
         for (int m = 0; m < k; ++m) heaps[qi0 * kst + m] = 0ull;
+        for (int m = 0; m < 8; ++m) top8[qi0 * 8 + m] = 0ull;
         hlocks[qi0] = 0u;
       }
       named_bar_sync(9, 256);
     }
+    // KP == 0: T = the m-th largest of the partitions' published 8th-best keys of query qq,
+    // m = ceil(k / 8) (a running descending list of the 16 largest)
+    auto pub8_bound = [&](int32_t qq) -> uint64_t {
+      const int m8 = (k + 7) >> 3;
+      uint64_t best[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x) best[x] = 0ull;
+      const volatile unsigned long long* row = args.pub8 + (int64_t)qq * args.n_parts;
+      for (int32_t pp = 0; pp < args.n_parts; ++pp) {
+        uint64_t val = row[pp];
+#pragma unroll
+        for (int x = 0; x < 16; ++x) {
+          const uint64_t hi = best[x] > val ? best[x] : val;
+          val = best[x] > val ? val : best[x];
+          best[x] = hi;
+        }
+      }
+      uint64_t T = 0ull;
+#pragma unroll
+      for (int x = 0; x < 16; ++x)
+        if (x == m8 - 1) T = best[x];
+      return T;
+    };
     for (int32_t u = (int32_t)ufirst; u < n_units; u += (int32_t)ustride) {
       int32_t qt, p, t0, t1;
       decode(u, qt, p, t0, t1);
@@ -246,7 +277,14 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       uint64_t gth = 0ull, pub = 0ull;  // shared bound seen / own thr last published
       if (args.gthr != nullptr && q < args.q_pad)
         gth = *reinterpret_cast<volatile unsigned long long*>(args.gthr + q);
+      if constexpr (KP == 0) {
+        if (args.pub8 != nullptr && q < args.q_pad) {
+          const uint64_t T = pub8_bound(q);
+          gth = T > gth ? T : gth;
+        }
+      }
       uint64_t lim = gth;         // max(thr, gth): only keys above it can enter
+      const uint32_t mine0 = mine;  // this unit's first tile (KP == 0: refresh the bound often early)
       float thr_f = pooled_thr_score(lim);  // its score: most candidates fail one float compare
       const int32_t first = t0 + (int32_t)((grp - (t & 1u)) & 1u);
       t += (uint32_t)(t1 - t0);
@@ -333,10 +371,24 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                     }
                     heap[i] = key;
                     root = heap[0];
+                    if (args.pub8 != nullptr) {  // the unit's 8 best keys of this query
+                      volatile uint64_t* t8 = top8 + qi * 8;
+                      if (key > t8[7]) {
+                        int pos = 7;
+                        while (pos > 0 && t8[pos - 1] < key) {
+                          t8[pos] = t8[pos - 1];
+                          --pos;
+                        }
+                        t8[pos] = key;
+                      }
+                    }
                   }
                 }
+                const uint64_t my8 = args.pub8 != nullptr ? top8[qi * 8 + 7] : 0ull;
                 __threadfence_block();
                 atomicExch_block(hlocks + qi, 0u);
+                if (my8 != 0ull && q < args.q_pad)
+                  atomicMax(args.pub8 + (int64_t)q * args.n_parts + p, (unsigned long long)my8);
                 thr = root;
                 lim = thr > gth ? thr : gth;
                 thr_f = pooled_thr_score(lim);
@@ -386,6 +438,14 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               const uint64_t cur = *reinterpret_cast<volatile unsigned long long*>(args.gthr + q);
               gth = cur > gth ? cur : gth;
             }
+            if constexpr (KP == 0) {
+              // every tile during the unit's first 8 (the bound rises fastest while the heaps fill),
+              // then every 8th
+              if (args.pub8 != nullptr && (mine - mine0 < 8u || (mine & 7u) == 0)) {
+                const uint64_t T = pub8_bound(q);
+                gth = T > gth ? T : gth;
+              }
+            }
             const uint64_t nl = thr > gth ? thr : gth;
             if (nl != lim) {
               lim = nl;
@@ -410,6 +470,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             if (q < args.n_q) dst[m] = heap[m];
             heap[m] = 0ull;
           }
+          for (int m = 0; m < 8; ++m) top8[qi * 8 + m] = 0ull;
         }
         named_bar_sync(9, 256);  // cleared before the next unit's first insertion
       }
