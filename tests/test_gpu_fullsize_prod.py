@@ -244,3 +244,68 @@ def test_config4v_3p6m_packed_one_gpu_top100(H):
     ref = torch_ref_packed(lay, row_chunk, C, qrows, LQ)
     no_better_unreturned(ref, s, i, sample, 0, "config4v packed 3.6M")
     del corpus, idx, lay, ref, row_chunk
+
+
+def test_two_stage_3p6m_full_size(H):
+    """bench.py --workload two_stage at size: 3.6M pooled (768-d) + the same chunks' packed token rows,
+    Q = 1024, k1 = 100, k = 10.  Stage 1 is checked against a torch/cuBLAS pooled-cosine reference over
+    the whole pooled index (its top-100 set, up to near-ties); stage 2 against the oracle's exact MaxSim
+    of every candidate of the sampled queries (SPEC.md:268-276 rerank)."""
+    need_free(115)
+    C, Q, K1, K, DP = 3_600_000, 1024, 100, 10, 768
+    from synth import device
+    lens = gen.semantic_lengths(SEED, C, L)
+    dst, n_rows = H.hiper_pack_dst_rows(lens)
+    tok = torch.empty((n_rows, D), dtype=torch.bfloat16, device="cuda")
+    lens_dev = torch.from_numpy(lens).cuda()
+    device.corpus_packed_(tok, SEED, 0, torch.from_numpy(dst).cuda(), lens_dev, L)
+    tidx = H.hiper_index_build(tok, lens, flags=H.HIPER_PACKED | H.HIPER_BORROW_TOKENS)
+    PSEED = SEED + 1000                       # bench.py's pooled corpus seed
+    pool = torch.empty((C, 1, DP), dtype=torch.bfloat16, device="cuda")
+    device.corpus_(pool, PSEED, 0)
+    pidx = H.hiper_index_build(pool, np.ones(C, np.int32), flags=H.HIPER_POOLED | H.HIPER_BORROW_TOKENS)
+    qt = torch.empty((Q, LQ, D), dtype=torch.bfloat16, device="cuda")
+    device.queries_(qt, QSEED, corpus_seed=SEED, n_chunks=C, L=L, chunk_lens=lens_dev)
+    qp = torch.empty((Q, 1, DP), dtype=torch.bfloat16, device="cuda")
+    device.queries_(qp, QSEED, corpus_seed=PSEED, n_chunks=C, L=1)
+    qlen = np.full(Q, LQ, np.int32)
+    s, i = [t.cpu().numpy() for t in H.hiper_two_stage_topk(pidx, tidx, qp, qt, qlen, K1, K)]
+    tgt = gen.query_targets(QSEED, Q, C, False)
+    assert (i[:, 0] == tgt).all()
+    check_lists(s, i, 0, C, K)
+    # stage 1 vs a cuBLAS reference over all 3.6M pooled rows (the exact top-100 set up to near-ties)
+    s1, i1 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(pidx, qp, np.ones(Q, np.int32), K1)]
+    sample = [0, 511, 1023]
+    # (the pooled query rows: the oracle's NORM of the raw inputs, which the pooled tests show the
+    # library reproduces bitwise)
+    qpb = np.stack([oracle.norm_rows(gen.queries(QSEED, 1, 1, DP, corpus_seed=PSEED, n_chunks=C, L=1,
+                                                 start=qq)[0, 0]) for qq in sample])
+    torch.backends.cuda.matmul.allow_tf32 = False
+    qrow = torch.from_numpy(qpb.view(np.int16)).cuda().view(torch.bfloat16).float()
+    ref = (qrow @ pidx.layout()[:, 0].float().T).cpu().numpy().astype(np.float64)   # [3][C]
+    for r, qq in enumerate(sample):
+        kth = np.sort(ref[r])[::-1][K1 - 1]
+        tol = 2e-3 * abs(kth) + DP * 2.0 ** -24
+        got = ref[r][i1[qq]]
+        assert (got >= kth - tol).all(), f"stage 1 query {qq}: a returned candidate below the 100th"
+        others = np.setdiff1d(np.arange(C), i1[qq])
+        assert ref[r][others].max() <= s1[qq][-1] + tol, f"stage 1 query {qq}: a better unreturned chunk"
+    # stage 2: the oracle's exact MaxSim of each sampled query's 100 candidates, re-sorted
+    qlay, _ = H.hiper_prepare_queries(qt, qlen)
+    qlay = bits(qlay)
+    lay = tidx.layout()
+    for qq in sample:
+        cands = i1[qq]
+        S2 = np.empty(len(cands))
+        for jx, c in enumerate(cands.tolist()):
+            rows = bits(lay[int(dst[c]):int(dst[c]) + int(lens[c])])
+            raw = gen.f32_to_bf16_bits(gen.corpus_tokens_f32(SEED, [c], L, D))[0][:lens[c]]
+            assert np.array_equal(rows, oracle.norm_rows(raw))
+            S2[jx] = oracle.maxsim(qlay[qq], rows)
+        o_s, o_i = oracle.topk(S2, cands.astype(np.int64), K)
+        tol = score_tol(o_s, LQ, D)
+        assert (np.abs(s[qq] - o_s) <= tol).all(), (qq, s[qq], o_s)
+        for r_ in range(K):   # ids equal except inside near-tie runs
+            if i[qq][r_] != o_i[r_]:
+                assert abs(S2[list(cands).index(i[qq][r_])] - o_s[r_]) <= tol[r_]
+    del tok, tidx, pool, pidx, lay
