@@ -2120,10 +2120,12 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     constexpr int VPL = decltype(vpl)::value;
     using Tin = decltype(tin);
     auto gqs = grad_q_stream_kernel<VPL / 2>;
-    const int gsm = 1024 + 2 * ld_pad * 128 * (VPL / 2) + 64;
+    const int gstage = ld_pad * 128 * (VPL / 2);
+    const int gns = std::max(2, std::min(4, (di.max_smem - 1024 - 128) / gstage));  // TMA ring depth
+    const int gsm = 1024 + gns * gstage + 128;
     CUDA_TRY(set_max_smem((const void*)gqs, gsm));
     gqs<<<(unsigned)(qblk * R), (kGqWarps + 1) * 32, gsm, stream>>>(tdg, G, amax, n_q, n_d, ld_pad,
-                                                                    qlens_dev, R, qpart);
+                                                                    qlens_dev, R, qpart, gns);
     CUDA_TRY(cudaGetLastError());
     grad_q_reduce_kernel<VPL, Tin><<<qblocks, 256, 0, stream>>>(qpart, R, n_q, (const Tin*)q_tokens,
                                                                 q_max_len, qlens_dev, an, grad_q);

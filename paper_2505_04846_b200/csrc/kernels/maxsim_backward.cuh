@@ -91,7 +91,8 @@ template <int NKB>
 __global__ void __launch_bounds__((kGqWarps + 1) * 32, 1)
     grad_q_stream_kernel(const __grid_constant__ CUtensorMap tmap_d, const float* __restrict__ G,
                          const uint8_t* __restrict__ amax, int32_t B, int32_t M, int32_t ld_pad,
-                         const int32_t* __restrict__ q_lens, int32_t R, float* __restrict__ part) {
+                         const int32_t* __restrict__ q_lens, int32_t R, float* __restrict__ part,
+                         int32_t NS) {
   constexpr int D = 64 * NKB;
   extern __shared__ uint8_t smem_raw[];
   using namespace ptx;
@@ -99,11 +100,11 @@ __global__ void __launch_bounds__((kGqWarps + 1) * 32, 1)
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t kb_bytes = (uint32_t)ld_pad * 128u;
   const uint32_t stage_bytes = kb_bytes * NKB;
-  const uint32_t bars = base + 2u * stage_bytes;  // full[2], empty[2]
+  const uint32_t bars = base + (uint32_t)NS * stage_bytes;  // full[NS], empty[NS]
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(bars + 8u * s, 1);
-      mbar_init(bars + 16u + 8u * s, kGqWarps);
+      mbar_init(bars + 8u * (NS + s), kGqWarps);
     }
     fence_mbarrier_init();
   }
@@ -114,8 +115,8 @@ __global__ void __launch_bounds__((kGqWarps + 1) * 32, 1)
     if (lane == 0) {
       prefetch_tmap(&tmap_d);
       for (int32_t j = j0; j < j1; ++j) {
-        const uint32_t s = (uint32_t)(j - j0) & 1u, ph = ((uint32_t)(j - j0) >> 1) & 1u;
-        mbar_wait(bars + 16u + 8u * s, ph ^ 1u);
+        const uint32_t s = (uint32_t)(j - j0) % (uint32_t)NS, ph = ((uint32_t)(j - j0) / (uint32_t)NS) & 1u;
+        mbar_wait(bars + 8u * (NS + s), ph ^ 1u);
         mbar_arrive_expect_tx(bars + 8u * s, stage_bytes);
 #pragma unroll
         for (int kb = 0; kb < NKB; ++kb)
@@ -130,10 +131,19 @@ __global__ void __launch_bounds__((kGqWarps + 1) * 32, 1)
   float acc[D];
 #pragma unroll
   for (int v = 0; v < D; ++v) acc[v] = 0.0f;
+  // G_ij and a(i, t, j) of the next chunk are loaded one iteration ahead (L2 latency off the loop)
+  auto load_gu = [&](int32_t jj, float& gg, uint32_t& uu) {
+    gg = (i < B && jj < j1) ? __ldg(G + (int64_t)i * M + jj) : 0.0f;
+    uu = (i < B && jj < j1) ? __ldg(amax + ((int64_t)i * M + jj) * 32 + t) : 0u;
+  };
+  float g_n;
+  uint32_t u_n;
+  load_gu(j0, g_n, u_n);
   for (int32_t j = j0; j < j1; ++j) {
-    const uint32_t s = (uint32_t)(j - j0) & 1u, ph = ((uint32_t)(j - j0) >> 1) & 1u;
-    const float g = i < B ? __ldg(G + (int64_t)i * M + j) : 0.0f;
-    const uint32_t u = i < B ? __ldg(amax + ((int64_t)i * M + j) * 32 + t) : 0u;
+    const uint32_t s = (uint32_t)(j - j0) % (uint32_t)NS, ph = ((uint32_t)(j - j0) / (uint32_t)NS) & 1u;
+    const float g = g_n;
+    const uint32_t u = u_n;
+    load_gu(j + 1, g_n, u_n);
     mbar_wait(bars + 8u * s, ph);
     if (valid) {
       const uint32_t row = base + s * stage_bytes + u * 128u;
@@ -151,7 +161,7 @@ __global__ void __launch_bounds__((kGqWarps + 1) * 32, 1)
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(bars + 16u + 8u * s);
+    if (lane == 0) mbar_arrive(bars + 8u * (NS + s));
   }
   if (i < B) {
     float4* dst = reinterpret_cast<float4*>(part + (((int64_t)r * B + i) * 32 + t) * D);
