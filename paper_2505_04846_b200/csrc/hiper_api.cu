@@ -2021,21 +2021,29 @@ extern "C" hiper_status hiper_coltrast_loss_simulated(
 
 // ============================================================================ N1: L_LI backward
 struct GradWs {
-  size_t base = 0, amax = 0, G = 0, sorted = 0, bucket = 0, qpart = 0, total = 0;
+  size_t base = 0, amax = 0, G = 0, ent = 0, bucket = 0, scratch = 0, qpart = 0, total = 0;
+  int32_t S = 64, n_seg = 0;  // grad_d segments: hits per segment, segments per doc (at most)
   ColtrastWs cw;
 };
 static constexpr int32_t kGqRangesMax = 8;  // chunk ranges of the streamed grad_q (partials)
 static void grad_ws_layout(int32_t n_q, int32_t n_d, int32_t d_max_len, int32_t dim, GradWs& w) {
   coltrast_ws_layout(n_q, n_d, d_max_len, dim, w.cw);
+  const int32_t E = std::max(n_q, 1) * 32;
+  w.S = 128;  // a power of two; segments per doc stay <= 128 (bounded scratch)
+  if (const char* e = getenv("HIPER_GRAD_S")) w.S = std::max(64, std::min(1024, atoi(e)));
+  while (w.S < E / 128) w.S *= 2;
+  w.n_seg = (E + w.S - 1) / w.S;
   size_t off = align_up(w.cw.total, 1024);
   w.amax = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * std::max(n_d, 1) * 32, 1024);
   w.G = off;
   off = align_up(off + (size_t)std::max(n_q, 1) * std::max(n_d, 1) * 4, 1024);
-  w.sorted = off;  // inverted argmax map per doc: [n_d][n_q * 32] u16 entries + [n_d][258] offsets
-  off = align_up(off + (size_t)std::max(n_q, 1) * 32 * std::max(n_d, 1) * 2, 1024);
+  w.ent = off;  // inverted argmax map per doc: [n_d][n_q * 32] {i * 32 + t, G_ij} + [n_d][258] starts
+  off = align_up(off + (size_t)E * std::max(n_d, 1) * 8, 1024);
   w.bucket = off;
   off = align_up(off + (size_t)std::max(n_d, 1) * 258 * 4, 1024);
+  w.scratch = off;  // [n_d][n_seg][2][dim] fp32 partials of rows that cross segments
+  off = align_up(off + (size_t)std::max(n_d, 1) * w.n_seg * 2 * dim * 4, 1024);
   w.qpart = off;  // [R][n_q * 32][dim] fp32 partial sums of grad_q
   off = align_up(off + (size_t)kGqRangesMax * std::max(n_q, 1) * 32 * dim * 4, 1024);
   w.total = off;
@@ -2109,7 +2117,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
   const int64_t qrows = (int64_t)n_q * q_max_len;
   const unsigned qblocks = (unsigned)((qrows + 7) / 8);
-  const size_t dsmem = (size_t)n_q * 32 * 3 + (size_t)n_q * 8 + 2 * 8 * 257 * 4;
+  const size_t dsmem = (size_t)n_q * 32 * 3 + (size_t)n_q * 8 + 2 * kSortWarps * 257 * 4;
   // grad_q: chunk tiles streamed through shared memory per 8 queries (partials over R chunk ranges)
   const int32_t qblk = (n_q + kGqWarps - 1) / kGqWarps;
   const int32_t R = std::max(1, std::min({kGqRangesMax, n_d, di.num_sms / std::max(qblk, 1)}));
@@ -2131,22 +2139,25 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
                                                                 q_max_len, qlens_dev, an, grad_q);
     CUDA_TRY(cudaGetLastError());
     g_launches += 1;
-    // grad_d: sort-only pass (one block per doc), then one warp per output row for the gathers.
-    // (A per-doc CTA streaming the query rows through shared memory was 2.2x slower: a few hub doc
-    // rows take most argmax hits and serialise their threads -- profiles/r02/ablation/grad.txt.)
-    auto gk = grad_d_kernel<VPL, Tin>;
-    CUDA_TRY(set_max_smem((const void*)gk, (int)dsmem));
-    uint16_t* srt = (uint16_t*)(ws + w.sorted);
+    // grad_d: the inverted argmax map per doc (one block per doc), then one warp per segment of S
+    // sorted hits, so "hub" doc rows that take most argmax hits are spread over many warps.
+    CUDA_TRY(set_max_smem((const void*)grad_d_sort_kernel, (int)dsmem));
+    uint2* ent = (uint2*)(ws + w.ent);
     int32_t* bkt = (int32_t*)(ws + w.bucket);
-    gk<<<(unsigned)n_d, 256, dsmem, stream>>>(G, amax, n_q, n_d, qlayout, qlens_dev, ld_pad,
-                                              (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d,
-                                              srt, bkt);
+    grad_d_sort_kernel<<<(unsigned)n_d, kSortWarps * 32, dsmem, stream>>>(amax, G, n_q, n_d,
+                                                                           qlens_dev, ent, bkt);
     CUDA_TRY(cudaGetLastError());
-    const int64_t drows = (int64_t)n_d * d_max_len;
-    grad_d_gather_kernel<VPL, Tin><<<(unsigned)((drows + 7) / 8), 256, 0, stream>>>(
-        G, n_q, n_d, qlayout, srt, bkt, (const Tin*)d_tokens, d_max_len, dlens_dev, an, grad_d);
+    const int64_t sblocks = (int64_t)n_d * ((w.n_seg + 7) / 8);
+    float* scr = (float*)(ws + w.scratch);
+    grad_d_seg_kernel<VPL><<<(unsigned)sblocks, 256, 0, stream>>>(n_q, qlayout, ent, bkt,
+                                                                  __builtin_ctz((unsigned)w.S), w.n_seg,
+                                                                  scr, d_max_len, grad_d);
     CUDA_TRY(cudaGetLastError());
-    g_launches += 3;
+    const int64_t fwarps = (int64_t)n_d * ((d_max_len + 3) / 4);  // 4 rows per warp
+    grad_d_finish_kernel<VPL, Tin><<<(unsigned)((fwarps + 7) / 8), 256, 0, stream>>>(
+        bkt, w.S, w.n_seg, scr, n_d, (const Tin*)d_tokens, d_max_len, an, grad_d);
+    CUDA_TRY(cudaGetLastError());
+    g_launches += 4;
     return HIPER_OK;
   };
   using I2 = std::integral_constant<int, 2>;
