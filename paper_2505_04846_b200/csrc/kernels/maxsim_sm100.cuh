@@ -161,22 +161,47 @@ __device__ __forceinline__ void max64_masked(const uint32_t (&v)[64], float (&m)
     m[i & 3] = fmaxf(m[i & 3], x);
   }
 }
-// Running max and argmax (lowest column on exact ties) with one running pair per thread: the block
-// max costs 21 FMNMX3; only a block that raises the running max is scanned (downwards, == test) for
-// its lowest column attaining it.  The lowest match is always a real column: the block max is
-// attained by one, and padded columns (index >= rem) come after every real one.
+// Running max and argmax (lowest column on exact ties) with one running pair per thread.  The block
+// max is the max of its two 32-column halves (FMNMX3 chains); only a block that raises the running max
+// is scanned for its lowest column attaining it: the first half holding the max is selected (32 SEL)
+// and scanned downwards with == in 8 interleaved chains (64 instructions instead of 128 for the whole
+// block -- the scan is issue-bound, and the warp runs it whenever any lane improves).  The lowest
+// match is always a real column: the max is attained by one, and padded columns (index >= rem) come
+// after every real one.
 __device__ __forceinline__ void max64_arg1(const uint32_t (&v)[64], float& m, int& ix, int base,
                                            int rem) {
-  float b[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  if (rem >= 64) max64(v, b);
-  else max64_masked(v, b, rem);
-  const float mb = fmaxf(fmaxf(b[0], b[1]), fmaxf(b[2], b[3]));
-  if (mb > m) {
-    int j = 63;
+  float h[2][2] = {{-INFINITY, -INFINITY}, {-INFINITY, -INFINITY}};
+  if (rem >= 64) {
 #pragma unroll
-    for (int i = 63; i >= 0; --i) j = (__uint_as_float(v[i]) == mb) ? i : j;
+    for (int half = 0; half < 2; ++half)
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          h[half][c] = fmaxf(fmaxf(h[half][c], __uint_as_float(v[32 * half + i + 2 * c])),
+                             __uint_as_float(v[32 * half + i + 2 * c + 1]));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const float x = (i < rem) ? __uint_as_float(v[i]) : -INFINITY;
+      h[i >> 5][i & 1] = fmaxf(h[i >> 5][i & 1], x);
+    }
+  }
+  const float h0 = fmaxf(h[0][0], h[0][1]), h1 = fmaxf(h[1][0], h[1][1]);
+  const float mb = fmaxf(h0, h1);
+  if (mb > m) {
+    const bool upper = !(h0 == mb);  // ties go to the lower half
+    int jc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) jc[c] = 32;
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+      const float x = __uint_as_float(upper ? v[32 + i] : v[i]);
+      jc[i & 7] = (x == mb) ? i : jc[i & 7];
+    }
+    const int j = min(min(min(jc[0], jc[1]), min(jc[2], jc[3])), min(min(jc[4], jc[5]), min(jc[6], jc[7])));
     m = mb;
-    ix = base + j;
+    ix = base + (upper ? 32 : 0) + j;
   }
 }
 
