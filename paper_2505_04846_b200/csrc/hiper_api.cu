@@ -1713,7 +1713,7 @@ static hiper_status launch_loss(const float* S, int32_t n_q, int32_t n_d, int64_
                                 const int32_t* pos_dev, float tau, float* out_loss,
                                 cudaStream_t stream, const float* combine_with = nullptr,
                                 float* out_combined = nullptr, double* rows = nullptr,
-                                uint32_t* counter = nullptr) {
+                                uint32_t* counter = nullptr, float* G = nullptr) {
   if (rows != nullptr && counter != nullptr && combine_with == nullptr) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)((n_q + 7) / 8));
@@ -1725,7 +1725,7 @@ static hiper_status launch_loss(const float* S, int32_t n_q, int32_t n_d, int64_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, infonce_rows_kernel, S, n_q, n_d, ld, pos_dev, tau, rows,
-                                counter, out_loss));
+                                counter, out_loss, G));
   } else
     infonce_loss_kernel<<<1, 1024, 0, stream>>>(S, n_q, n_d, ld, pos_dev, tau, out_loss, combine_with,
                                                 out_combined);
@@ -2109,11 +2109,9 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
   a.amax = amax;
   TRY(launch_maxsim(2, 1, kp, tq, td, a, stream));                       // S + argmax (a3-a5)
   const int32_t* pd = pos_idx ? pos_dev : nullptr;
+  // a11 and G = dL_LI/dS in one launch (the row warps write their row of G)
   TRY(launch_loss(S, n_q, n_d, n_d, pd, temperature, out_loss, stream, nullptr, nullptr,
-                  (double*)(ws + c.rowloss), (uint32_t*)(ws + c.status + kLossCounterOff)));  // a11
-  infonce_grad_kernel<<<(n_q + 7) / 8, 256, 0, stream>>>(S, n_q, n_d, n_d, pd, temperature, G);
-  CUDA_TRY(cudaGetLastError());
-  ++g_launches;
+                  (double*)(ws + c.rowloss), (uint32_t*)(ws + c.status + kLossCounterOff), G));
   const uint32_t an = (flags & HIPER_ASSUME_NORMALIZED) ? 1u : 0u;
   const int64_t qrows = (int64_t)n_q * q_max_len;
   const unsigned qblocks = (unsigned)((qrows + 7) / 8);

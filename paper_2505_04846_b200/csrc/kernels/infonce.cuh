@@ -29,6 +29,26 @@ __device__ __forceinline__ float infonce_row(const float* __restrict__ row, int3
   return (mx == zp) ? log1pf(r) : (mx - zp) + logf(expf(zp - mx) + r);
 }
 
+// dL_LI/dS_ij of one row (N1): G_ij = (softmax_j(S_i / tau) - [j == p]) / (B tau), the softmax over
+// all j with the same fixed-order lane partials (written by the loss kernel's warp for its row).
+__device__ __forceinline__ void infonce_row_grad(const float* __restrict__ row, int32_t B, int32_t M,
+                                                 int32_t p, float tau, uint32_t lane,
+                                                 float* __restrict__ g) {
+  float mx = -INFINITY;
+  for (int32_t j = lane; j < M; j += 32) mx = fmaxf(mx, __fdiv_rn(row[j], tau));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.0f;
+  for (int32_t j = lane; j < M; j += 32) sum += expf(__fdiv_rn(row[j], tau) - mx);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float scale = 1.0f / ((float)B * tau);
+  for (int32_t j = lane; j < M; j += 32) {
+    const float pj = expf(__fdiv_rn(row[j], tau) - mx) / sum;
+    g[j] = (pj - (j == p ? 1.0f : 0.0f)) * scale;
+  }
+}
+
 // Row-parallel form (the ColTrast step): one warp per row over ceil(B/8) blocks; each row's l_i goes to
 // rowloss[i]; the last block to finish (completion counter, zeroed by the caller, reset here) sums
 // rowloss in index order in fp64 -> L.  Deterministic: the order depends on nothing but B.
@@ -36,15 +56,18 @@ __global__ void __launch_bounds__(256) infonce_rows_kernel(const float* __restri
                                                            int32_t M, int64_t ld,
                                                            const int32_t* __restrict__ pos, float tau,
                                                            double* __restrict__ rowloss,
-                                                           uint32_t* counter, float* __restrict__ out_loss) {
+                                                           uint32_t* counter, float* __restrict__ out_loss,
+                                                           float* __restrict__ G = nullptr) {
   __shared__ double part[256];
   __shared__ bool last;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: S is the previous kernel's output
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t i = (int32_t)blockIdx.x * 8 + (int32_t)warp;
   if (i < B) {
-    const float li = infonce_row(S + (int64_t)i * ld, M, pos ? pos[i] : i, tau, lane);
+    const int32_t p = pos ? pos[i] : i;
+    const float li = infonce_row(S + (int64_t)i * ld, M, p, tau, lane);
     if (lane == 0) rowloss[i] = (double)li;
+    if (G != nullptr) infonce_row_grad(S + (int64_t)i * ld, B, M, p, tau, lane, G + (int64_t)i * M);
   }
   __threadfence();
   __syncthreads();

@@ -1,7 +1,7 @@
 // maxsim_backward.cuh -- NEXT N1: gradient of the ColTrast late-interaction loss L_LI.
 //
 // Chain rule (the objective is trained by backpropagation):
-//   G_ij          = (softmax_j(S_i / tau)_j - [j == pos_i]) / (B tau)            infonce_grad_kernel
+//   G_ij          = (softmax_j(S_i / tau)_j - [j == pos_i]) / (B tau)   infonce_rows_kernel (G out)
 //   a(i,t,j)      = argmax_{u < len_j} <qn_{i,t}, dn_{j,u}>  (saved by the forward, MODE 2)
 //   g_q(i,t)      = sum_j G_ij dn_{j, a(i,t,j)}                  grad_q_stream_kernel + _reduce
 //   g_d(j,u)      = sum_i sum_{t: a(i,t,j) = u} G_ij qn_{i,t}       grad_d_sort_kernel + _seg
@@ -17,30 +17,6 @@
 #include "../ptx.cuh"
 
 namespace hiper {
-
-__global__ void __launch_bounds__(256) infonce_grad_kernel(const float* __restrict__ S, int32_t B,
-                                                           int32_t M, int64_t ld,
-                                                           const int32_t* __restrict__ pos,
-                                                           float tau, float* __restrict__ G) {
-  const uint32_t lane = threadIdx.x & 31;
-  const int32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (i >= B) return;
-  const float* row = S + (int64_t)i * ld;
-  const int32_t p = pos ? pos[i] : i;
-  float mx = -INFINITY;
-  for (int32_t j = lane; j < M; j += 32) mx = fmaxf(mx, __fdiv_rn(row[j], tau));
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float sum = 0.0f;
-  for (int32_t j = lane; j < M; j += 32) sum += expf(__fdiv_rn(row[j], tau) - mx);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  const float scale = 1.0f / ((float)B * tau);
-  for (int32_t j = lane; j < M; j += 32) {
-    const float pj = expf(__fdiv_rn(row[j], tau) - mx) / sum;
-    G[(int64_t)i * M + j] = (pj - (j == p ? 1.0f : 0.0f)) * scale;
-  }
-}
 
 template <typename Tin>
 __device__ __forceinline__ float load_raw(const Tin* p);
