@@ -1,7 +1,7 @@
 # A/B of grad_d segment sizes (HIPER_GRAD_S) on config2 --grad; launch list per setting
 python __graft_entry__.py > gpurun_out/build.log 2>&1 || tail -20 gpurun_out/build.log
 timeout 600 python -m pytest tests -q -m gpu -x -p no:cacheprovider -k "grad" > gpurun_out/pytest_grad.log 2>&1; tail -1 gpurun_out/pytest_grad.log
-for S in 128; do
+for S in 128 256; do
   for i in 1 2; do
     HIPER_GRAD_S=$S timeout 300 python bench.py --workload config2 --grad --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('S=$S', round(d['value'],1), round(d['ms_per_step']*1000,1), 'us')"
   done
