@@ -37,6 +37,10 @@ def widen(a):
     (16, 40, 20, 64, 64, "bf16", 0.1, "iid"),
     (37, 37, 32, 128, 128, "bf16", 0.5, "planted"),
     (64, 80, 32, 256, 128, "bf16", 1.0, "planted"),   # 8 query tiles x full-length docs (streamed paths)
+    # ld_pad 144 and 208 (not multiples of 64: the argmax epilogue's last 64-column block is
+    # partial), ragged lengths
+    (24, 30, 32, 144, 64, "bf16", 1.0, "iid"),
+    (33, 40, 17, 200, 128, "f32", 0.3, "planted"),
 ])
 def test_li_backward_matches_oracle(H, n_q, n_d, Lq, Ld, d, dtype, tau, kind):
     corp = gen.corpus(71, 0, n_d, Ld, d, kind=kind, dtype=dtype)
