@@ -991,18 +991,23 @@ static hiper_status launch_maxsim(int mode, int k, const KernelPlan& kp, const C
   return launch_maxsim_qh<1, 4, false>(kp, tq, td, a, stream);
 }
 
+// list_len: keys per list (<= 128; 0 = k)
 static hiper_status launch_merge(const uint64_t* lists, int32_t n_lists, int64_t list_stride,
                                  int32_t n_q, int64_t q_stride, int32_t k, uint64_t* out_keys,
-                                 float* out_scores, int64_t* out_ids, cudaStream_t stream) {
+                                 float* out_scores, int64_t* out_ids, cudaStream_t stream,
+                                 int32_t list_len = 0) {
   if (n_q == 0) return HIPER_OK;
   const int threads = 256, qpb = threads / 32;
   const int blocks = (n_q + qpb - 1) / qpb;
-  if (k <= 32)
-    topk_merge_kernel<1><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids);
-  else if (k <= 64)
-    topk_merge_kernel<2><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids);
+  const int32_t ll = list_len > 0 ? list_len : k;
+  // KR covers both the output k and the list length (a list is read KR x 32 keys at a time)
+  const int32_t kr = std::max(k, ll);
+  if (kr <= 32)
+    topk_merge_kernel<1><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids, ll);
+  else if (kr <= 64)
+    topk_merge_kernel<2><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids, ll);
   else
-    topk_merge_kernel<4><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids);
+    topk_merge_kernel<4><<<blocks, threads, 0, stream>>>(lists, n_lists, list_stride, n_q, q_stride, k, out_keys, out_scores, out_ids, ll);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return HIPER_OK;
@@ -1290,7 +1295,7 @@ static int32_t pooled_qtiles(int32_t n_q, int cl) {
 }
 
 static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks, PooledPlan& pp,
-                                bool topk = true, int32_t k = 1) {
+                                bool topk = true, int32_t k = 1, bool append = false) {
   pp.cl = pooled_cluster(topk);
   pp.n_qtiles = pooled_qtiles(n_q, pp.cl);
   pp.q_pad = pp.n_qtiles * 256;
@@ -1303,7 +1308,7 @@ static hiper_status plan_pooled(const DevInfo& di, int32_t n_q, int64_t n_chunks
   if (const char* e = getenv("HIPER_POOLED_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(e)));
   pp.n_parts = choose_parts(pp.n_qtiles / (pp.cl / 2), pp.n_ctiles, di.num_sms / pp.cl);
   uint32_t fixed = 1024u + 1024u;  // align slack, barriers
-  if (topk && k > kPooledKP) fixed += 128u * (uint32_t)(k | 1) * 8u + 512u + 8192u;  // heaps, locks, top-8
+  if (topk && k > kPooledKP && !append) fixed += 128u * (uint32_t)(k | 1) * 8u + 512u + 8192u;  // heaps, locks, top-8
   pp.n_stages = (int32_t)std::min<uint32_t>(8u, ((uint32_t)di.max_smem - fixed) / pp.stage_bytes);
   if (pp.n_stages < 2) return fail(HIPER_ERR_UNSUPPORTED, "not enough shared memory");
   pp.smem_bytes = fixed + pp.n_stages * pp.stage_bytes;
@@ -1320,9 +1325,12 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   auto kern = pp.cl == 4 ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 4>
               : pstats_on ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 2, true>
                           : pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
-  if (MODE == 1 && a.k > kPooledKP) {  // warp-cooperative lists in the partial buffer
+  if (MODE == 1 && a.k > kPooledKP) {  // shared-memory heaps, or the APPEND candidate buffers
     if (pp.cl != 2) return fail(HIPER_ERR_UNSUPPORTED, "pooled k > %d with HIPER_POOLED_MC", kPooledKP);
-    kern = pstats_on ? pooled_sm100_pair_kernel<MODE, 0, 0, 2, true> : pooled_sm100_pair_kernel<MODE, 0, 0, 2>;
+    if (a.cand != nullptr)
+      kern = pstats_on ? pooled_sm100_pair_kernel<MODE, -1, 0, 2, true> : pooled_sm100_pair_kernel<MODE, -1, 0, 2>;
+    else
+      kern = pstats_on ? pooled_sm100_pair_kernel<MODE, 0, 0, 2, true> : pooled_sm100_pair_kernel<MODE, 0, 0, 2>;
   }
   if (MODE == 1 && debug_mode() == 1) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 1, 2, true>;
   if (MODE == 1 && debug_mode() == 2) kern = pooled_sm100_pair_kernel<MODE, kPooledKP, 2, 2, true>;
@@ -1374,10 +1382,29 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
 
 struct PooledWs {
   size_t status = 0, progress = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0,
-         gthr = 0, pub8 = 0, total = 0;
+         gthr = 0, pub8 = 0, thrk = 0, cand = 0, ccnt = 0, total = 0;
 };
+// Pooled top-k with 16 < k <= 128, APPEND path: a pre-pass takes the exact top-k of a corpus sample
+// (the first S chunks, whole 256-chunk tiles, S ~ n / 32 and >= 8k) with the heap kernel; the k-th
+// key of the sample, T_q, bounds the k-th key of the corpus from below, so the main pass only has to
+// append the keys >= T_q (~32 k per query) and a warp per query selects the top k of them.  The
+// heaps leave shared memory to the pipeline (6 stages instead of 3).  0 = no APPEND (small corpora,
+// or HIPER_POOLED_APPEND=0).
+static int64_t pooled_append_sample(int64_t n_chunks, int32_t k) {
+  static const bool off = getenv("HIPER_POOLED_APPEND") && getenv("HIPER_POOLED_APPEND")[0] == '0';
+  if (off || k <= kPooledKP) return 0;
+  int64_t s = std::max<int64_t>(n_chunks / 32, 8 * (int64_t)k);
+  s = (s + 255) / 256 * 256;
+  return s * 4 <= n_chunks ? s : 0;
+}
+// candidate buffer slots per query: ~2x the expected ~32 k (HIPER_POOLED_APPEND_CAP: tests of the
+// overflow fallback)
+static int32_t pooled_append_cap(int32_t k) {
+  if (const char* e = getenv("HIPER_POOLED_APPEND_CAP")) return std::max(k, atoi(e));
+  return std::max(4096, 64 * k);
+}
 static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t q_pad, int32_t k,
-                             int32_t world, bool with_comm, PooledWs& w) {
+                             int32_t world, bool with_comm, PooledWs& w, bool append = false) {
   size_t off = 0;
   w.status = off;
   off += 256;
@@ -1397,6 +1424,16 @@ static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t 
   off = align_up(off + (size_t)q_pad * 8, 256);
   w.pub8 = off;  // k > kPooledKP: [q_pad][n_parts] published 8th-best keys
   if (k > kPooledKP) off = align_up(off + (size_t)q_pad * std::max(n_parts, 1) * 8, 256);
+  w.thrk = off;  // APPEND: [n_q][k] the sample's top-k keys (T_q = the last)
+  w.cand = off;
+  w.ccnt = off;
+  if (append) {
+    off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
+    w.cand = off;  // [n_q][cap] candidate keys
+    off = align_up(off + (size_t)std::max(n_q, 1) * pooled_append_cap(k) * 8, 256);
+    w.ccnt = off;  // [n_q] candidate counts
+    off = align_up(off + (size_t)std::max(n_q, 1) * 4, 256);
+  }
   w.total = off;
 }
 
@@ -1405,15 +1442,18 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
                                   uint32_t flags, const hiper_comm* comm, void* workspace,
                                   size_t workspace_bytes, float* out_scores, int64_t* out_ids,
                                   float* dense_scores, cudaStream_t stream,
-                                  uint64_t* out_keys = nullptr) {
+                                  uint64_t* out_keys = nullptr, bool allow_append = true) {
   DevInfo di;
   TRY(device_info(di));
   PooledPlan pp;
   TRY(plan_pooled(di, n_q, ix->n, pp, dense_scores == nullptr, k));
   const int32_t world = comm ? comm->world : 1;
-  PooledWs w;
-  pooled_ws_layout(n_q, dim, pp.n_parts, pp.q_pad, dense_scores ? 1 : k, world, comm != nullptr, w);
   const bool glists = !dense_scores && k > kPooledKP;  // one shared list per query (see the kernel)
+  const bool append_ws = glists && pp.cl == 2 && pooled_append_sample(ix->n, k) > 0;
+  const int64_t sample = allow_append && append_ws ? pooled_append_sample(ix->n, k) : 0;
+  PooledWs w;
+  pooled_ws_layout(n_q, dim, pp.n_parts, pp.q_pad, dense_scores ? 1 : k, world, comm != nullptr, w,
+                   append_ws);
   TRY(check_ws(workspace, workspace_bytes, w.total));
   uint8_t* ws = (uint8_t*)workspace;
   uint32_t* status = (uint32_t*)(ws + w.status);
@@ -1449,6 +1489,70 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
       a.pub8 = (unsigned long long*)(ws + w.pub8);
       CUDA_TRY(cudaMemsetAsync(a.pub8, 0, (size_t)pp.q_pad * std::max(pp.n_parts, 1) * 8, stream));
     }
+  }
+  if (sample > 0) {
+    // APPEND: (1) the sample with the fast register kernel (per-(partition, group) top-16 lists, no
+    // shared pruning bound, so each list is its own sub-sample's exact top 16) -> T_q = the k-th key of
+    // the union of the lists: a k-th largest of real corpus keys, so at least k corpus keys are >= T_q;
+    // and as close to the sample's own k-th as long as no list holds more than 16 of its top k
+    alignas(64) CUtensorMap tq;
+    TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
+    PooledPlan p0;
+    TRY(plan_pooled(di, n_q, sample, p0, true, kPooledKP));
+    PooledArgs a0 = a;
+    a0.k = kPooledKP;
+    a0.n_ctiles = p0.n_ctiles;
+    a0.n_parts = p0.n_parts;
+    a0.n_stages = p0.n_stages;
+    a0.n_chunks = sample;
+    a0.gthr = nullptr;
+    a0.pub8 = nullptr;
+    TRY(launch_pooled<1>(p0, tq, ix->tmap, a0, stream));
+    uint64_t* thrk = (uint64_t*)(ws + w.thrk);
+    TRY(launch_merge(partial, p0.n_parts * kEpiGroups, (int64_t)p0.q_pad * kPooledKP, n_q, kPooledKP, k,
+                     thrk, nullptr, nullptr, stream, kPooledKP));
+    // (2) the whole corpus: every key >= T_q into the query's candidate buffer
+    PooledPlan p1;
+    TRY(plan_pooled(di, n_q, ix->n, p1, true, k, /*append=*/true));
+    PooledArgs a1 = a;
+    a1.n_stages = p1.n_stages;
+    a1.n_parts = p1.n_parts;
+    a1.gthr = nullptr;
+    a1.pub8 = nullptr;
+    const int32_t cap = pooled_append_cap(k);
+    uint32_t* ccnt = (uint32_t*)(ws + w.ccnt);
+    a1.cand = (uint64_t*)(ws + w.cand);
+    a1.cand_cnt = ccnt;
+    a1.cand_cap = cap;
+    a1.cand_thr = thrk + (k - 1);
+    a1.thr_stride = k;
+    CUDA_TRY(cudaMemsetAsync(ccnt, 0, (size_t)n_q * 4, stream));
+    if (a1.progress != nullptr)
+      CUDA_TRY(cudaMemsetAsync(ws + w.progress, 0xFF, w.qlens - w.progress, stream));  // "not started"
+    TRY(launch_pooled<1>(p1, tq, ix->tmap, a1, stream));
+    // (3) a warp per query: the top k of its buffer, as keys or decoded (this shard's, or the global
+    // answer after the all-gather)
+    uint64_t* local = (uint64_t*)(ws + w.local);
+    uint64_t* keys_to = out_keys ? out_keys : ((comm && comm->world > 1) ? local : nullptr);
+    const int blocks = (n_q + 7) / 8;
+#define HIPER_SELECT(KR)                                                                          \
+  cand_select_kernel<KR><<<blocks, 256, 0, stream>>>(a1.cand, ccnt, cap, n_q, k, keys_to,         \
+                                                     keys_to ? nullptr : out_scores,              \
+                                                     keys_to ? nullptr : out_ids, status)
+    if (k <= 32) HIPER_SELECT(1); else if (k <= 64) HIPER_SELECT(2); else HIPER_SELECT(4);
+#undef HIPER_SELECT
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    // a buffer that overflowed (the sample was unrepresentative) cannot be trusted: redo the batch on
+    // the heap path (one host sync per call on this path)
+    uint32_t h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (h & 16u)
+      return pooled_search(ix, q_tokens, dtype, q_lens, n_q, dim, k, flags, comm, workspace,
+                           workspace_bytes, out_scores, out_ids, dense_scores, stream, out_keys, false);
+    if (out_keys || !comm || comm->world == 1) return HIPER_OK;
+    return gather_merge(comm, local, (uint64_t*)(ws + w.gathered), n_q, k, out_scores, out_ids, stream);
   }
   if (ix->n > 0) {
     alignas(64) CUtensorMap tq;
@@ -1488,7 +1592,8 @@ static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, cons
   const int32_t ct = (int32_t)((ix->n + 255) / 256);
   PooledWs w;
   pooled_ws_layout(n_q, ix->dim, choose_parts(qt / (cl / 2), ct, num_sms / cl), qt * 256, k,
-                   comm ? comm->world : 1, comm != nullptr, w);
+                   comm ? comm->world : 1, comm != nullptr, w,
+                   topk && cl == 2 && pooled_append_sample(ix->n, k) > 0);
   return w.total;
 }
 

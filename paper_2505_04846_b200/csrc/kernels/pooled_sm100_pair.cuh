@@ -43,6 +43,14 @@ struct PooledArgs {
   // (atomicMax, monotone).  If m = ceil(k / 8) partitions each hold 8 keys >= T, at least k keys of the
   // corpus are >= T, so a key below the m-th largest pub8 value cannot be in the top k.
   unsigned long long* pub8;
+  // KP < 0 (APPEND, 16 < k <= 128): a per-query key bound T_q = cand_thr[q * thr_stride] (the k-th
+  // best key of a corpus sample, so at least k corpus keys are >= T_q) and every key >= T_q is
+  // appended to cand[q][0 .. cand_cap) (cand_cnt[q] counts them all, also past the capacity).
+  uint64_t* cand;
+  uint32_t* cand_cnt;
+  int32_t cand_cap;
+  const uint64_t* cand_thr;
+  int32_t thr_stride;
   unsigned long long* stats;  // pipeline statistics (HIPER_PIPE_STATS), or nullptr: [0] MMA cycles
                               // waiting for a free accumulator, [1] for a full stage, [2] MMA
                               // thread total, [3] epilogue drain cycles, [4] epilogue wait, [5] tiles
@@ -67,6 +75,10 @@ __device__ __forceinline__ float pooled_thr_score(uint64_t thr) {
 // the chunk operand costs half the L2 reads.  tmap_c then has a 64-row box.
 // STATS: HIPER_PIPE_STATS instrumentation compiled in (diagnostics only; see the MaxSim pair kernel).
 // KP > 0: each epilogue thread keeps its query's list in KP registers (k <= KP, the fast path).
+// KP < 0 (APPEND): no list at all -- a key that reaches the query's sample bound T_q is appended to
+// its global candidate buffer (one L2 atomic per candidate, ~32 k per query with a 1/32 sample);
+// cand_select_kernel takes the exact top-k from the buffer.  The tile scan is the fast path's
+// (block max, one compare) without the list upkeep, and no shared memory goes to heaps.
 // KP == 0 (16 < k <= 128): each query's (unit) list is a binary MIN-heap of k keys in shared memory
 // (root = the k-th best key so far = the filter threshold; empty slots are key 0, below every real key),
 // so an insertion is one root replacement and a log2(k)-level sift-down by the thread that owns the
@@ -283,6 +295,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           gth = T > gth ? T : gth;
         }
       }
+      if constexpr (KP < 0)  // APPEND: the static sample bound (a real key: its chunk is appended too)
+        gth = (q < args.n_q) ? args.cand_thr[(int64_t)q * args.thr_stride] : ~0ull;
       uint64_t lim = gth;         // max(thr, gth): only keys above it can enter
       const uint32_t mine0 = mine;  // this unit's first tile (KP == 0: refresh the bound often early)
       float thr_f = pooled_thr_score(lim);  // its score: most candidates fail one float compare
@@ -332,7 +346,23 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               for (int j = 0; j < 64; ++j)
                 hits |= (uint64_t)(__uint_as_float(r[j]) >= thr_f && j < nj) << j;
             }
-            if constexpr (KP == 0) {
+            if constexpr (KP < 0) {
+              if (hits) {  // rare: append the keys >= T_q (exact key test past the float filter)
+                float xs[64];
+#pragma unroll
+                for (int jj = 0; jj < 64; ++jj) xs[jj] = __uint_as_float(r[jj]) + 0.0f;
+                while (hits) {
+                  const int j = __ffsll((long long)hits) - 1;
+                  hits &= hits - 1;
+                  const uint64_t key = make_key(xs[j], args.id_base + cbase + col + j);
+                  if (key >= gth) {
+                    if (STATS && args.stats) ++st_ins;
+                    const uint32_t pos = atomicAdd(args.cand_cnt + q, 1u);
+                    if (pos < (uint32_t)args.cand_cap) args.cand[(int64_t)q * args.cand_cap + pos] = key;
+                  }
+                }
+              }
+            } else if constexpr (KP == 0) {
               if (hits) {  // rare: this thread's query heap, under its lock (shared with the other group)
                 float xs[64];
 #pragma unroll
@@ -428,7 +458,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           st_drain += clock64() - e1;
           ++st_tiles;
         }
-        if constexpr (MODE == 1) {
+        if constexpr (MODE == 1 && KP >= 0) {
           if (args.gthr != nullptr && q < args.q_pad) {
             if (thr > pub) {  // publish this list's k-th key; learn the others'
               const uint64_t old = atomicMax(args.gthr + q, (unsigned long long)thr);

@@ -20,14 +20,16 @@ __device__ __forceinline__ float key_score(uint64_t key) {
 __device__ __forceinline__ int64_t key_id(uint64_t key) { return (int64_t)(uint32_t)(~(uint32_t)key); }
 
 // One warp per query.  lists: list l of query q starts at lists + l*list_stride + q*q_stride and holds
-// k sorted keys.  Writes out_keys[q][k] (if not null) and/or decoded out_scores/out_ids [q][k].
+// list_len keys (any order; key 0 = empty).  Writes the k largest as out_keys[q][k] (if not null)
+// and/or decoded out_scores/out_ids [q][k].
 template <int KR>
 __global__ void __launch_bounds__(256) topk_merge_kernel(const uint64_t* __restrict__ lists,
                                                          int32_t n_lists, int64_t list_stride,
                                                          int32_t n_q, int64_t q_stride, int32_t k,
                                                          uint64_t* __restrict__ out_keys,
                                                          float* __restrict__ out_scores,
-                                                         int64_t* __restrict__ out_ids) {
+                                                         int64_t* __restrict__ out_ids,
+                                                         int32_t list_len) {
   const uint32_t lane = threadIdx.x & 31;
   const int32_t q = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (q >= n_q) return;
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(const uint64_t* __restr
 #pragma unroll
       for (int r = 0; r < KR; ++r) {
         const int i = r * 32 + (int)lane;
-        cand[u][r] = (l0 + u < n_lists && i < k) ? __ldcs(src + i) : 0ull;
+        cand[u][r] = (l0 + u < n_lists && i < list_len) ? __ldcs(src + i) : 0ull;
       }
     }
 #pragma unroll
@@ -58,6 +60,59 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(const uint64_t* __restr
           const uint64_t key = __shfl_sync(0xffffffffu, cand[u][r], srcl);
           if (key > top.thresh) top.insert(key, k, lane);
         }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < KR; ++r) {
+    const int i = r * 32 + (int)lane;
+    if (i < k) {
+      const uint64_t key = top.v[r];
+      const int64_t o = (int64_t)q * k + i;
+      if (out_keys) out_keys[o] = key;
+      if (out_scores) out_scores[o] = key ? key_score(key) : -INFINITY;
+      if (out_ids) out_ids[o] = key ? key_id(key) : -1;
+    }
+  }
+}
+
+// Pooled top-k, APPEND path (16 < k <= 128): query q's candidate buffer cand[q][0 .. n) with
+// n = min(cnt[q], cap) holds every corpus key >= its sample bound, hence its whole top-k; one warp per
+// query takes the k largest (32 keys per round, 8 rounds of loads in flight).  A query whose buffer
+// overflowed (cnt > cap) sets bit 4 of *status (the host then reruns the batch on the heap path).
+template <int KR>
+__global__ void __launch_bounds__(256) cand_select_kernel(const uint64_t* __restrict__ cand,
+                                                          const uint32_t* __restrict__ cnt, int32_t cap,
+                                                          int32_t n_q, int32_t k,
+                                                          uint64_t* __restrict__ out_keys,
+                                                          float* __restrict__ out_scores,
+                                                          int64_t* __restrict__ out_ids,
+                                                          uint32_t* __restrict__ status) {
+  const uint32_t lane = threadIdx.x & 31;
+  const int32_t q = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (q >= n_q) return;
+  const uint32_t c = cnt[q];
+  if (c > (uint32_t)cap && lane == 0) atomicOr(status, 16u);
+  const int32_t n = (int32_t)min(c, (uint32_t)cap);
+  const uint64_t* src = cand + (int64_t)q * cap;
+  WarpTopK<KR> top;
+  top.init();
+  constexpr int U = 8;
+  for (int32_t b0 = 0; b0 < n; b0 += 32 * U) {
+    uint64_t cv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t i = b0 + u * 32 + (int32_t)lane;
+      cv[u] = i < n ? __ldcs(src + i) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t mask = __ballot_sync(0xffffffffu, cv[u] > top.thresh);
+      while (mask) {
+        const int srcl = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const uint64_t key = __shfl_sync(0xffffffffu, cv[u], srcl);
+        if (key > top.thresh) top.insert(key, k, lane);
       }
     }
   }

@@ -72,6 +72,24 @@ def test_pooled_topk(H, k, kind):
         assert (i[:, 0] == gen.query_targets(12, Q, C, False) + 77).all()
 
 
+def test_pooled_topk_append_overflow_falls_back(H, monkeypatch):
+    """k > 16 on a corpus >= 32 k chunks takes the APPEND path (sample bound + candidate buffers);
+    a buffer too small for the candidates must trigger the heap-path rerun, with the same answer."""
+    C, Q, k = 6000, 40, 100
+    corp, q = case(C, Q, kind="iid")
+    idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32), flags=H.HIPER_POOLED)
+    s0, i0 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(idx, to_dev(q), np.ones(Q, np.int32), k)]
+    monkeypatch.setenv("HIPER_POOLED_APPEND_CAP", "100")   # = k: every query overflows
+    s1, i1 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(idx, to_dev(q), np.ones(Q, np.int32), k)]
+    assert np.array_equal(i0, i1) and np.array_equal(s0.view(np.uint32), s1.view(np.uint32))
+    lay = bits(idx.layout().clone())
+    S_o = oracle.maxsim_matrix(oracle.norm_rows(q[:, 0])[:, None], np.ones(Q, np.int32), lay,
+                               np.ones(C, np.int32))
+    ids = np.arange(C, dtype=np.int64)
+    for r in range(Q):
+        assert_topk_ok(s1[r], i1[r], S_o[r], ids, k, 1, D, f"append overflow q{r}")
+
+
 def test_pooled_edge_cases(H):
     corp, q = case(3, 5)
     idx = H.hiper_index_build(to_dev(corp), np.ones(3, np.int32), flags=H.HIPER_POOLED)
