@@ -1393,15 +1393,18 @@ struct PooledWs {
 static int64_t pooled_append_sample(int64_t n_chunks, int32_t k) {
   static const bool off = getenv("HIPER_POOLED_APPEND") && getenv("HIPER_POOLED_APPEND")[0] == '0';
   if (off || k <= kPooledKP) return 0;
-  int64_t s = std::max<int64_t>(n_chunks / 32, 8 * (int64_t)k);
+  static const int64_t div = getenv("HIPER_POOLED_SAMPLE_DIV") ? atoll(getenv("HIPER_POOLED_SAMPLE_DIV")) : 32;
+  int64_t s = std::max<int64_t>(n_chunks / std::max<int64_t>(div, 4), 8 * (int64_t)k);
   s = (s + 255) / 256 * 256;
   return s * 4 <= n_chunks ? s : 0;
 }
-// candidate buffer slots per query: ~2x the expected ~32 k (HIPER_POOLED_APPEND_CAP: tests of the
-// overflow fallback)
-static int32_t pooled_append_cap(int32_t k) {
-  if (const char* e = getenv("HIPER_POOLED_APPEND_CAP")) return std::max(k, atoi(e));
-  return std::max(4096, 64 * k);
+// candidate slots per (query, partition, group) segment: 3x the expected k * div / (2P) + 16
+// (HIPER_POOLED_APPEND_CAP: tests of the overflow fallback)
+static int32_t pooled_append_cap(int32_t k, int32_t n_parts) {
+  if (const char* e = getenv("HIPER_POOLED_APPEND_CAP")) return std::max(1, atoi(e));
+  static const int64_t div = getenv("HIPER_POOLED_SAMPLE_DIV") ? atoll(getenv("HIPER_POOLED_SAMPLE_DIV")) : 32;
+  const int64_t e = (int64_t)k * std::max<int64_t>(div, 4) / (2 * std::max(n_parts, 1));
+  return (int32_t)std::max<int64_t>(32, (3 * e + 16 + 7) / 8 * 8);
 }
 static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t q_pad, int32_t k,
                              int32_t world, bool with_comm, PooledWs& w, bool append = false) {
@@ -1429,10 +1432,11 @@ static void pooled_ws_layout(int32_t n_q, int32_t dim, int32_t n_parts, int32_t 
   w.ccnt = off;
   if (append) {
     off = align_up(off + (size_t)std::max(n_q, 1) * k * 8, 256);
-    w.cand = off;  // [n_q][cap] candidate keys
-    off = align_up(off + (size_t)std::max(n_q, 1) * pooled_append_cap(k) * 8, 256);
-    w.ccnt = off;  // [n_q] candidate counts
-    off = align_up(off + (size_t)std::max(n_q, 1) * 4, 256);
+    const size_t segs = (size_t)std::max(n_q, 1) * std::max(n_parts, 1) * kEpiGroups;
+    w.cand = off;  // [n_q][P][2][cap] candidate keys, one segment per unit thread
+    off = align_up(off + segs * pooled_append_cap(k, n_parts) * 8, 256);
+    w.ccnt = off;  // [n_q][P][2] segment counts
+    off = align_up(off + segs * 4, 256);
   }
   w.total = off;
 }
@@ -1519,14 +1523,14 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
     a1.n_parts = p1.n_parts;
     a1.gthr = nullptr;
     a1.pub8 = nullptr;
-    const int32_t cap = pooled_append_cap(k);
+    if (p1.n_parts != pp.n_parts) return fail(HIPER_ERR_UNSUPPORTED, "APPEND partition plan mismatch");
+    const int32_t cap = pooled_append_cap(k, p1.n_parts);
     uint32_t* ccnt = (uint32_t*)(ws + w.ccnt);
     a1.cand = (uint64_t*)(ws + w.cand);
-    a1.cand_cnt = ccnt;
+    a1.cand_cnt = ccnt;  // every (q < n_q, p, g) count is written by its unit thread
     a1.cand_cap = cap;
     a1.cand_thr = thrk + (k - 1);
     a1.thr_stride = k;
-    CUDA_TRY(cudaMemsetAsync(ccnt, 0, (size_t)n_q * 4, stream));
     if (a1.progress != nullptr)
       CUDA_TRY(cudaMemsetAsync(ws + w.progress, 0xFF, w.qlens - w.progress, stream));  // "not started"
     TRY(launch_pooled<1>(p1, tq, ix->tmap, a1, stream));
@@ -1536,7 +1540,8 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
     uint64_t* keys_to = out_keys ? out_keys : ((comm && comm->world > 1) ? local : nullptr);
     const int blocks = (n_q + 7) / 8;
 #define HIPER_SELECT(KR)                                                                          \
-  cand_select_kernel<KR><<<blocks, 256, 0, stream>>>(a1.cand, ccnt, cap, n_q, k, keys_to,         \
+  cand_select_kernel<KR><<<blocks, 256, 0, stream>>>(a1.cand, ccnt, p1.n_parts * kEpiGroups, cap, \
+                                                     n_q, k, keys_to,                              \
                                                      keys_to ? nullptr : out_scores,              \
                                                      keys_to ? nullptr : out_ids, status)
     if (k <= 32) HIPER_SELECT(1); else if (k <= 64) HIPER_SELECT(2); else HIPER_SELECT(4);

@@ -44,8 +44,10 @@ struct PooledArgs {
   // corpus are >= T, so a key below the m-th largest pub8 value cannot be in the top k.
   unsigned long long* pub8;
   // KP < 0 (APPEND, 16 < k <= 128): a per-query key bound T_q = cand_thr[q * thr_stride] (the k-th
-  // best key of a corpus sample, so at least k corpus keys are >= T_q) and every key >= T_q is
-  // appended to cand[q][0 .. cand_cap) (cand_cnt[q] counts them all, also past the capacity).
+  // best key of a corpus sample, so at least k corpus keys are >= T_q); every key >= T_q is appended
+  // to the segment of (query q, partition p, group g): cand[(q * P + p) * 2 + g][0 .. cand_cap), owned
+  // by that unit's thread (no atomics); cand_cnt[(q * P + p) * 2 + g] = its count, also past the
+  // capacity (the host then reruns on the heap path).
   uint64_t* cand;
   uint32_t* cand_cnt;
   int32_t cand_cap;
@@ -297,6 +299,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
       }
       if constexpr (KP < 0)  // APPEND: the static sample bound (a real key: its chunk is appended too)
         gth = (q < args.n_q) ? args.cand_thr[(int64_t)q * args.thr_stride] : ~0ull;
+      uint32_t n_app = 0;  // APPEND: keys this thread appended to its (q, p, grp) segment
+      uint64_t* seg = args.cand + (((int64_t)q * args.n_parts + p) * kEpiGroups + grp) * args.cand_cap;
       uint64_t lim = gth;         // max(thr, gth): only keys above it can enter
       const uint32_t mine0 = mine;  // this unit's first tile (KP == 0: refresh the bound often early)
       float thr_f = pooled_thr_score(lim);  // its score: most candidates fail one float compare
@@ -357,8 +361,8 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
                   const uint64_t key = make_key(xs[j], args.id_base + cbase + col + j);
                   if (key >= gth) {
                     if (STATS && args.stats) ++st_ins;
-                    const uint32_t pos = atomicAdd(args.cand_cnt + q, 1u);
-                    if (pos < (uint32_t)args.cand_cap) args.cand[(int64_t)q * args.cand_cap + pos] = key;
+                    if (n_app < (uint32_t)args.cand_cap) seg[n_app] = key;
+                    ++n_app;
                   }
                 }
               }
@@ -483,6 +487,9 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
             }
           }
         }
+      }
+      if constexpr (MODE == 1 && KP < 0) {
+        if (q < args.n_q) args.cand_cnt[((int64_t)q * args.n_parts + p) * kEpiGroups + grp] = n_app;
       }
       if constexpr (MODE == 1 && KP > 0) {
         if (q < args.n_q) {

@@ -76,14 +76,15 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(const uint64_t* __restr
   }
 }
 
-// Pooled top-k, APPEND path (16 < k <= 128): query q's candidate buffer cand[q][0 .. n) with
-// n = min(cnt[q], cap) holds every corpus key >= its sample bound, hence its whole top-k; one warp per
-// query takes the k largest (32 keys per round, 8 rounds of loads in flight).  A query whose buffer
-// overflowed (cnt > cap) sets bit 4 of *status (the host then reruns the batch on the heap path).
+// Pooled top-k, APPEND path (16 < k <= 128): query q's n_seg candidate segments (one per (partition,
+// group) unit thread: cand[q * n_seg + s][0 .. min(cnt, cap))) hold every corpus key >= its sample
+// bound, hence its whole top-k; one warp per query takes the k largest, lane l walking segment l
+// of each group of 32.  A segment
+// that overflowed (cnt > cap) sets bit 4 of *status (the host then reruns the batch on the heap path).
 template <int KR>
 __global__ void __launch_bounds__(256) cand_select_kernel(const uint64_t* __restrict__ cand,
-                                                          const uint32_t* __restrict__ cnt, int32_t cap,
-                                                          int32_t n_q, int32_t k,
+                                                          const uint32_t* __restrict__ cnt, int32_t n_seg,
+                                                          int32_t cap, int32_t n_q, int32_t k,
                                                           uint64_t* __restrict__ out_keys,
                                                           float* __restrict__ out_scores,
                                                           int64_t* __restrict__ out_ids,
@@ -91,31 +92,37 @@ __global__ void __launch_bounds__(256) cand_select_kernel(const uint64_t* __rest
   const uint32_t lane = threadIdx.x & 31;
   const int32_t q = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (q >= n_q) return;
-  const uint32_t c = cnt[q];
-  if (c > (uint32_t)cap && lane == 0) atomicOr(status, 16u);
-  const int32_t n = (int32_t)min(c, (uint32_t)cap);
-  const uint64_t* src = cand + (int64_t)q * cap;
   WarpTopK<KR> top;
   top.init();
-  constexpr int U = 8;
-  for (int32_t b0 = 0; b0 < n; b0 += 32 * U) {
-    uint64_t cv[U];
+  bool over = false;
+  // 32 segments at a time, lane l walking segment s0 + l: 4 independent loads per lane per round
+  for (int32_t s0 = 0; s0 < n_seg; s0 += 32) {
+    const bool live = s0 + (int32_t)lane < n_seg;
+    const uint32_t my_c = live ? __ldg(cnt + (int64_t)q * n_seg + s0 + lane) : 0u;
+    over |= my_c > (uint32_t)cap;
+    const int32_t my_n = (int32_t)min(my_c, (uint32_t)cap);
+    int32_t mx = my_n;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int32_t i = b0 + u * 32 + (int32_t)lane;
-      cv[u] = i < n ? __ldcs(src + i) : 0ull;
-    }
+    for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const uint64_t* src = cand + ((int64_t)q * n_seg + s0 + (live ? (int32_t)lane : 0)) * cap;
+    constexpr int U = 4;
+    for (int32_t i0 = 0; i0 < mx; i0 += U) {
+      uint64_t cv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      uint32_t mask = __ballot_sync(0xffffffffu, cv[u] > top.thresh);
-      while (mask) {
-        const int srcl = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const uint64_t key = __shfl_sync(0xffffffffu, cv[u], srcl);
-        if (key > top.thresh) top.insert(key, k, lane);
+      for (int u = 0; u < U; ++u) cv[u] = i0 + u < my_n ? __ldcs(src + i0 + u) : 0ull;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t mask = __ballot_sync(0xffffffffu, cv[u] > top.thresh);
+        while (mask) {
+          const int srcl = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const uint64_t key = __shfl_sync(0xffffffffu, cv[u], srcl);
+          if (key > top.thresh) top.insert(key, k, lane);
+        }
       }
     }
   }
+  if (__any_sync(0xffffffffu, over) && lane == 0) atomicOr(status, 16u);
 #pragma unroll
   for (int r = 0; r < KR; ++r) {
     const int i = r * 32 + (int)lane;

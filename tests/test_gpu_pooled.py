@@ -79,7 +79,7 @@ def test_pooled_topk_append_overflow_falls_back(H, monkeypatch):
     corp, q = case(C, Q, kind="iid")
     idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32), flags=H.HIPER_POOLED)
     s0, i0 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(idx, to_dev(q), np.ones(Q, np.int32), k)]
-    monkeypatch.setenv("HIPER_POOLED_APPEND_CAP", "100")   # = k: every query overflows
+    monkeypatch.setenv("HIPER_POOLED_APPEND_CAP", "1")   # one slot per segment: overflows
     s1, i1 = [t.cpu().numpy() for t in H.hiper_maxsim_topk(idx, to_dev(q), np.ones(Q, np.int32), k)]
     assert np.array_equal(i0, i1) and np.array_equal(s0.view(np.uint32), s1.view(np.uint32))
     lay = bits(idx.layout().clone())
