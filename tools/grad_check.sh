@@ -1,3 +1,4 @@
+# N1 backward: grad/debug GPU tests, two config2 --grad bench lines, warm launch list of the step
 python __graft_entry__.py > gpurun_out/build.log 2>&1 || tail -20 gpurun_out/build.log
 timeout 600 python -m pytest tests -q -m gpu -x -p no:cacheprovider -k "grad or debug" > gpurun_out/pytest_grad.log 2>&1; tail -3 gpurun_out/pytest_grad.log
 for i in 1 2; do

@@ -1,3 +1,4 @@
+# N2 full loss: coltrast GPU tests, then peer-window vs NCCL gather at N = 2 (run under gpurun --gpus 2)
 python __graft_entry__.py > gpurun_out/build.log 2>&1
 timeout 600 python -m pytest tests -q -m gpu -x -k "coltrast" -p no:cacheprovider > gpurun_out/pytest_n2.log 2>&1; tail -2 gpurun_out/pytest_n2.log
 R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1"

@@ -1,3 +1,4 @@
+# pooled k > 16 heap path with the pub8 bound: tests + probe_pooled_k timings at k = 10, 100, 128
 python __graft_entry__.py > gpurun_out/build.log 2>&1
 timeout 600 python -m pytest tests -q -m gpu -x -p no:cacheprovider -k "pooled or rerank or shard_merge" 2>&1 | tail -2
 KS=10,100,128 timeout 300 python tools/probe_pooled_k.py
