@@ -2263,7 +2263,8 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     CUDA_TRY(cudaGetLastError());
     const int64_t fwarps = (int64_t)n_d * ((d_max_len + 3) / 4);  // 4 rows per warp
     grad_d_finish_kernel<VPL, Tin><<<(unsigned)((fwarps + 7) / 8), 256, 0, stream>>>(
-        bkt, w.S, w.n_seg, scr, n_d, (const Tin*)d_tokens, d_max_len, an, grad_d);
+        bkt, __builtin_ctz((unsigned)w.S), w.n_seg, scr, n_d, (const Tin*)d_tokens, d_max_len, dlens_dev,
+        an, grad_d);
     CUDA_TRY(cudaGetLastError());
     g_launches += 4;
     return HIPER_OK;

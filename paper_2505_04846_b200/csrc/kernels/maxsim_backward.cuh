@@ -312,6 +312,31 @@ __global__ void __launch_bounds__(kSortWarps * 32) grad_d_sort_kernel(
   for (int32_t x = threadIdx.x; x <= NB; x += blockDim.x) base_out[(int64_t)j * (NB + 1) + x] = base[x];
 }
 
+// VPL consecutive values (8- or 16-byte aligned) as floats, one vector load.
+template <int VPL>
+__device__ __forceinline__ void load_vec(const float* p, float (&x)[VPL]) {
+  if constexpr (VPL == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+  } else {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    x[0] = t.x; x[1] = t.y;
+  }
+}
+template <int VPL>
+__device__ __forceinline__ void load_vec(const __nv_bfloat16* p, float (&x)[VPL]) {
+  if constexpr (VPL == 4) {
+    const uint2 t = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.y));
+    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+  } else {
+    const uint32_t t = *reinterpret_cast<const uint32_t*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t));
+    x[0] = a.x; x[1] = a.y;
+  }
+}
+
 template <int VPL>
 struct RawRow;  // one lane's VPL bf16 values of a row, as raw words
 template <>
@@ -418,39 +443,14 @@ __global__ void __launch_bounds__(256, 2) grad_d_seg_kernel(
   flush();  // the segment's last row (it ends at hi, or continues past it)
 }
 
-// VPL consecutive values (8- or 16-byte aligned) as floats, one vector load.
-template <int VPL>
-__device__ __forceinline__ void load_vec(const float* p, float (&x)[VPL]) {
-  if constexpr (VPL == 4) {
-    const float4 t = *reinterpret_cast<const float4*>(p);
-    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
-  } else {
-    const float2 t = *reinterpret_cast<const float2*>(p);
-    x[0] = t.x; x[1] = t.y;
-  }
-}
-template <int VPL>
-__device__ __forceinline__ void load_vec(const __nv_bfloat16* p, float (&x)[VPL]) {
-  if constexpr (VPL == 4) {
-    const uint2 t = *reinterpret_cast<const uint2*>(p);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t.y));
-    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
-  } else {
-    const uint32_t t = *reinterpret_cast<const uint32_t*>(p);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t));
-    x[0] = a.x; x[1] = a.y;
-  }
-}
-
 // grad_d, pass 3 -- one warp per FR output rows (j, u .. u + FR - 1), their loads issued together:
 // g_d(j, u) is 0 (no hit), the row pass 2 wrote (one segment), or the sum of its segments' partials in
 // segment order; then NORM's Jacobian.
 template <int VPL, typename Tin>
 __global__ void __launch_bounds__(256) grad_d_finish_kernel(
-    const int32_t* __restrict__ base, int32_t S, int32_t n_seg, const float* __restrict__ scratch,
-    int32_t M, const Tin* __restrict__ xd, int32_t d_max_len, uint32_t assume_normalized,
-    float* __restrict__ grad_d) {
+    const int32_t* __restrict__ base, int32_t log2S, int32_t n_seg, const float* __restrict__ scratch,
+    int32_t M, const Tin* __restrict__ xd, int32_t d_max_len, const int32_t* __restrict__ d_lens,
+    uint32_t assume_normalized, float* __restrict__ grad_d) {
   constexpr int D = VPL * 32;
   constexpr int NB = 257;
   constexpr int FR = 4;
@@ -460,40 +460,44 @@ __global__ void __launch_bounds__(256) grad_d_finish_kernel(
   if (w >= (int64_t)M * wpd) return;
   const int32_t j = (int32_t)(w / wpd), u0 = (int32_t)(w - (int64_t)j * wpd) * FR;
   const int32_t* bj = base + (int64_t)j * (NB + 1);
+  const int32_t lj = __ldg(d_lens + j);
   int32_t rs[FR + 1];
 #pragma unroll
   for (int k = 0; k <= FR; ++k) rs[k] = __ldg(bj + min(u0 + k, NB));
+  // every row's g and x loads issue together (unconditionally: a row without hits reads a stale
+  // g it then ignores); the crossing rows' partials follow
   float g[FR][VPL];
   float x[FR][VPL];
 #pragma unroll
   for (int k = 0; k < FR; ++k) {
-    const int32_t u = u0 + k;
-    const int64_t row = (int64_t)j * d_max_len + u;
+    const int64_t row = (int64_t)j * d_max_len + min(u0 + k, d_max_len - 1);
+    load_vec<VPL>(grad_d + row * D + lane * VPL, g[k]);
+    if (!assume_normalized) load_vec<VPL>(xd + row * D + lane * VPL, x[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < FR; ++k) {
+    if (rs[k + 1] == rs[k]) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) g[k][v] = 0.0f;
+      continue;
+    }
+    const int32_t s0 = rs[k] >> log2S, s1 = (rs[k + 1] - 1) >> log2S;
+    if (s0 == s1) continue;
+    // partials in segment order, 4 loads in flight (a missing one adds an exact +0)
 #pragma unroll
     for (int v = 0; v < VPL; ++v) g[k][v] = 0.0f;
-    if (u < d_max_len) {
-      if (!assume_normalized) load_vec<VPL>(xd + row * D + lane * VPL, x[k]);
-      if (rs[k + 1] > rs[k]) {
-        const int32_t s0 = rs[k] / S, s1 = (rs[k + 1] - 1) / S;
-        if (s0 == s1) {
-          load_vec<VPL>(grad_d + row * D + lane * VPL, g[k]);
-        } else {
-          // partials in segment order, 4 loads in flight (a missing one adds an exact +0)
-          const float* sl = scratch + (int64_t)j * n_seg * 2 * D + lane * VPL;
-          for (int32_t ss = s0; ss <= s1; ss += 4) {
-            float p[4][VPL];
+    const float* sl = scratch + (int64_t)j * n_seg * 2 * D + lane * VPL;
+    for (int32_t ss = s0; ss <= s1; ss += 4) {
+      float pq[4][VPL];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-              for (int v = 0; v < VPL; ++v)
-                p[q][v] = ss + q <= s1 ? sl[((int64_t)(ss + q) * 2 + (ss + q > s0 ? 0 : 1)) * D + v] : 0.0f;
+        for (int v = 0; v < VPL; ++v)
+          pq[q][v] = ss + q <= s1 ? sl[((int64_t)(ss + q) * 2 + (ss + q > s0 ? 0 : 1)) * D + v] : 0.0f;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-              for (int v = 0; v < VPL; ++v) g[k][v] += p[q][v];
-          }
-        }
-      }
+        for (int v = 0; v < VPL; ++v) g[k][v] += pq[q][v];
     }
   }
 #pragma unroll
@@ -501,6 +505,11 @@ __global__ void __launch_bounds__(256) grad_d_finish_kernel(
     const int32_t u = u0 + k;
     if (u >= d_max_len) break;
     float* out = grad_d + ((int64_t)j * d_max_len + u) * D + lane * VPL;
+    if (u >= lj) {  // padding rows: exactly 0 (their raw x may be anything, even 0)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) out[v] = 0.0f;
+      continue;
+    }
     if (assume_normalized) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v) out[v] = g[k][v];

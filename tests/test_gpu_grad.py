@@ -74,3 +74,27 @@ def test_li_backward_matches_oracle(H, n_q, n_d, Lq, Ld, d, dtype, tau, kind):
         assert (gq[i, ql[i]:] == 0).all()
     for j in range(n_d):
         assert (gd[j, dl[j]:] == 0).all()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_li_backward_zero_padding_rows(H, dtype):
+    """Raw inputs whose padding rows are ZERO (norm 0: NORM's Jacobian would divide by 0 there):
+    both gradients stay finite, padding rows exactly 0, real rows equal to the run with non-zero
+    padding (padding never enters the forward)."""
+    n_q, n_d, Lq, Ld, d = 20, 24, 32, 160, 128
+    corp = gen.corpus(73, 0, n_d, Ld, d, dtype=dtype)
+    dl = gen.lengths(73, n_d, Ld, True)
+    q = gen.queries(74, n_q, Lq, d, corpus_seed=73, n_chunks=n_d, L=Ld, chunk_lens_fn=lambda c: dl[c],
+                    dtype=dtype, diagonal=True)
+    ql = gen.lengths(74, n_q, Lq, True, stream=gen.QLEN)
+    ref = H.hiper_coltrast_scores_loss_grad(to_dev(q), ql, to_dev(corp), dl)
+    qz, cz = q.copy(), corp.copy()
+    for i in range(n_q):
+        qz[i, ql[i]:] = 0
+    for j in range(n_d):
+        cz[j, dl[j]:] = 0
+    got = H.hiper_coltrast_scores_loss_grad(to_dev(qz), ql, to_dev(cz), dl)
+    for a, b in zip(ref, got):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.isfinite(b).all()
+        assert np.array_equal(a, b)
