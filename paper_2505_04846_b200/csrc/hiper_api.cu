@@ -26,6 +26,7 @@
 #include "kernels/maxsim_backward.cuh"
 #include "kernels/maxsim_sm100_pair.cuh"
 #include "kernels/pooled_sm100_pair.cuh"
+#include "kernels/pooled_cs_sm100.cuh"
 #include "kernels/rerank_gather.cuh"
 #include "kernels/peer_gather.cuh"
 #include "kernels/norm_layout.cuh"
@@ -140,16 +141,19 @@ static hiper_status get_encode_fn(PFN_encodeTiled* fn) {
 }
 
 // 2-D bf16 tensor map over rows of `dim` elements, box = 64 elements x box_rows rows, 128B swizzle.
+// box_cols = 64 (128-B rows, SWIZZLE_128B) or 32 (64-B rows, SWIZZLE_64B: the chunk-stationary
+// pooled kernel's query stages)
 static hiper_status make_tmap(CUtensorMap* map, const void* base, int64_t rows, int32_t dim,
-                              int32_t box_rows) {
+                              int32_t box_rows, int32_t box_cols = 64) {
   PFN_encodeTiled enc;
   TRY(get_encode_fn(&enc));
   cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)dim * 2};
-  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(HIPER_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld dim=%d box_rows=%d",
@@ -1380,6 +1384,96 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   return HIPER_OK;
 }
 
+// a12 with the chunk tile stationary (kernels/pooled_cs_sm100.cuh): every pair owns a contiguous
+// range of chunk tiles and streams all query tiles against each.  Exact and tested, but measured
+// slower than the streaming kernel at config 5 (0.78 vs 0.81 of burst, same box: the query feed from
+// L2 with <= 3 stages beside the resident tile; profiles/r02/ablation/pooled_cs.txt), so it is
+// opt-in: HIPER_POOLED_CS=2 uses it for the register top-k (k <= kPooledKP) when the resident tile
+// leaves >= 2 query stages and every pair gets >= 2 chunk tiles, =1 forces it on any corpus (tests:
+// min(pairs, chunk tiles) pairs).  HIPER_POOLED_CS_N = chunk tile width (default 224, the best
+// measured), HIPER_POOLED_CS_A = query stage width 32 | 64 (default 64).
+struct PooledCsPlan {
+  bool use = false;
+  int32_t n_parts = 0, n_stages = 0, two_slots = 0, tile_n = 256, n_ctiles = 0, a_cols = 32;
+  uint32_t smem_bytes = 0;
+  int grid = 0;
+};
+static void plan_pooled_cs(int num_sms, int max_smem, int32_t n_q, int64_t n_chunks, int32_t dim,
+                           int32_t k, bool topk, PooledCsPlan& cp) {
+  cp = PooledCsPlan{};
+  const char* e = getenv("HIPER_POOLED_CS");
+  const int mode = e ? atoi(e) : 0;  // 0 off, 1 forced, 2 auto
+  if (mode == 0 || !topk || k > kPooledKP || pooled_cluster(true) != 2 || n_chunks <= 0) return;
+  const int64_t nkb = num_kb_of(dim);
+  const char* en = getenv("HIPER_POOLED_CS_N");
+  const int64_t tn = en ? std::max(16, std::min(256, atoi(en) / 16 * 16)) : 224;
+  const char* ea = getenv("HIPER_POOLED_CS_A");
+  const int64_t ac = (ea && atoi(ea) == 32) ? 32 : 64;
+  const int64_t fixed = 1024 + 1024;  // align slack, barriers + TMEM pointer
+  const int64_t avail = (int64_t)max_smem - fixed - nkb * tn * 64;
+  const int64_t S = std::min<int64_t>(12, avail / (256 * ac));
+  const int32_t pairs = num_sms / 2;
+  const int64_t ct = (n_chunks + tn - 1) / tn;
+  if (S < (ac == 64 ? 2 : 3) || (mode == 2 && ct < 2 * (int64_t)pairs)) return;
+  const int32_t nqt = (int32_t)((std::max(n_q, 1) + 255) / 256);
+  cp.use = true;
+  cp.n_parts = (int32_t)std::min<int64_t>(pairs, ct);
+  cp.n_stages = (int32_t)S;
+  cp.two_slots = (nqt & 1) ? 1 : 0;
+  cp.tile_n = (int32_t)tn;
+  cp.a_cols = (int32_t)ac;
+  cp.n_ctiles = (int32_t)ct;
+  cp.smem_bytes = (uint32_t)(fixed + nkb * tn * 64 + S * 256 * ac);
+  cp.grid = 2 * cp.n_parts;
+}
+
+static hiper_status launch_pooled_cs(const PooledCsPlan& cp, const CUtensorMap& tq32,
+                                     const CUtensorMap& tc, const PooledCsArgs& a, cudaStream_t stream) {
+  static const bool stats_on = getenv("HIPER_PIPE_STATS") != nullptr;
+  auto kern = cp.a_cols == 64
+                  ? (stats_on ? pooled_cs_sm100_kernel<kPooledKP, 64, true> : pooled_cs_sm100_kernel<kPooledKP, 64>)
+                  : (stats_on ? pooled_cs_sm100_kernel<kPooledKP, 32, true> : pooled_cs_sm100_kernel<kPooledKP, 32>);
+  CUDA_TRY(set_max_smem((const void*)kern, (int)cp.smem_bytes));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cp.grid);
+  cfg.blockDim = dim3(kMaxsimThreads);
+  cfg.dynamicSmemBytes = cp.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  unsigned long long* st = nullptr;
+  PooledCsArgs b = a;
+  if (stats_on) {
+    CUDA_TRY(cudaMalloc(&st, 16 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(st, 0, 16 * sizeof(unsigned long long), stream));
+    b.stats = st;
+  }
+  ProfTicket ev;
+  TRY(profile_begin(stream, HIPER_PROF_POOLED, &ev));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tq32, tc, b));
+  TRY(profile_end(stream, ev));
+  ++g_launches;
+  if (st) {
+    unsigned long long h[16];
+    CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    cudaFree(st);
+    const double pairs = cp.grid / 2.0, ep = 8.0 * cp.grid;
+    fprintf(stderr, "[hiper pipe] pooled_cs: MMA thread %.0f cyc avg; waits acc %.1f%% A %.1f%% B %.1f%%; "
+            "epilogue drain %.0f cyc/tile, wait %.0f cyc/tile, tiles/warp %.0f; per thread-tile: "
+            "blocks past the threshold %.3f, list loads %.3f\n",
+            h[2] / pairs, 100.0 * h[0] / h[2], 100.0 * h[1] / h[2], 100.0 * h[6] / h[2],
+            (double)h[3] / h[5], (double)h[4] / h[5], h[5] / ep, (double)h[7] / (32.0 * h[5]),
+            (double)h[8] / (32.0 * h[5]));
+  }
+  return HIPER_OK;
+}
+
 struct PooledWs {
   size_t status = 0, progress = 0, qlens = 0, qlayout = 0, partial = 0, local = 0, gathered = 0,
          gthr = 0, pub8 = 0, thrk = 0, cand = 0, ccnt = 0, total = 0;
@@ -1451,13 +1545,15 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   TRY(device_info(di));
   PooledPlan pp;
   TRY(plan_pooled(di, n_q, ix->n, pp, dense_scores == nullptr, k));
+  PooledCsPlan cp;
+  plan_pooled_cs(di.num_sms, di.max_smem, n_q, ix->n, dim, k, dense_scores == nullptr, cp);
   const int32_t world = comm ? comm->world : 1;
   const bool glists = !dense_scores && k > kPooledKP;  // one shared list per query (see the kernel)
   const bool append_ws = glists && pp.cl == 2 && pooled_append_sample(ix->n, k) > 0;
   const int64_t sample = allow_append && append_ws ? pooled_append_sample(ix->n, k) : 0;
   PooledWs w;
-  pooled_ws_layout(n_q, dim, pp.n_parts, pp.q_pad, dense_scores ? 1 : k, world, comm != nullptr, w,
-                   append_ws);
+  pooled_ws_layout(n_q, dim, std::max(pp.n_parts, cp.n_parts), pp.q_pad, dense_scores ? 1 : k, world,
+                   comm != nullptr, w, append_ws);
   TRY(check_ws(workspace, workspace_bytes, w.total));
   uint8_t* ws = (uint8_t*)workspace;
   uint32_t* status = (uint32_t*)(ws + w.status);
@@ -1563,7 +1659,29 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
     alignas(64) CUtensorMap tq;
     TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
     if (dense_scores) return launch_pooled<0>(pp, tq, ix->tmap, a, stream);
-    if (pp.cl == 4) {  // chunk halves of 64 rows, multicast to both pairs of a cluster
+    if (cp.use) {
+      alignas(64) CUtensorMap tq32, tcn;
+      TRY(make_tmap(&tq32, qlayout, n_q, dim, 128, cp.a_cols));
+      TRY(make_tmap(&tcn, ix->tok, ix->n, dim, cp.tile_n / 2));
+      PooledCsArgs c{};
+      c.n_q = n_q;
+      c.n_qtiles = pp.n_qtiles;
+      c.n_ctiles = cp.n_ctiles;
+      c.tile_n = cp.tile_n;
+      c.a_cols = cp.a_cols;
+      c.dbg = getenv("HIPER_POOLED_CS_DBG") ? atoi(getenv("HIPER_POOLED_CS_DBG")) : 0;
+      c.n_parts = cp.n_parts;
+      c.num_kb = num_kb_of(dim);
+      c.k = k;
+      c.n_stages = cp.n_stages;
+      c.q_pad = pp.q_pad;
+      c.two_slots = cp.two_slots;
+      c.n_chunks = ix->n;
+      c.id_base = ix->id_base;
+      c.partial = partial;
+      c.gthr = a.gthr;
+      TRY(launch_pooled_cs(cp, tq32, tcn, c, stream));
+    } else if (pp.cl == 4) {  // chunk halves of 64 rows, multicast to both pairs of a cluster
       alignas(64) CUtensorMap tc64;
       TRY(make_tmap(&tc64, ix->tok, ix->n, dim, 64));
       TRY(launch_pooled<1>(pp, tq, tc64, a, stream));
@@ -1573,8 +1691,11 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   }
   // the per-(partition, group) lists; k > kPooledKP: one (shared-heap) list per partition, in the
   // group-0 slot of each partition
-  const int32_t n_lists = ix->n > 0 ? (glists ? pp.n_parts : pp.n_parts * kEpiGroups) : 0;
-  const int64_t list_stride = (int64_t)pp.q_pad * k * (glists ? kEpiGroups : 1);
+  // chunk-stationary kernel: lists [pair][slot] (slot 0 only when the query tiles are even)
+  const bool one_slot = glists || (cp.use && !cp.two_slots);
+  const int32_t n_lists =
+      ix->n > 0 ? (cp.use ? cp.n_parts : pp.n_parts) * (one_slot ? 1 : kEpiGroups) : 0;
+  const int64_t list_stride = (int64_t)pp.q_pad * k * (one_slot ? kEpiGroups : 1);
   if (out_keys)  // this shard's top-k keys (a8's all-gather payload)
     return launch_merge(partial, n_lists, list_stride, n_q, k, k, out_keys, nullptr, nullptr, stream);
   if (!comm || comm->world == 1)
@@ -1595,8 +1716,15 @@ static size_t pooled_ws_size(const hiper_index* ix, int32_t n_q, int32_t k, cons
   const int cl = pooled_cluster(topk);
   const int32_t qt = pooled_qtiles(n_q, cl);
   const int32_t ct = (int32_t)((ix->n + 255) / 256);
+  int max_smem = 0;
+  if (cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix->device) != cudaSuccess) {
+    cudaGetLastError();
+    max_smem = 232448;
+  }
+  PooledCsPlan cp;
+  plan_pooled_cs(num_sms, max_smem, n_q, ix->n, ix->dim, k, topk, cp);
   PooledWs w;
-  pooled_ws_layout(n_q, ix->dim, choose_parts(qt / (cl / 2), ct, num_sms / cl), qt * 256, k,
+  pooled_ws_layout(n_q, ix->dim, std::max(choose_parts(qt / (cl / 2), ct, num_sms / cl), cp.n_parts), qt * 256, k,
                    comm ? comm->world : 1, comm != nullptr, w,
                    topk && cl == 2 && pooled_append_sample(ix->n, k) > 0);
   return w.total;

@@ -72,6 +72,56 @@ def test_pooled_topk(H, k, kind):
         assert (i[:, 0] == gen.query_targets(12, Q, C, False) + 77).all()
 
 
+def _kernels_launched(fn):
+    """Names of the CUDA kernels fn() launches (CUPTI via torch.profiler)."""
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        out = fn()
+        torch.cuda.synchronize()
+    return out, {e.name for e in prof.events() if e.device_type.name == "CUDA"}
+
+
+@pytest.mark.parametrize("C,Q,k,dim,mode,tn", [
+    (3, 5, 7, 768, "1", None),          # one ragged chunk tile on one pair, k > n
+    (1000, 8, 10, 768, "1", None),      # 4 tiles (ragged) on 4 pairs, one query tile: two list slots
+    (5000, 300, 16, 768, "1", None),    # 2 query tiles: one list slot per (pair, query)
+    (40_123, 40, 10, 768, "2", None),   # auto selection (>= 2 tiles per pair), ragged tail
+    (39_000, 600, 1, 256, "2", None),   # 3 query tiles, dim 256: 4 resident K-blocks, 12 query stages
+    (38_500, 100, 10, 720, "2", None),  # dim % 64 != 0: zero-filled K tail in both operands
+    (5000, 300, 10, 768, "1", "256"),   # 256-chunk tiles (MMA N = 256, 128 rows per CTA, 2 stages)
+    (41_000, 513, 16, 768, "2", "240"), # 240-chunk tiles, 3 query tiles
+    (9_999, 70, 5, 768, "1", "192"),    # 192-chunk tiles
+])
+def test_pooled_chunk_stationary(H, monkeypatch, C, Q, k, dim, mode, tn):
+    """a12 on the chunk-stationary kernel (pooled_cs_sm100.cuh) vs the oracle, and bitwise vs the
+    streaming kernel (same K order of the same MMAs)."""
+    corp = gen.corpus(31, 0, C, 1, dim, kind="planted", dtype="bf16")
+    q = gen.queries(32, Q, 1, dim, corpus_seed=31, n_chunks=C, L=1, kind="planted", dtype="bf16")
+    if mode:
+        monkeypatch.setenv("HIPER_POOLED_CS", mode)
+    if tn:
+        monkeypatch.setenv("HIPER_POOLED_CS_N", tn)
+    if C == 1000:
+        monkeypatch.setenv("HIPER_POOLED_CS_A", "32")   # 32-dim query stages (64-B swizzle)
+    idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32), id_base=5, flags=H.HIPER_POOLED)
+    qd = to_dev(q)
+    (s, i), names = _kernels_launched(lambda: H.hiper_maxsim_topk(idx, qd, np.ones(Q, np.int32), k))
+    assert any("pooled_cs_sm100_kernel" in n for n in names), names
+    s, i = s.cpu().numpy(), i.cpu().numpy()
+    lay = bits(idx.layout().clone())
+    qn = oracle.norm_rows(q[:, 0])
+    S_o = oracle.maxsim_matrix(qn[:, None], np.ones(Q, np.int32), lay, np.ones(C, np.int32))
+    ids = np.arange(C, dtype=np.int64) + 5
+    for r in range(Q):
+        assert_topk_ok(s[r], i[r], S_o[r], ids, k, 1, dim, f"pooled_cs q{r}")
+    assert (i[:, 0] == gen.query_targets(32, Q, C, False) + 5).all()
+    monkeypatch.setenv("HIPER_POOLED_CS", "0")
+    (s0, i0), names0 = _kernels_launched(lambda: H.hiper_maxsim_topk(idx, qd, np.ones(Q, np.int32), k))
+    assert not any("pooled_cs_sm100_kernel" in n for n in names0)
+    s0, i0 = s0.cpu().numpy(), i0.cpu().numpy()
+    assert np.array_equal(i, i0) and np.array_equal(s.view(np.uint32), s0.view(np.uint32))
+
+
 def test_pooled_topk_append_overflow_falls_back(H, monkeypatch):
     """k > 16 on a corpus >= 32 k chunks takes the APPEND path (sample bound + candidate buffers);
     a buffer too small for the candidates must trigger the heap-path rerun, with the same answer."""
