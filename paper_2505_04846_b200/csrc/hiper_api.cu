@@ -2295,6 +2295,28 @@ extern "C" size_t hiper_coltrast_grad_workspace_size(int32_t n_q, int32_t n_d, i
   return w.total;
 }
 
+// Fork/join onto a side stream (per host thread and device): grad_q and grad_d only share their
+// inputs (G, the argmax map, the layouts), so they run concurrently.  Stream capture follows the
+// fork/join (event record + wait), so the pattern is graph-capturable.  HIPER_GRAD_FORK=0: serial.
+namespace {
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+}  // namespace
+static hiper_status side_stream(int device, SideStream** out) {
+  thread_local SideStream tab[16];
+  if (device < 0 || device >= 16) return fail(HIPER_ERR_UNSUPPORTED, "device %d", device);
+  SideStream& ss = tab[device];
+  if (!ss.s) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
+  return HIPER_OK;
+}
+
 extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     const void* q_tokens, const int32_t* q_lens, int32_t n_q, int32_t q_max_len, const void* d_tokens,
     const int32_t* d_lens, int32_t n_d, int32_t d_max_len, int32_t dim, hiper_dtype dtype,
@@ -2368,12 +2390,22 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     const int gns = std::max(2, std::min(4, (di.max_smem - 1024 - 128) / gstage));  // TMA ring depth
     const int gsm = 1024 + gns * gstage + 128;
     CUDA_TRY(set_max_smem((const void*)gqs, gsm));
-    gqs<<<(unsigned)(qblk * R), (kGqWarps + 1) * 32, gsm, stream>>>(tdg, G, amax, n_q, n_d, ld_pad,
-                                                                    qlens_dev, R, qpart, gns);
+    const char* ef = getenv("HIPER_GRAD_FORK");
+    SideStream* ss = nullptr;
+    if (!(ef && ef[0] == '0')) TRY(side_stream(di.device, &ss));
+    cudaStream_t qs = stream;
+    if (ss) {  // grad_q on the side stream, grad_d on the caller's
+      CUDA_TRY(cudaEventRecord(ss->fork, stream));
+      CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+      qs = ss->s;
+    }
+    gqs<<<(unsigned)(qblk * R), (kGqWarps + 1) * 32, gsm, qs>>>(tdg, G, amax, n_q, n_d, ld_pad,
+                                                                qlens_dev, R, qpart, gns);
     CUDA_TRY(cudaGetLastError());
-    grad_q_reduce_kernel<VPL, Tin><<<qblocks, 256, 0, stream>>>(qpart, R, n_q, (const Tin*)q_tokens,
-                                                                q_max_len, qlens_dev, an, grad_q);
+    grad_q_reduce_kernel<VPL, Tin><<<qblocks, 256, 0, qs>>>(qpart, R, n_q, (const Tin*)q_tokens,
+                                                            q_max_len, qlens_dev, an, grad_q);
     CUDA_TRY(cudaGetLastError());
+    if (ss) CUDA_TRY(cudaEventRecord(ss->join, ss->s));
     g_launches += 1;
     // grad_d: the inverted argmax map per doc (one block per doc), then one warp per segment of S
     // sorted hits, so "hub" doc rows that take most argmax hits are spread over many warps.
@@ -2394,6 +2426,7 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
         bkt, __builtin_ctz((unsigned)w.S), w.n_seg, scr, n_d, (const Tin*)d_tokens, d_max_len, dlens_dev,
         an, grad_d);
     CUDA_TRY(cudaGetLastError());
+    if (ss) CUDA_TRY(cudaStreamWaitEvent(stream, ss->join, 0));  // join: the call ends on `stream`
     g_launches += 4;
     return HIPER_OK;
   };
