@@ -2295,6 +2295,27 @@ extern "C" size_t hiper_coltrast_grad_workspace_size(int32_t n_q, int32_t n_d, i
   return w.total;
 }
 
+// Programmatic dependent launch of a plain kernel: it may start while its stream predecessor
+// drains and calls griddepcontrol.wait before touching that kernel's outputs (hides the launch gap
+// between the short N1 backward kernels).
+template <typename... KArgs, typename... Args>
+static hiper_status launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                               cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool off = getenv("HIPER_GRAD_PDL") && getenv("HIPER_GRAD_PDL")[0] == '0';  // A/B
+  cfg.numAttrs = off ? 0 : 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  return HIPER_OK;
+}
+
 // Fork/join onto a side stream (per host thread and device): grad_q and grad_d only share their
 // inputs (G, the argmax map, the layouts), so they run concurrently.  Stream capture follows the
 // fork/join (event record + wait), so the pattern is graph-capturable.  HIPER_GRAD_FORK=0: serial.
@@ -2402,9 +2423,8 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     gqs<<<(unsigned)(qblk * R), (kGqWarps + 1) * 32, gsm, qs>>>(tdg, G, amax, n_q, n_d, ld_pad,
                                                                 qlens_dev, R, qpart, gns);
     CUDA_TRY(cudaGetLastError());
-    grad_q_reduce_kernel<VPL, Tin><<<qblocks, 256, 0, qs>>>(qpart, R, n_q, (const Tin*)q_tokens,
-                                                            q_max_len, qlens_dev, an, grad_q);
-    CUDA_TRY(cudaGetLastError());
+    TRY(launch_pdl(grad_q_reduce_kernel<VPL, Tin>, qblocks, 256, 0, qs, (const float*)qpart, R, n_q,
+                   (const Tin*)q_tokens, q_max_len, (const int32_t*)qlens_dev, an, grad_q));
     if (ss) CUDA_TRY(cudaEventRecord(ss->join, ss->s));
     g_launches += 1;
     // grad_d: the inverted argmax map per doc (one block per doc), then one warp per segment of S
@@ -2412,20 +2432,18 @@ extern "C" hiper_status hiper_coltrast_scores_loss_grad(
     CUDA_TRY(set_max_smem((const void*)grad_d_sort_kernel, (int)dsmem));
     uint2* ent = (uint2*)(ws + w.ent);
     int32_t* bkt = (int32_t*)(ws + w.bucket);
-    grad_d_sort_kernel<<<(unsigned)n_d, kSortWarps * 32, dsmem, stream>>>(amax, G, n_q, n_d,
-                                                                           qlens_dev, ent, bkt);
-    CUDA_TRY(cudaGetLastError());
+    TRY(launch_pdl(grad_d_sort_kernel, (unsigned)n_d, kSortWarps * 32, dsmem, stream,
+                   (const uint8_t*)amax, (const float*)G, n_q, n_d, (const int32_t*)qlens_dev, ent, bkt));
     const int64_t sblocks = (int64_t)n_d * ((w.n_seg + 7) / 8);
     float* scr = (float*)(ws + w.scratch);
-    grad_d_seg_kernel<VPL><<<(unsigned)sblocks, 256, 0, stream>>>(n_q, qlayout, ent, bkt,
-                                                                  __builtin_ctz((unsigned)w.S), w.n_seg,
-                                                                  scr, d_max_len, grad_d);
-    CUDA_TRY(cudaGetLastError());
+    TRY(launch_pdl(grad_d_seg_kernel<VPL>, (unsigned)sblocks, 256, 0, stream, n_q,
+                   (const __nv_bfloat16*)qlayout, (const uint2*)ent, (const int32_t*)bkt,
+                   (int32_t)__builtin_ctz((unsigned)w.S), (int32_t)w.n_seg, scr, d_max_len, grad_d));
     const int64_t fwarps = (int64_t)n_d * ((d_max_len + 3) / 4);  // 4 rows per warp
-    grad_d_finish_kernel<VPL, Tin><<<(unsigned)((fwarps + 7) / 8), 256, 0, stream>>>(
-        bkt, __builtin_ctz((unsigned)w.S), w.n_seg, scr, n_d, (const Tin*)d_tokens, d_max_len, dlens_dev,
-        an, grad_d);
-    CUDA_TRY(cudaGetLastError());
+    TRY(launch_pdl(grad_d_finish_kernel<VPL, Tin>, (unsigned)((fwarps + 7) / 8), 256, 0, stream,
+                   (const int32_t*)bkt, (int32_t)__builtin_ctz((unsigned)w.S), (int32_t)w.n_seg,
+                   (const float*)scr, n_d, (const Tin*)d_tokens, d_max_len, (const int32_t*)dlens_dev,
+                   an, grad_d));
     if (ss) CUDA_TRY(cudaStreamWaitEvent(stream, ss->join, 0));  // join: the call ends on `stream`
     g_launches += 4;
     return HIPER_OK;

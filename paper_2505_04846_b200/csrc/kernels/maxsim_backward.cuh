@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(256) grad_q_reduce_kernel(const float* __restr
                                                             const int32_t* __restrict__ q_lens,
                                                             uint32_t assume_normalized,
                                                             float* __restrict__ grad_q) {
+  ptx::grid_dependency_wait();  // PDL: launched early, waits for its predecessor here
   constexpr int D = VPL * 32;
   const uint32_t lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -230,6 +231,7 @@ constexpr int kSortWarps = 16;
 __global__ void __launch_bounds__(kSortWarps * 32) grad_d_sort_kernel(
     const uint8_t* __restrict__ amax, const float* __restrict__ G, int32_t B, int32_t M,
     const int32_t* __restrict__ q_lens, uint2* __restrict__ ent, int32_t* __restrict__ base_out) {
+  ptx::grid_dependency_wait();  // PDL: launched early, waits for its predecessor here
   constexpr int NB = 257;  // 256 buckets + 1 for padding entries (t >= len_q)
   constexpr int NW = kSortWarps;
   extern __shared__ uint8_t smem[];
@@ -377,6 +379,7 @@ __global__ void __launch_bounds__(256, 2) grad_d_seg_kernel(
     int32_t B, const __nv_bfloat16* __restrict__ qlay, const uint2* __restrict__ ent,
     const int32_t* __restrict__ base, int32_t log2S, int32_t n_seg, float* __restrict__ scratch,
     int32_t d_max_len, float* __restrict__ grad_d) {
+  ptx::grid_dependency_wait();  // PDL: launched early, waits for its predecessor here
   constexpr int D = VPL * 32;
   constexpr int NB = 257;
   constexpr int R = 32;  // rows in flight
@@ -451,6 +454,7 @@ __global__ void __launch_bounds__(256) grad_d_finish_kernel(
     const int32_t* __restrict__ base, int32_t log2S, int32_t n_seg, const float* __restrict__ scratch,
     int32_t M, const Tin* __restrict__ xd, int32_t d_max_len, const int32_t* __restrict__ d_lens,
     uint32_t assume_normalized, float* __restrict__ grad_d) {
+  ptx::grid_dependency_wait();  // PDL: launched early, waits for its predecessor here
   constexpr int D = VPL * 32;
   constexpr int NB = 257;
   constexpr int FR = 4;
