@@ -117,6 +117,30 @@ def main():
             print(f"two-stage rank{r}: equal to 1-GPU bitwise {same}", flush=True)
             ok &= same
     del pidx, tidx
+    # ---- the same with the LAST rank holding an empty shard (advisor round 1): it still takes part in
+    # both all-gathers, and every rank gets the answer over the other ranks' chunks
+    Ce = 1500
+    ce0, ce1 = H.hiper_shard_range(Ce, world - 1, rank) if rank < world - 1 else (Ce, Ce)
+    tle = gen.lengths(81, Ce, Lt, True)
+    pidx = H.hiper_index_build(to_dev16(gen.corpus(82, ce0, ce1 - ce0, 1, dp)), np.ones(ce1 - ce0, np.int32),
+                               id_base=ce0, flags=H.HIPER_POOLED)
+    tidx = H.hiper_index_build(to_dev16(gen.corpus(81, ce0, ce1 - ce0, Lt, d)), tle[ce0:ce1], id_base=ce0)
+    s2, i2 = H.hiper_two_stage_topk(pidx, tidx, to_dev16(qp2), to_dev16(qt2), ql2, k1, k, comm=comm)
+    torch.cuda.synchronize()
+    gs = [torch.empty_like(s2) for _ in range(world)]
+    gi = [torch.empty_like(i2) for _ in range(world)]
+    dist.all_gather(gs, s2)
+    dist.all_gather(gi, i2)
+    if rank == 0:
+        fp = H.hiper_index_build(to_dev16(gen.corpus(82, 0, Ce, 1, dp)), np.ones(Ce, np.int32),
+                                flags=H.HIPER_POOLED)
+        ft = H.hiper_index_build(to_dev16(gen.corpus(81, 0, Ce, Lt, d)), tle)
+        fs, fi = H.hiper_two_stage_topk(fp, ft, to_dev16(qp2), to_dev16(qt2), ql2, k1, k)
+        for r in range(world):
+            same = torch.equal(gi[r], fi) and torch.equal(gs[r].view(torch.int32), fs.view(torch.int32))
+            print(f"two-stage, empty last shard, rank{r}: equal to 1-GPU bitwise {same}", flush=True)
+            ok &= same
+    del pidx, tidx
     # ---- NEXT N2: full ColTrast loss with the gathered pooled candidates (min(N, W) rule)
     import oracle
     b, dp, Lc = 24, 768, 128

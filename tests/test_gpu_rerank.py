@@ -85,3 +85,19 @@ def test_two_stage_packed_token_index_bitwise(H):
     assert np.array_equal(i1, i0)
     assert np.array_equal(s1.view(np.uint32), s0.view(np.uint32))
     assert (i0[:, 0] >= 7).all()
+
+
+@pytest.mark.parametrize("k1", [16, 100])
+def test_two_stage_empty_index(H, k1):
+    """An empty shard (no chunks): both stages return padding (ids -1, scores -inf), and the stage-2
+    kernel is never launched over an empty token index (advisor round 1)."""
+    n_q, Lq, d, dp, k = 4, 32, 128, 768, 10
+    pidx = H.hiper_index_build(torch.empty((0, 1, dp), dtype=torch.bfloat16, device="cuda"), [],
+                               flags=H.HIPER_POOLED)
+    tidx = H.hiper_index_build(torch.empty((0, 64, d), dtype=torch.bfloat16, device="cuda"), [])
+    qt = gen.queries(95, n_q, Lq, d, corpus_seed=95, n_chunks=10, L=64)
+    qp = gen.queries(96, n_q, 1, dp, corpus_seed=96, n_chunks=10, L=1)
+    ql = gen.lengths(95, n_q, Lq, True, stream=gen.QLEN)
+    s, i = H.hiper_two_stage_topk(pidx, tidx, to_dev(qp), to_dev(qt), ql, k1, k)
+    torch.cuda.synchronize()
+    assert (i.cpu().numpy() == -1).all() and np.isneginf(s.cpu().numpy()).all()
