@@ -929,6 +929,8 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
   cfg.numAttrs = 2;
   unsigned long long* st = nullptr;
   MaxsimArgs b = a;
+  static const bool late = getenv("HIPER_LATE_RELEASE") && getenv("HIPER_LATE_RELEASE")[0] == '1';
+  b.late_release = late ? 1 : 0;
   if (stats_on) {
     CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));

@@ -340,11 +340,18 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           // build, pack_pad_replicate_kernel), and a repeated column cannot change a maximum, so the
           // group max is the max over the chunk's real columns (reading R2) with no tail re-reads.
           float m16[16];
+          bool released = false;  // early release after the last TMEM load (see the dense path)
 #pragma unroll
           for (int blk = 0; blk < 4; ++blk) {
             if (blk * 4 < n_grp) {
               uint32_t v[64];
               tmem_ld64_wait(taddr_base + (uint32_t)(blk * 64), v);
+              if (blk == ((n_grp - 1) >> 2) && !args.late_release) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader);
+                released = true;
+              }
 #pragma unroll
               for (int gg = 0; gg < 4; ++gg) {
                 float a0 = fmaxf(__uint_as_float(v[gg * 16]), __uint_as_float(v[gg * 16 + 1]));
@@ -358,9 +365,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               for (int gg = 0; gg < 4; ++gg) m16[blk * 4 + gg] = -INFINITY;
             }
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader);  // TMEM drained: release the accumulator
+          if (!released) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader);  // TMEM drained: release the accumulator
+          }
           if (STATS && args.stats) {
             st_drain_g += clock64() - e1;
             ++st_tiles_g;
@@ -435,10 +444,21 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           // real columns of this half (H = 1: the chunk's length)
           const int32_t lh = H == 1 ? ld : min(max(ld - 256 * h, 0), 256);
           const uint32_t taddr = H == 1 ? taddr_base : lanes + (uint32_t)h * kAccStride;
+          // early release: the accumulator goes back to the MMA as soon as its last block is in
+          // registers, before that block's arithmetic (the release is on the MMA's critical path:
+          // commit -> epilogue wake -> drain -> arrive -> MMA wake; args.late_release: A/B only)
+          bool released = false;
+          const uint32_t rel_bar = H == 1 ? tempty_leader : mapa_shared(bar_tempty(h), 0);
           for (int32_t col = 0; col < ((DBG == 1 || DBG == 2 || DBG == 4) ? 0 : lh); col += 64) {
             uint32_t v[64];
             tmem_ld64_wait(taddr + (uint32_t)col, v);
             const int rem = lh - col;
+            if (rem <= 64 && !args.late_release) {  // warp-uniform: the chunk's length
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(rel_bar);
+              released = true;
+            }
             if constexpr (MODE == 2) {
               max64_arg1(v, m4[0], ix4[0], col, rem);  // chains 1..3 stay at -inf
             } else {
@@ -446,9 +466,11 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
               else max64_masked(v, m4, rem);
             }
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(H == 1 ? tempty_leader : mapa_shared(bar_tempty(h), 0));
+          if (!released) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(rel_bar);
+          }
           if (STATS && args.stats) {
             st_drain_g += clock64() - e1;
             ++st_tiles_g;
