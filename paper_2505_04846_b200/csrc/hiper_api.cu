@@ -1279,6 +1279,7 @@ extern "C" hiper_status hiper_workspace_status(const void* workspace, hiper_stre
 // One vector per query and per chunk: S = <NORM(q), NORM(c)> via the K-pipelined pair GEMM with a
 // fused per-query register top-k (kernels/pooled_sm100_pair.cuh).
 constexpr int kPooledKP = 16;  // register top-k slots per query thread (k <= 16; larger k: warp lists)
+constexpr int kPooledKP8 = 8;  // the short register list (k <= 8)
 
 struct PooledPlan {
   int32_t n_qtiles = 0, n_ctiles = 0, n_parts = 0, n_stages = 0, q_pad = 0;
@@ -1331,6 +1332,13 @@ static hiper_status launch_pooled(const PooledPlan& pp, const CUtensorMap& tq, c
   auto kern = pp.cl == 4 ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 4>
               : pstats_on ? pooled_sm100_pair_kernel<MODE, kPooledKP, 0, 2, true>
                           : pooled_sm100_pair_kernel<MODE, kPooledKP, 0>;
+  // k <= 8 (and the APPEND sample pre-pass): an 8-slot register list, half the work per insertion
+  if constexpr (MODE == 1) {
+    static const bool kp8_off = getenv("HIPER_POOLED_KP8") && getenv("HIPER_POOLED_KP8")[0] == '0';  // A/B
+    if (pp.cl == 2 && a.k <= kPooledKP8 && !kp8_off)
+      kern = pstats_on ? pooled_sm100_pair_kernel<MODE, kPooledKP8, 0, 2, true>
+                       : pooled_sm100_pair_kernel<MODE, kPooledKP8, 0>;
+  }
   if (MODE == 1 && a.k > kPooledKP) {  // shared-memory heaps, or the APPEND candidate buffers
     if (pp.cl != 2) return fail(HIPER_ERR_UNSUPPORTED, "pooled k > %d with HIPER_POOLED_MC", kPooledKP);
     if (a.cand != nullptr)
@@ -1601,8 +1609,15 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
     TRY(make_tmap(&tq, qlayout, n_q, dim, 128));
     PooledPlan p0;
     TRY(plan_pooled(di, n_q, sample, p0, true, kPooledKP));
+    // each (partition, group) list keeps its sub-sample's top kp0: any k-th largest key of the union
+    // of real keys is a valid bound once the union holds >= k keys (2 P kp0 >= k), and it equals the
+    // sample's own k-th unless one list holds more than kp0 of the sample's top k (expected k / 2P
+    // per list).  A short list pays ~kp0 (1 + ln(n / kp0)) insertions instead of 16 (1 + ln(n / 16)).
+    const int32_t per = (k + 2 * p0.n_parts - 1) / std::max(1, 2 * p0.n_parts);
+    int32_t kp0 = std::min(kPooledKP, std::max(4, 3 * per));
+    if (const char* e = getenv("HIPER_PREPASS_KP")) kp0 = std::min(kPooledKP, std::max(per, atoi(e)));  // A/B
     PooledArgs a0 = a;
-    a0.k = kPooledKP;
+    a0.k = kp0;
     a0.n_ctiles = p0.n_ctiles;
     a0.n_parts = p0.n_parts;
     a0.n_stages = p0.n_stages;
@@ -1611,8 +1626,8 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
     a0.pub8 = nullptr;
     TRY(launch_pooled<1>(p0, tq, ix->tmap, a0, stream));
     uint64_t* thrk = (uint64_t*)(ws + w.thrk);
-    TRY(launch_merge(partial, p0.n_parts * kEpiGroups, (int64_t)p0.q_pad * kPooledKP, n_q, kPooledKP, k,
-                     thrk, nullptr, nullptr, stream, kPooledKP));
+    TRY(launch_merge(partial, p0.n_parts * kEpiGroups, (int64_t)p0.q_pad * kp0, n_q, kp0, k,
+                     thrk, nullptr, nullptr, stream, kp0));
     // (2) the whole corpus: every key >= T_q into the query's candidate buffer
     PooledPlan p1;
     TRY(plan_pooled(di, n_q, ix->n, p1, true, k, /*append=*/true));
