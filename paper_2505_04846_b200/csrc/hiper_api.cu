@@ -1590,8 +1590,14 @@ static hiper_status pooled_search(const hiper_index* ix, const void* q_tokens, h
   a.partial = partial;
   a.scores = dense_scores;
   a.score_ld = ix->n;
-  a.progress = getenv("HIPER_NO_LOCKSTEP") == nullptr ? (uint32_t*)(ws + w.progress) : nullptr;
+  // The L2 lockstep pays off for the token MaxSim kernel under the power cap (less DRAM, higher
+  // clocks), not here: the pooled kernel's feed is latency-bound, and without it config 5 runs 2.6%
+  // faster in a burst and 1% faster sustained (profiles/r02/ablation/pooled_lockstep.txt).
+  // HIPER_POOLED_LOCKSTEP=1 turns it on.
+  a.progress = (getenv("HIPER_POOLED_LOCKSTEP") && getenv("HIPER_POOLED_LOCKSTEP")[0] == '1')
+                   ? (uint32_t*)(ws + w.progress) : nullptr;
   a.window = 16;
+  if (const char* e = getenv("HIPER_POOLED_WINDOW")) a.window = std::max(1, atoi(e));  // ablation
   if (!dense_scores && getenv("HIPER_NO_SHARED_BOUND") == nullptr) {
     a.gthr = (unsigned long long*)(ws + w.gthr);
     CUDA_TRY(cudaMemsetAsync(a.gthr, 0, (size_t)pp.q_pad * 8, stream));
