@@ -931,6 +931,14 @@ static hiper_status launch_maxsim_t(const KernelPlan& kp, const CUtensorMap& tq,
   MaxsimArgs b = a;
   static const bool late = getenv("HIPER_LATE_RELEASE") && getenv("HIPER_LATE_RELEASE")[0] == '1';
   b.late_release = late ? 1 : 0;
+  static const int32_t ls_every = [] {  // lockstep publish / check interval in chunks (ablation knob)
+    const char* e = getenv("HIPER_LOCKSTEP_EVERY");
+    int v = e ? atoi(e) : 256;  // 16 -> 256: +2-3% at config 3 (ablation/lockstep_r02.txt)
+    int p = 1;
+    while (p < v && p < 1024) p <<= 1;
+    return p;
+  }();
+  b.ls_mask = ls_every - 1;
   if (stats_on) {
     CUDA_TRY(cudaMalloc(&st, 8 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemsetAsync(st, 0, 8 * sizeof(unsigned long long), stream));

@@ -66,6 +66,7 @@ struct MaxsimArgs {
   // padding rows of a chunk's last 16-row group repeat its last real row (no column masking).
   const uint32_t* recs;
   unsigned long long* stats;  // HIPER_PIPE_STATS diagnostics (see pooled_sm100_pair.cuh), or nullptr
+  int32_t ls_mask;            // L2 lockstep: publish / check every ls_mask + 1 chunks (a power of two)
   int32_t late_release;       // A/B only (HIPER_LATE_RELEASE=1): release the accumulator after the
                               // drain's arithmetic instead of after its last TMEM load
 };

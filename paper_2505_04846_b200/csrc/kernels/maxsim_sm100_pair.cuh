@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
           brow = (int32_t)(c * args.ld_pad + (int64_t)rank * (half_n(0) >> 1));
         }
         if (lane == 0) {
-          if (args.progress != nullptr && rank == 0 && ((c - c0) & 15) == 0) {
+          if (args.progress != nullptr && rank == 0 && ((c - c0) & args.ls_mask) == 0) {
             const uint32_t pos = streamed + (uint32_t)(c - c0);
             lockstep_publish(args.progress, pair, pos);
             lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
