@@ -54,6 +54,23 @@ __device__ __forceinline__ void lockstep_wait(const uint32_t* progress, uint32_t
   }
 }
 
+// The same wait by a whole warp: lane l scans the words l, l + 32, ... and the minimum is a butterfly,
+// so one check costs ~one L2 round trip instead of n_pairs dependent-issue loads by one thread.
+__device__ __forceinline__ void lockstep_wait_warp(const uint32_t* progress, uint32_t n_pairs, uint32_t pos,
+                                                   uint32_t window, uint32_t lane) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t mn = 0xFFFFFFFFu;
+    for (uint32_t j = lane; j < n_pairs; j += 32)
+      mn = min(mn, *reinterpret_cast<const volatile uint32_t*>(progress + j));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((uint64_t)pos <= (uint64_t)mn + window) return;
+    __nanosleep(200);
+    if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) ptx::hiper_watchdog_fail("lockstep", pos, mn);
+  }
+}
+
 // PACKED (N4): the slots are the tiles of a length-bucketed packed corpus (MaxsimArgs::recs): the MMA
 // N is the tile's n_rows, and the epilogue reduces each chunk over its own column segment.
 // STATS: HIPER_PIPE_STATS instrumentation compiled in (diagnostics builds only; the production
@@ -183,12 +200,12 @@ __global__ void __launch_bounds__(kMaxsimThreads, 1)
         } else {
           brow = (int32_t)(c * args.ld_pad + (int64_t)rank * (half_n(0) >> 1));
         }
+        if (args.progress != nullptr && rank == 0 && ((c - c0) & args.ls_mask) == 0) {  // warp-uniform
+          const uint32_t pos = streamed + (uint32_t)(c - c0);
+          if (lane == 0) lockstep_publish(args.progress, pair, pos);
+          lockstep_wait_warp(args.progress, n_pairs, pos, (uint32_t)args.window, lane);
+        }
         if (lane == 0) {
-          if (args.progress != nullptr && rank == 0 && ((c - c0) & args.ls_mask) == 0) {
-            const uint32_t pos = streamed + (uint32_t)(c - c0);
-            lockstep_publish(args.progress, pair, pos);
-            lockstep_wait(args.progress, n_pairs, pos, (uint32_t)args.window);
-          }
 #pragma unroll
           for (int h = 0; h < H; ++h) {
             // one stage = this CTA's rows of one whole chunk (half), all K-blocks

@@ -2,7 +2,7 @@
 set -x
 python __graft_entry__.py > gpurun_out/build.log 2>&1 || exit 1
 for i in 1 2; do
-  for E in 16 256 512 1024; do
+  for E in 256 16 64; do
     HIPER_LOCKSTEP_EVERY=$E timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/lse_${E}_$i.json 2>/dev/null
   done
 done
