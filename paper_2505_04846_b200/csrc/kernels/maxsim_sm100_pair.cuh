@@ -45,9 +45,17 @@ __device__ __forceinline__ void lockstep_wait(const uint32_t* progress, uint32_t
                                               uint32_t window) {
   const long long t0 = clock64();
   while (true) {
+    // 16 independent loads in flight per round (a plain loop waits out each load's L2 latency in
+    // turn: ~n_pairs round trips per check)
     uint32_t mn = 0xFFFFFFFFu;
-    for (uint32_t j = 0; j < n_pairs; ++j)
-      mn = min(mn, *reinterpret_cast<const volatile uint32_t*>(progress + j));
+    for (uint32_t j0 = 0; j0 < n_pairs; j0 += 16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        v[q] = j0 + q < n_pairs ? *reinterpret_cast<const volatile uint32_t*>(progress + j0 + q) : 0xFFFFFFFFu;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) mn = min(mn, v[q]);
+    }
     if ((uint64_t)pos <= (uint64_t)mn + window) return;
     __nanosleep(200);
     if (clock64() - t0 > HIPER_WATCHDOG_CYCLES) ptx::hiper_watchdog_fail("lockstep", pos, mn);
