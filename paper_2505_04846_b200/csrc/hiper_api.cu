@@ -2354,6 +2354,12 @@ namespace {
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  ~SideStream() {  // at host-thread exit (errors ignored: the context may already be gone)
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (s) cudaStreamDestroy(s);
+    cudaGetLastError();
+  }
 };
 }  // namespace
 static hiper_status side_stream(int device, SideStream** out) {
