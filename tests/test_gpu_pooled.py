@@ -122,6 +122,26 @@ def test_pooled_chunk_stationary(H, monkeypatch, C, Q, k, dim, mode, tn):
     assert np.array_equal(i, i0) and np.array_equal(s.view(np.uint32), s0.view(np.uint32))
 
 
+@pytest.mark.parametrize("k", [1, 8, 9])
+def test_pooled_short_register_list(H, k):
+    """k <= 8 runs the 8-slot register-list instantiation (k = 9: the 16-slot one), checked by the
+    kernel names CUPTI records; both against the oracle's exact top-k."""
+    C, Q = 7000, 260
+    corp, q = case(C, Q, kind="iid")
+    idx = H.hiper_index_build(to_dev(corp), np.ones(C, np.int32), id_base=3, flags=H.HIPER_POOLED)
+    qd = to_dev(q)
+    (s, i), names = _kernels_launched(lambda: H.hiper_maxsim_topk(idx, qd, np.ones(Q, np.int32), k))
+    want = "pooled_sm100_pair_kernel<1, 8," if k <= 8 else "pooled_sm100_pair_kernel<1, 16,"
+    assert any(want in n for n in names), names
+    s, i = s.cpu().numpy(), i.cpu().numpy()
+    lay = bits(idx.layout().clone())
+    S_o = oracle.maxsim_matrix(oracle.norm_rows(q[:, 0])[:, None], np.ones(Q, np.int32), lay,
+                               np.ones(C, np.int32))
+    ids = np.arange(C, dtype=np.int64) + 3
+    for r in range(Q):
+        assert_topk_ok(s[r], i[r], S_o[r], ids, k, 1, D, f"pooled k={k} q{r}")
+
+
 def test_pooled_topk_append_overflow_falls_back(H, monkeypatch):
     """k > 16 on a corpus >= 32 k chunks takes the APPEND path (sample bound + candidate buffers);
     a buffer too small for the candidates must trigger the heap-path rerun, with the same answer."""
